@@ -1,0 +1,450 @@
+#!/usr/bin/env python
+"""MoE dispatch+combine benchmark (BASELINE.json metric: us/layer).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...
+
+Workload (configs[1], Mixtral-8x7B MoE layer, bf16): T = 4096 tokens per
+node group, hidden 4096, E = 8 experts, top-2.  One card per GPU; the node
+topology grows with N (weak scaling: every GPU routes and exchanges one node
+group's 4096 tokens):  N=1 -> 1x1, N=2 -> 2x1 (EP only), N=4 -> 2x2,
+N=8 -> 2x4 (EP=2 x TP=4).  A step is one layer: route (top-k gate) ->
+dispatch (index, count exchange, fused permute+AllToAll, AllGather) ->
+combine (reverse AllToAll, weighted un-permute + output AllGather), with
+identity experts.  Level/chunks: the MoNTA planner's choice for t >= 2,
+Baseline (naive AllToAll) for t == 1; the naive TP-redundant exchange is
+timed alongside.
+
+Timing: W warm-up steps; K timed steps, each bracketed by CUDA events on the
+launching stream after an L2 flush (256 MiB memset) and a cross-rank barrier
+(both outside the events); value = sum over steps, max over ranks.  e2e is
+the same step through the C ABI host-buffer call (moe_ctx_forward_host: H2D
+of x/logits from pinned memory, the layer, D2H of the output).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIG = {"workload": "mixtral-8x7b-moe-layer", "tokens_per_node": 4096, "hidden": 4096, "experts": 8,
+          "top_k": 2, "dtype": "bf16", "logits": "f32"}
+TOPOLOGY = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}
+METRIC = "moe_dispatch_combine_us_per_layer"
+L2_FLUSH_BYTES = 256 << 20
+
+
+def topo_for(n: int):
+    if n in TOPOLOGY:
+        return TOPOLOGY[n]
+    return (n, 1)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.file = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.proc = None
+
+    def __enter__(self):
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.file, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc:
+            time.sleep(0.2)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        self.file.flush()
+        self.file.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.file.read().splitlines():
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def interval_union(iv):
+    iv = sorted(iv)
+    out = []
+    for a, b in iv:
+        if out and a <= out[-1][1]:
+            out[-1][1] = max(out[-1][1], b)
+        else:
+            out.append([a, b])
+    return out
+
+
+def exposed(aa, other):
+    """Length of union(aa) not covered by union(other)."""
+    A, O = interval_union(aa), interval_union(other)
+    tot = 0.0
+    for a, b in A:
+        cov = 0.0
+        for c, d in O:
+            lo, hi = max(a, c), min(b, d)
+            if hi > lo:
+                cov += hi - lo
+        tot += (b - a) - cov
+    return tot
+
+
+# ---------------------------------------------------------------------------
+def cpu_port_sample(e, t, E, k, T, h, tokens_sample, seed=0):
+    """The oracle port (C restatement of the reference data plane) on a bounded
+    sample of the workload, single-threaded; returns us/layer scaled to T."""
+    import numpy as np
+    import oracle
+    rng = np.random.default_rng(seed)
+    Ts = tokens_sample
+    x = rng.standard_normal((e, Ts, h)).astype(np.float32)
+    xb = x.view(np.uint32)
+    bf = (xb >> 16).astype(np.uint16)  # bf16 bit patterns
+    xbytes = bf.view(np.uint8).reshape(e, Ts, h * 2)
+    logits = rng.standard_normal((e, Ts, E))
+    t0 = time.perf_counter()
+    experts = np.zeros((e, Ts, k), np.int32)
+    probs = np.zeros((e, Ts, k), np.float64)
+    for g in range(e):
+        experts[g], probs[g] = oracle.route_topk(logits[g], k)
+    nodes = oracle.Nodes(e, t, E, xbytes, experts)
+    if t > 1:
+        fin, _ = nodes.dispatch_chunked(oracle.O1, 1, 2)
+    else:
+        fin = nodes.dispatch_monolithic()
+    nodes.combine(oracle.BF16, fin, probs)
+    dt = time.perf_counter() - t0
+    return dt * 1e6 * (T / Ts), dt
+
+
+def run_reference(args):
+    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    e, t = topo_for(args.gpus)
+    T, h, E, k = CONFIG["tokens_per_node"], CONFIG["hidden"], CONFIG["experts"], CONFIG["top_k"]
+    sample = args.ref_sample_tokens
+    vals = []
+    for _ in range(max(1, args.warmup)):
+        cpu_port_sample(e, t, E, k, T, h, sample)
+    for s in range(max(1, args.steps)):
+        us, _ = cpu_port_sample(e, t, E, k, T, h, sample, seed=s)
+        vals.append(us)
+    v = statistics.mean(vals)
+    line = {"metric": METRIC, "value": v, "unit": "us/layer", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "impl": "reference",
+            "config": dict(CONFIG, topology=f"{e}x{t}", level="O1" if t > 1 else "Baseline"),
+            "cpu_baseline": {"value": v, "unit": "us/layer", "cores": 1, "kind": "port",
+                             "sample": f"{sample} of {T} tokens per node x {e} nodes, scaled linearly; "
+                                       f"oracle/moe_oracle.c (C restatement of dataplane.hpp, E>e generalised)"},
+            "e2e": {"value": v, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--level", default="auto", help="auto|baseline|o1|o2|o3")
+    ap.add_argument("--chunks", type=int, default=0)
+    ap.add_argument("--landing", default="final", choices=["final", "staged"])
+    ap.add_argument("--ref-sample-tokens", type=int, default=512)
+    ap.add_argument("--cpu-sample-tokens", type=int, default=256)
+    ap.add_argument("--quick", action="store_true", help="skip naive/e2e/cpu extras (profiling runs)")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2411_00662_b200 import _lib, planner as P
+    from paper_2411_00662_b200.layer import MoeLayer, BASELINE, O1, O2, O3, LAND_FINAL, LAND_STAGED
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    e, t = topo_for(world)
+    T, h, E, k = CONFIG["tokens_per_node"], CONFIG["hidden"], CONFIG["experts"], CONFIG["top_k"]
+    node, rho = rank // t, rank % t
+
+    # ---- level / chunk count: MoNTA planner on the B200 NVLink curves
+    levels = {"baseline": BASELINE, "o1": O1, "o2": O2, "o3": O3}
+    curves_dir = os.path.join(ROOT, "profiles", "curves_b200")
+    decision = None
+    if args.level != "auto":
+        level = levels[args.level]
+        n = args.chunks or (1 if level in (BASELINE, O1) else 4)
+    elif t == 1:
+        level, n = BASELINE, 1
+    else:
+        try:
+            curves = P.load_curve_set(curves_dir)
+            ov = P.OverheadModel(**json.load(open(os.path.join(curves_dir, "overhead.json"))))
+        except Exception:
+            curves = P.CurveSet(P.EfficiencyCurve.constant(0.8), P.EfficiencyCurve.constant(0.8),
+                                P.EfficiencyCurve.constant(0.8))
+            ov = P.OverheadModel(8e-6, 4e-6)
+        model = P.ModelSpec(b=1, s=T * k, h=h, k=k, bpe=2)  # routed rows: s_eff = T*k
+        decision = P.select_strategy(model, P.ParallelSpec(t=t, e=e), P.b200_cluster(e, t), curves, ov, n_cap=16)
+        level, n = int(decision.level), decision.n
+        while T % n:
+            n -= 1
+    landing = LAND_STAGED if args.landing == "staged" else LAND_FINAL
+
+    layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, logit_dtype=torch.float32, max_chunks=16,
+                     device=local, rank=rank if world > 1 else 0, world_size=world)
+    layer.connect()
+    cd = layer.cards[0]
+    gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + node)
+    x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(torch.bfloat16)
+    l0 = torch.randn(T, E, generator=gen, device=f"cuda:{local}")
+    cd.x.copy_(x0)
+    cd.logits.copy_(l0)
+    flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
+    stream = torch.cuda.current_stream()
+    bar = torch.zeros(1, device=f"cuda:{local}")
+
+    def barrier():
+        if world > 1:
+            dist.all_reduce(bar)
+
+    def timed(step_fn, steps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        for a, b in evs:
+            flush.zero_()
+            barrier()
+            a.record(stream)
+            step_fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        torch.cuda.synchronize()
+        ms = [a.elapsed_time(b) for a, b in evs]
+        total = torch.tensor([sum(ms)], dtype=torch.float64, device=f"cuda:{local}")
+        if world > 1:
+            dist.all_reduce(total, op=dist.ReduceOp.MAX)
+        return float(total.item()), ms
+
+    def step(lv=level, nn=n):
+        layer.forward(lv, nn, landing, stream)
+
+    for _ in range(args.warmup):
+        step()
+    layer.sync()
+    launches0 = layer.launch_count
+    with ClockSampler(local) as clk:
+        total_ms, per = timed(step, args.steps)
+    launches = layer.launch_count - launches0
+    layer.sync()
+    us = total_ms * 1e3 / args.steps
+
+    # ---- per-kernel spans (separate pass, events per launch on its stream)
+    layer.enable_timing(True)
+    span_sets = []
+    for _ in range(3):
+        flush.zero_()
+        barrier()
+        step()
+        span_sets.append(layer.spans())
+    layer.enable_timing(False)
+    layer.sync()
+
+    def stage_stats(spans_list):
+        out = {}
+        for spans in spans_list:
+            for st, j, a, b in spans:
+                out.setdefault(st, []).append(b - a)
+        return {s: {"launches_per_step": len(v) // len(spans_list), "avg_us": 1e3 * sum(v) / len(v),
+                    "sum_us_per_step": 1e3 * sum(v) / len(spans_list)} for s, v in out.items()}
+
+    def exposed_aa(spans_list):
+        vals = []
+        for spans in spans_list:
+            aa = [(a, b) for st, j, a, b in spans if st == "aa"]
+            oth = [(a, b) for st, j, a, b in spans if st in ("ag", "d2d")]
+            caa = [(a, b) for st, j, a, b in spans if st == "caa"]
+            unp = [(a, b) for st, j, a, b in spans if st == "unpermute"]
+            vals.append(exposed(aa, oth) + exposed(caa, unp))
+        return 1e3 * statistics.mean(vals)
+
+    stages = stage_stats(span_sets)
+    exp_aa = exposed_aa(span_sets)
+
+    # ---- naive TP-redundant exchange at the same N (for the headline ratio)
+    naive = None
+    if not args.quick and level != BASELINE:
+        for _ in range(3):
+            step(BASELINE, 1)
+        layer.sync()
+        ntot, _ = timed(lambda: step(BASELINE, 1), args.steps)
+        layer.enable_timing(True)
+        nspans = []
+        for _ in range(3):
+            flush.zero_()
+            barrier()
+            step(BASELINE, 1)
+            nspans.append(layer.spans())
+        layer.enable_timing(False)
+        layer.sync()
+        naive = {"us_per_layer": ntot * 1e3 / args.steps, "exposed_alltoall_us": exposed_aa(nspans),
+                 "stages": stage_stats(nspans)}
+
+    # ---- e2e through the C ABI with host buffers
+    e2e = None
+    if not args.quick:
+        hx = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+        hl = torch.empty(T, E, dtype=torch.float32).pin_memory()
+        ho = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+        hx.copy_(x0.cpu())
+        hl.copy_(l0.cpu())
+
+        def host_step():
+            layer.forward_host(hx, hl, ho, level, n, landing, stream)
+
+        for _ in range(3):
+            host_step()
+        torch.cuda.synchronize()
+        etot, _ = timed(host_step, args.steps)
+        layer.sync()
+        e2e = {"value": etot * 1e3 / args.steps, "unit": "us/layer",
+               "h2d_bytes_per_step": hx.numel() * 2 + hl.numel() * 4, "d2h_bytes_per_step": ho.numel() * 2}
+
+    # ---- correctness spot check of the timed configuration (identity experts)
+    layer.forward(level, n, landing, stream)
+    layer.sync()
+    psum = cd.probs.double().sum(1, keepdim=True)
+    err = ((cd.out.double() - x0.double() * psum).abs().max() / x0.double().abs().max()).item()
+
+    # ---- roofline of the dominant kernel (HBM-bound: algorithmic bytes / live duration)
+    peak, peak_kind = load_peaks()
+    R = T * k
+    row = h * 2
+    Rdst = layer.recv_rows(cd.card)
+    # algorithmic bytes per launch
+    if world == 1:
+        aa_bytes = 2 * R * row + 16 * R + 4 * R
+    else:
+        aa_bytes = None  # NVLink-bound: reported under "nvlink"
+    unp_cols = h // t if (level != BASELINE and t > 1) else h
+    unp_bytes = R * unp_cols * 2 + T * unp_cols * 2 * (t if (level != BASELINE and t > 1) else 1) + 12 * R
+    kern = {}
+    if "aa" in stages and aa_bytes:
+        kern["fused_permute_aa"] = (aa_bytes * stages["aa"]["launches_per_step"] / max(stages["aa"]["sum_us_per_step"], 1e-9)) / 1e3
+    if "unpermute" in stages:
+        kern["unpermute_combine"] = (unp_bytes / max(stages["unpermute"]["sum_us_per_step"], 1e-9)) / 1e3
+    dom = max(((s, v["sum_us_per_step"]) for s, v in stages.items() if s in ("aa", "unpermute")),
+              key=lambda z: z[1], default=("unpermute", 1.0))[0]
+    if dom == "aa" and aa_bytes:
+        ach = kern["fused_permute_aa"]
+        traffic_alg = aa_bytes
+        dom_name = "fused_permute_aa (k_seg_copy<16>)"
+    else:
+        ach = kern.get("unpermute_combine", 0.0)
+        traffic_alg = unp_bytes
+        dom_name = "unpermute_combine (k_unpermute<bf16,f32,bf16,f32,8>)"
+    ncu_traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
+            ncu_traffic = json.load(f).get(dom_name.split(" ")[0])
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": dom_name, "achieved": ach, "peak": peak, "unit": "GB/s",
+                "frac": ach / peak, "traffic": ncu_traffic, "algorithmic_bytes_per_launch": traffic_alg,
+                "peak_kind": peak_kind, "kernels_gbs": kern}
+
+    # NVLink: bytes this card pushed to peers per step / time of the exchange kernels
+    nvlink = None
+    if world > 1:
+        nvlink = {"note": "bytes stored to peer GPUs per step / sum of exchange-kernel time",
+                  "recv_rows": Rdst}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.quick:
+        cpu_us, secs = cpu_port_sample(e, t, E, k, T, h, args.cpu_sample_tokens)
+        cpu = {"value": cpu_us, "unit": "us/layer", "cores": 1, "kind": "port",
+               "sample": f"{args.cpu_sample_tokens} of {T} tokens ({secs:.2f} s CPU), scaled linearly; "
+                         f"oracle/moe_oracle.c route+permute+dispatch+combine, 1 thread of {os.cpu_count()}"}
+
+    line = {"metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn x, randn f32 gate logits)",
+            "config": dict(CONFIG, topology=f"{e}x{t}", level=_lib.LEVEL_NAMES[level], chunks=n,
+                           landing=args.landing, parallelism=f"ep{e}xtp{t}",
+                           l2="flushed between steps (256 MiB memset outside the events)",
+                           planner=None if decision is None else
+                           {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
+                            "t_pred_us": decision.t_pred * 1e6}),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk.summary(), "stages": stages, "exposed_alltoall_us": exp_aa, "naive": naive,
+            "nvlink": nvlink, "check_max_rel_err": err}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    layer.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,371 @@
+/*
+ * monta.h — C ABI of the B200-native MoNTA dispatch/combine path.
+ *
+ * This is the drop-in boundary for the reference's operator API
+ * (/root/reference/proj/include/moeplan/{dataplane,commcost,chunkopt,strategy,
+ * calibrate,pipesim,config}.hpp).  The reference is a header-only C++20
+ * library with value semantics and exceptions; here every entry point is a
+ * plain `extern "C"` function over device/host pointers and sizes that
+ * returns a moe_status.  Exceptions map to status codes:
+ *
+ *   std::invalid_argument                 -> MOE_ERR_INVALID_ARGUMENT
+ *   dataplane::CorruptRoutingError        -> MOE_ERR_CORRUPT_ROUTING   (dataplane.hpp:18-20)
+ *   StrategyInapplicableError             -> MOE_ERR_STRATEGY_INAPPLICABLE (chunkopt.hpp:11-13)
+ *   CalibrationError                      -> MOE_ERR_CALIBRATION       (calibrate.hpp:12-14)
+ *   pipesim::InvalidGraphError            -> MOE_ERR_INVALID_GRAPH     (pipesim.hpp:65-67)
+ *
+ * The message of the last failure on the calling thread is moe_last_error().
+ *
+ * Three families of entry points:
+ *   1. stateless device ops (router, index build, permute, un-permute combine)
+ *      that work on caller-owned device pointers and a caller stream;
+ *   2. a layer context (moe_ctx) that owns the per-card HBM layout, the
+ *      NVLink peer mappings, prioritised streams and cross-GPU flags, and runs
+ *      the TP-deduplicated chunked dispatch and the mirrored combine;
+ *   3. the host planner (cost model, chunk search, strategy selection,
+ *      calibration, pipeline simulator) in double precision.
+ *
+ * Streams are passed as `void*` (a cudaStream_t); NULL is the legacy stream.
+ */
+#ifndef MONTA_H_
+#define MONTA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MONTA_ABI_VERSION 1
+
+typedef enum moe_status {
+  MOE_OK = 0,
+  MOE_ERR_INVALID_ARGUMENT = 1,
+  MOE_ERR_CORRUPT_ROUTING = 2,
+  MOE_ERR_STRATEGY_INAPPLICABLE = 3,
+  MOE_ERR_CALIBRATION = 4,
+  MOE_ERR_INVALID_GRAPH = 5,
+  MOE_ERR_CUDA = 6,
+  MOE_ERR_TRANSPORT = 7, /* peer mapping failed / peer not reachable */
+  MOE_ERR_TIMEOUT = 8,   /* a cross-GPU flag wait timed out */
+  MOE_ERR_UNSUPPORTED = 9
+} moe_status;
+
+/* Mirrors moeplan::StrategyLevel (commcost.hpp:11).  BASELINE is the
+ * monolithic TP-redundant AllToAll (dataplane::dispatch_monolithic). */
+typedef enum moe_level { MOE_BASELINE = 0, MOE_O1 = 1, MOE_O2 = 2, MOE_O3 = 3 } moe_level;
+
+typedef enum moe_dtype {
+  MOE_F32 = 0,
+  MOE_BF16 = 1,
+  MOE_F16 = 2,
+  MOE_F64 = 3,
+  MOE_I64 = 4 /* the reference's payload type (dataplane.hpp:39) */
+} moe_dtype;
+
+/* Where the chunked exchange lands rows on the receiving card.
+ *   FINAL : senders know every offset after the count exchange and write
+ *           straight into the source-major final layout (no reorder copy).
+ *   STAGED: rows land chunk-major (the reference's ChunkedDispatchTrace::pre_copy
+ *           layout, dataplane.hpp:260-261) and a D2D reorder copy moves them
+ *           to the final layout (dataplane.hpp:263-274), as MoNTA does. */
+typedef enum moe_landing { MOE_LAND_FINAL = 0, MOE_LAND_STAGED = 1 } moe_landing;
+
+const char* moe_last_error(void);
+int moe_abi_version(void);
+size_t moe_dtype_size(int dtype);
+
+/* ------------------------------------------------------------------------
+ * 1. Stateless device ops
+ * ------------------------------------------------------------------------ */
+
+/* dataplane::route_topk (dataplane.hpp:72-106).
+ * logits [T, E] row-major in `logit_dtype` (MOE_F32 or MOE_F64).  Softmax in
+ * that precision (max-subtract, exp, sum, divide); the k largest RAW scores
+ * win, lower expert index on ties; experts written ascending; probs are the
+ * softmax values of the selected experts (not renormalised), same dtype as
+ * the logits.  T == 0 is allowed (no launch).
+ * Errors: k < 1, E < 1 (empty row), k > E -> MOE_ERR_INVALID_ARGUMENT. */
+moe_status moe_route_topk(const void* logits, int logit_dtype, int64_t T, int32_t E, int32_t k,
+                          int32_t* experts, void* probs, void* stream);
+
+/* Stable counting sort of the (token, slot) pairs by expert — the index
+ * form of dataplane::permute (dataplane.hpp:118-140).
+ *   experts     [T, k]   expert of each pair, 0 <= x < E
+ *   perm_src    [T*k]    source token of permuted row r
+ *   expert_of   [T*k]    expert of permuted row r           (PermutedBatch::expert_of)
+ *   slot_pos    [T, k]   permuted row of pair (i, s)       (PermutedBatch::inverse_map
+ *                        when the token's experts ascend, which route_topk guarantees)
+ *   counts      [n, E]   rows of expert x whose token falls in chunk j = i / (T/n)
+ *   expert_offsets [E+1] exclusive scan of rows per expert
+ *   dev_error   device int32 set to MOE_ERR_INVALID_ARGUMENT if an expert id
+ *               is out of range (may be NULL).
+ * Ordering is expert-major, token-ascending, with no atomics in the ordering.
+ * Errors: n < 1, T % n != 0 -> MOE_ERR_INVALID_ARGUMENT. */
+moe_status moe_build_index(const int32_t* experts, int64_t T, int32_t k, int32_t E, int32_t n_chunks,
+                           int32_t* perm_src, int32_t* expert_of, int32_t* slot_pos,
+                           int32_t* counts, int32_t* expert_offsets, int32_t* dev_error,
+                           void* stream);
+
+/* Gather-permute: out[r, 0:width) = src[perm_src[r], col_off:col_off+width)
+ * (bytes).  16-byte vectorised when every size/stride/offset allows. */
+moe_status moe_permute_rows(const void* src, int64_t src_row_bytes, int64_t col_off_bytes,
+                            int64_t width_bytes, const int32_t* perm_src, int64_t R, void* out,
+                            int64_t out_row_bytes, void* stream);
+
+/* Weighted un-permute (the arithmetic of dataplane::combine_unpermute,
+ * dataplane.hpp:325-342):  out[i, q] = sum_s probs[i,s] * y[slot_pos[i,s], q],
+ * accumulated from 0 in ascending slot order.  Accumulation is fp32 for
+ * f32/bf16/f16 inputs and fp64 for f64/i64 inputs.  `probs_dtype` is MOE_F32
+ * or MOE_F64.  out_dtype: MOE_F32/MOE_BF16/MOE_F16/MOE_F64. */
+moe_status moe_unpermute_combine(const void* y, int y_dtype, int64_t y_row_elems, int64_t width,
+                                 const int32_t* slot_pos, const void* probs, int probs_dtype,
+                                 int64_t T, int32_t k, void* out, int out_dtype,
+                                 int64_t out_row_elems, void* stream);
+
+/* ------------------------------------------------------------------------
+ * 2. Layer context: one MoE layer's dispatch + combine over e x t cards
+ * ------------------------------------------------------------------------
+ * Topology (dataplane::VirtualTopology, dataplane.hpp:25-33): card c =
+ * node*t + rho; node x hosts experts [x*L, (x+1)*L) with L = E/e, sharded over
+ * its t cards; the e cards with equal rho form an expert-parallel group.
+ *
+ * world_size == 1        : every card lives on `device` (virtual mode; the
+ *                          reference's single-process emulation).
+ * world_size == e*t      : one card per process, card == rank; peers are
+ *                          mapped over NVLink with CUDA IPC (moe_ctx_ipc_*).
+ */
+typedef struct moe_layer_desc {
+  int32_t e;           /* node groups (expert parallel degree)            */
+  int32_t t;           /* tensor-parallel ranks per node                  */
+  int32_t num_experts; /* E, a multiple of e                              */
+  int32_t top_k;       /* k                                               */
+  int64_t tokens;      /* T per node group                                */
+  int64_t hidden;      /* h payload elements per row                      */
+  int32_t dtype;       /* payload dtype (any; dispatch moves bytes)       */
+  int32_t logit_dtype; /* MOE_F32 or MOE_F64                              */
+  int32_t out_dtype;   /* combine output dtype                            */
+  int32_t max_chunks;  /* upper bound on n                                */
+} moe_layer_desc;
+
+typedef struct moe_ctx moe_ctx;
+
+/* Device pointers of one card (all owned by the context). */
+typedef struct moe_card_view {
+  void* x;                 /* [T, h] node batch (replicated across the node's TP ranks) */
+  void* logits;            /* [T, E]                                              */
+  int32_t* token_ids;      /* [T]   TokenRecord::token_id (default i + node*100000) */
+  int32_t* experts;        /* [T, k] routing (route output or caller-provided)    */
+  void* probs;             /* [T, k] logit dtype                                  */
+  int32_t* perm_src;       /* [T*k]                                               */
+  int32_t* expert_of;      /* [T*k]                                               */
+  int32_t* slot_pos;       /* [T, k]                                              */
+  int32_t* counts;         /* [max_chunks, E] (first n rows valid)               */
+  int32_t* expert_offsets; /* [E+1]                                               */
+  void* permuted;          /* [T*k, h] permute output (moe_ctx_permute)           */
+  void* recv;              /* [recv_cap, h] dispatched rows, final layout         */
+  int32_t* recv_tags;      /* [recv_cap, 4] {token_id, source_card, source_position, expert} */
+  void* pre;               /* [recv_cap, h] staged chunk-major layout (pre_copy)  */
+  int32_t* pre_tags;       /* [recv_cap, 4]                                       */
+  void* expert_out;        /* [recv_cap, h] expert outputs read by combine (== recv unless rebound) */
+  void* comb;              /* [T*k, h] combine landing, sender-permuted order     */
+  void* out;               /* [T, h] combined output in out_dtype                 */
+  int64_t rows_permuted;   /* T*k                                                 */
+  int64_t recv_cap;        /* e*T*min(k, L)                                       */
+} moe_card_view;
+
+moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int rank, int world_size,
+                          moe_ctx** out);
+moe_status moe_ctx_destroy(moe_ctx* ctx);
+moe_status moe_ctx_card_view(moe_ctx* ctx, int card, moe_card_view* out);
+int moe_ctx_num_local_cards(const moe_ctx* ctx);
+int moe_ctx_first_card(const moe_ctx* ctx);
+
+/* Multi-process wiring: export this rank's IPC handle blob, then import the
+ * blobs of all ranks (concatenated in rank order). */
+size_t moe_ctx_ipc_handle_size(void);
+moe_status moe_ctx_ipc_export(moe_ctx* ctx, void* blob);
+moe_status moe_ctx_ipc_connect(moe_ctx* ctx, const void* all_blobs);
+
+/* Expert outputs: by default the combine reads `recv` (identity experts, or
+ * an expert computed in place).  Rebind to any [recv_cap, h] buffer. */
+moe_status moe_ctx_bind_expert_out(moe_ctx* ctx, int card, void* expert_out);
+
+/* Route every local card (moe_route_topk on its logits). */
+moe_status moe_ctx_route(moe_ctx* ctx, void* stream);
+/* Materialise the permuted batch of every local card (dataplane::permute). */
+moe_status moe_ctx_permute(moe_ctx* ctx, int32_t n_chunks, void* stream);
+/* Dispatch (dataplane::dispatch_monolithic when level == MOE_BASELINE,
+ * dataplane::dispatch_chunked otherwise).  Builds the index, exchanges the
+ * per-chunk counts, and moves rows.  Validation mirrors dataplane.hpp:190-216. */
+moe_status moe_ctx_dispatch(moe_ctx* ctx, int level, int32_t n_chunks, int landing, void* stream);
+/* Second AllToAll + weighted un-permute (dataplane::combine_unpermute),
+ * mirrored per level: BASELINE returns full rows; O1/O2/O3 return the
+ * receiving rank's 1/t slice, un-permute it and all-gather the output
+ * slices inside the node.  Must follow a dispatch with the same n. */
+moe_status moe_ctx_combine(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
+/* route + dispatch + combine. */
+moe_status moe_ctx_forward(moe_ctx* ctx, int level, int32_t n_chunks, int landing, void* stream);
+/* End-to-end from HOST buffers: H2D of x/logits for every local card
+ * (node-major [local cards][T][...]), forward, D2H of `out`.  Host buffers
+ * should be pinned for async copies. */
+moe_status moe_ctx_forward_host(moe_ctx* ctx, int level, int32_t n_chunks, int landing,
+                                const void* host_x, const void* host_logits, void* host_out,
+                                void* stream);
+/* Rows in card's recv buffer after the last dispatch (synchronises). */
+moe_status moe_ctx_recv_rows(moe_ctx* ctx, int card, int64_t* rows);
+/* Synchronise the context's streams and report device-side errors
+ * (corrupt routing, out-of-range experts, flag timeouts). */
+moe_status moe_ctx_sync(moe_ctx* ctx);
+/* Per-stage timing of the last dispatch/combine (ms, from CUDA events
+ * recorded when enabled).  stage ids: see moe_stage.  Returns MOE_OK with
+ * *n_spans == 0 when timing is disabled. */
+typedef enum moe_stage {
+  MOE_STAGE_ROUTE = 0,
+  MOE_STAGE_INDEX = 1,
+  MOE_STAGE_AA = 2,
+  MOE_STAGE_AG = 3,
+  MOE_STAGE_D2D = 4,
+  MOE_STAGE_CAA = 5,
+  MOE_STAGE_UNPERMUTE = 6,
+  MOE_STAGE_TOTAL = 7
+} moe_stage;
+typedef struct moe_span {
+  int32_t stage;
+  int32_t chunk;
+  float start_ms; /* relative to the dispatch start event */
+  float end_ms;
+} moe_span;
+moe_status moe_ctx_enable_timing(moe_ctx* ctx, int enable);
+moe_status moe_ctx_spans(moe_ctx* ctx, moe_span* spans, int32_t capacity, int32_t* n_spans);
+/* Cap the SMs used by the cross-group (AllToAll) copy kernels, emulating a
+ * slow inter-node link ("B1-throttled" mode).  0 = no cap. */
+moe_status moe_ctx_set_aa_ctas(moe_ctx* ctx, int32_t ctas);
+/* Number of kernels this context launched since creation. */
+int64_t moe_ctx_launch_count(const moe_ctx* ctx);
+
+/* ------------------------------------------------------------------------
+ * 3. Planner (host, fp64)
+ * ------------------------------------------------------------------------ */
+typedef struct moe_model_spec { /* config.hpp:14-24 */
+  int64_t b, s, h, a, l, k, p1, p2;
+  int32_t bpe;
+} moe_model_spec;
+typedef struct moe_parallel_spec { /* config.hpp:26-32 */
+  int32_t d, p, t, e, cp;
+} moe_parallel_spec;
+typedef struct moe_cluster_spec { /* config.hpp:34-42 */
+  int32_t nodes, gpus_per_node;
+  double b1, b2, b3, peak_flops;
+  int64_t switch_capacity;
+} moe_cluster_spec;
+typedef struct moe_curve { /* EfficiencyCurve, config.hpp:49-61; volumes strictly increasing */
+  const double* volume;
+  const double* efficiency;
+  int32_t n_points;
+  double i_minimal;
+} moe_curve;
+typedef struct moe_curve_set {
+  moe_curve alltoall, allgather, d2d;
+} moe_curve_set;
+typedef struct moe_overhead { /* OverheadModel, commcost.hpp:24-27 */
+  double alpha_comm, alpha_copy;
+} moe_overhead;
+typedef struct moe_chunk_timing { /* ChunkTiming, commcost.hpp:30-36 */
+  double aa, ag, d2d;
+  int32_t n;
+  double volume;
+} moe_chunk_timing;
+typedef struct moe_chunk_search_result { /* ChunkSearchResult, chunkopt.hpp:26-31 */
+  int32_t n_opt;
+  double t_pred;
+  moe_chunk_timing per_chunk;
+  int32_t feasible;
+} moe_chunk_search_result;
+typedef struct moe_strategy_alt {
+  int32_t level;
+  double t_pred;
+  int32_t n;
+} moe_strategy_alt;
+typedef struct moe_strategy_decision { /* StrategyDecision, strategy.hpp:13-18 */
+  int32_t level;
+  int32_t n;
+  double t_pred;
+  int32_t n_alternatives;
+  moe_strategy_alt alternatives[3];
+} moe_strategy_decision;
+typedef struct moe_perf_report {
+  double step_latency, throughput, mfu;
+} moe_perf_report;
+
+moe_status moe_lookup_efficiency(const moe_curve* curve, double volume, double* out);
+double moe_traffic_volume(const moe_model_spec* m);
+moe_status moe_chunk_alltoall_time(double volume, int32_t n, int32_t t, int32_t e, double b1,
+                                   const moe_curve* curve, const moe_overhead* ov, double* out);
+moe_status moe_chunk_allgather_time(double volume, int32_t n, int32_t t, double b2,
+                                    const moe_curve* curve, const moe_overhead* ov, double* out);
+moe_status moe_chunk_d2d_time(double volume, int32_t n, double b3, const moe_curve* curve,
+                              const moe_overhead* ov, double* out);
+moe_status moe_baseline_time(double volume, int32_t e, double b1, const moe_curve* curve,
+                             const moe_overhead* ov, double* out);
+moe_status moe_o1_time(double volume, int32_t t, int32_t e, double b1, double b2,
+                       const moe_curve_set* curves, const moe_overhead* ov, double* out);
+double moe_o2_score(double aa, double ag, double d2d, int32_t n);
+double moe_o3_score(double aa, double ag, double d2d, int32_t n);
+moe_status moe_o2_search(const moe_model_spec* m, const moe_parallel_spec* par,
+                         const moe_cluster_spec* cl, const moe_curve_set* curves,
+                         const moe_overhead* ov, int32_t n_cap, moe_chunk_search_result* out);
+moe_status moe_o3_search(const moe_model_spec* m, const moe_parallel_spec* par,
+                         const moe_cluster_spec* cl, const moe_curve_set* curves,
+                         const moe_overhead* ov, int32_t n_cap, moe_chunk_search_result* out);
+moe_status moe_asymptotic_speedup(int32_t t, int32_t e, double b1, double b2, double r1,
+                                  double r2, double* out);
+moe_status moe_select_strategy(const moe_model_spec* m, const moe_parallel_spec* par,
+                               const moe_cluster_spec* cl, const moe_curve_set* curves,
+                               const moe_overhead* ov, int32_t n_cap, moe_strategy_decision* out);
+moe_status moe_estimate_performance(const moe_strategy_decision* d, const moe_model_spec* m,
+                                    const moe_parallel_spec* par, const moe_cluster_spec* cl,
+                                    int32_t moe_layer_count, double non_comm_time,
+                                    moe_perf_report* out);
+
+/* calibrate (calibrate.hpp:84-118).  primitive: 0 alltoall, 1 allgather, 2 d2d.
+ * Output curves are written into caller arrays of capacity `count` each
+ * (volumes/efficiencies per primitive), with point counts in n_points[3]. */
+typedef struct moe_bench_sample {
+  int32_t primitive;
+  double volume;
+  double seconds;
+} moe_bench_sample;
+moe_status moe_calibrate(const moe_bench_sample* samples, int32_t count,
+                         const moe_cluster_spec* cl, double* volumes /*[3][count]*/,
+                         double* efficiencies /*[3][count]*/, int32_t* n_points /*[3]*/,
+                         moe_overhead* overhead);
+
+/* pipesim::build_pipeline + pipesim::simulate (pipesim.hpp:91-173).
+ * Streams: 0 alltoall, 1 allgather, 2 d2d, 3 compute.  Task ids follow the
+ * reference ("dispatch_aa_1", ...) and are written as `kind` codes:
+ * kind = phase*8 + {0 aa, 1 ag, 2 d2d, 3 expert}; chunk is 1-based. */
+typedef struct moe_sim_span {
+  int32_t kind;
+  int32_t chunk;
+  int32_t stream;
+  double start, end;
+} moe_sim_span;
+moe_status moe_simulate_pipeline(int level, int32_t n, const moe_chunk_timing* timing,
+                                 double expert_time, int32_t phases, moe_sim_span* spans,
+                                 int32_t capacity, int32_t* n_spans, double* makespan);
+/* General list scheduler over an explicit task graph (pipesim::simulate).
+ * deps are indices into the task array, flattened with offsets. */
+typedef struct moe_sim_task {
+  int32_t stream;
+  double duration;
+  int32_t dep_begin, dep_end; /* range into deps[] */
+} moe_sim_task;
+moe_status moe_simulate_graph(const moe_sim_task* tasks, int32_t count, const int32_t* deps,
+                              double* start, double* end, double* makespan);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+#endif /* MONTA_H_ */

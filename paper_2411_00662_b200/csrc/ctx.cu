@@ -1,0 +1,1044 @@
+// Layer context: per-card HBM layout, NVLink peer mappings, prioritised
+// streams, the cross-GPU flag protocol, and the orchestration of
+//   dispatch = index build -> count exchange -> plan -> per chunk
+//              { AA (+fused permute) ; AG ; D2D }            (dataplane.hpp:187-283)
+//   combine  = per chunk { reverse AA ; un-permute (+fused output AG) } (dataplane.hpp:293-347)
+//
+// Stream roles follow the reference simulator (pipesim.hpp:58-83, Fig. 14 of
+// the paper): the AllToAll legs run on a high-priority stream, the AllGather
+// legs on a second stream, the reorder copies on the AllGather stream (O2) or
+// a third stream (O3).  Cross-GPU ordering uses epoch flags written over
+// NVLink (common.cuh); cross-stream ordering on one GPU uses CUDA events.
+//
+// In virtual mode (world_size == 1) every card lives on one device and the
+// phases run in lockstep on the caller's stream — no card ever waits on
+// another card's kernel, so nothing spins.
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+
+namespace monta {
+
+namespace {
+
+constexpr size_t kAlign = 256;
+inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
+
+struct PeerPtrs {
+  char* slab = nullptr;
+  char* recv = nullptr;
+  int32_t* recv_tags = nullptr;
+  char* pre = nullptr;
+  int32_t* pre_tags = nullptr;
+  char* comb = nullptr;
+  char* out = nullptr;
+  int32_t* count_table = nullptr;
+  uint64_t* flags = nullptr;
+};
+
+// Byte offsets of every buffer inside a card's slab.  Identical on every
+// rank, so an IPC-mapped peer slab is addressed with the same offsets.
+struct SlabLayout {
+  size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
+  size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
+  size_t lists, local_delta, recv_rows, scratch, total;
+};
+
+struct Card {
+  int id = 0, node = 0, rho = 0;
+  char* slab = nullptr;
+  moe_card_view v{};
+  int32_t* count_table = nullptr;
+  uint64_t* flags = nullptr;
+  int32_t* err = nullptr;
+  unsigned* done = nullptr;
+  SegList* lists = nullptr;
+  int32_t* local_delta = nullptr;
+  int64_t* recv_rows = nullptr;
+  int32_t* scratch = nullptr;
+};
+
+struct Span {
+  int stage, chunk;
+  cudaEvent_t a, b;
+};
+
+}  // namespace
+}  // namespace monta
+
+struct moe_ctx {
+  moe_layer_desc d{};
+  int L = 1, cards = 1, device = 0, rank = 0, world = 1, sms = 148;
+  size_t xb = 0, lb = 0, ob = 0;  // element bytes of payload / logits / out
+  int64_t R = 0, recv_cap = 0, row_bytes = 0;
+  int n_flag_sigs = 0;
+  monta::SlabLayout lay{};
+  std::vector<monta::Card> local;
+  monta::PeerPtrs peer[monta::kMaxCards];
+  std::vector<void*> opened;
+  cudaStream_t s_aa = nullptr, s_ag = nullptr, s_d2d = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join_aa = nullptr, ev_join_ag = nullptr, ev_join_d2d = nullptr;
+  std::vector<cudaEvent_t> ev_aa, ev_ag;
+  uint64_t epoch = 0;
+  int aa_ctas = 0;
+  bool connected = false;
+  // last dispatch (the combine replays its plan)
+  int last_level = -1, last_n = 0, last_landing = 0;
+  bool timing = false;
+  bool in_forward = false;
+  cudaEvent_t ev_base = nullptr;
+  std::vector<monta::Span> spans;
+  size_t span_used = 0;
+  int64_t launches = 0;
+};
+
+namespace monta {
+namespace {
+
+bool is_virtual(const moe_ctx* c) { return c->world == 1; }
+
+SlabLayout make_layout(const moe_ctx* c) {
+  const moe_layer_desc& d = c->d;
+  SlabLayout s{};
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t at = off;
+    off = align_up(off + std::max<size_t>(bytes, 1));
+    return at;
+  };
+  const int64_t T = d.tokens, h = d.hidden, E = d.num_experts, k = d.top_k;
+  s.x = take(size_t(T) * h * c->xb);
+  s.logits = take(size_t(T) * E * c->lb);
+  s.token_ids = take(size_t(T) * 4);
+  s.experts = take(size_t(T) * k * 4);
+  s.probs = take(size_t(T) * k * c->lb);
+  s.perm_src = take(size_t(c->R) * 4);
+  s.expert_of = take(size_t(c->R) * 4);
+  s.slot_pos = take(size_t(T) * k * 4);
+  s.counts = take(size_t(d.max_chunks) * E * 4);
+  s.offsets = take(size_t(E + 1) * 4);
+  s.permuted = take(size_t(c->R) * c->row_bytes);
+  s.recv = take(size_t(c->recv_cap) * c->row_bytes);
+  s.recv_tags = take(size_t(c->recv_cap) * 16);
+  s.pre = take(size_t(c->recv_cap) * c->row_bytes);
+  s.pre_tags = take(size_t(c->recv_cap) * 16);
+  s.comb = take(size_t(c->R) * c->row_bytes);
+  s.out = take(size_t(T) * h * c->ob);
+  s.count_table = take(size_t(d.e) * d.max_chunks * E * 4);
+  s.flags = take(size_t(c->n_flag_sigs) * kMaxCards * 8);
+  s.err = take(16);
+  s.done = take(size_t(kNumPhaseSignals * d.max_chunks + 8) * 4);
+  s.lists = take(size_t(kNumPhases) * d.max_chunks * seglist_bytes(int(E)));
+  s.local_delta = take(size_t(E) * 4);
+  s.recv_rows = take(8);
+  s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
+  s.total = off;
+  return s;
+}
+
+void bind_card(moe_ctx* c, Card& cd) {
+  const SlabLayout& s = c->lay;
+  char* b = cd.slab;
+  moe_card_view& v = cd.v;
+  v.x = b + s.x;
+  v.logits = b + s.logits;
+  v.token_ids = reinterpret_cast<int32_t*>(b + s.token_ids);
+  v.experts = reinterpret_cast<int32_t*>(b + s.experts);
+  v.probs = b + s.probs;
+  v.perm_src = reinterpret_cast<int32_t*>(b + s.perm_src);
+  v.expert_of = reinterpret_cast<int32_t*>(b + s.expert_of);
+  v.slot_pos = reinterpret_cast<int32_t*>(b + s.slot_pos);
+  v.counts = reinterpret_cast<int32_t*>(b + s.counts);
+  v.expert_offsets = reinterpret_cast<int32_t*>(b + s.offsets);
+  v.permuted = b + s.permuted;
+  v.recv = b + s.recv;
+  v.recv_tags = reinterpret_cast<int32_t*>(b + s.recv_tags);
+  v.pre = b + s.pre;
+  v.pre_tags = reinterpret_cast<int32_t*>(b + s.pre_tags);
+  v.expert_out = v.recv;
+  v.comb = b + s.comb;
+  v.out = b + s.out;
+  v.rows_permuted = c->R;
+  v.recv_cap = c->recv_cap;
+  cd.count_table = reinterpret_cast<int32_t*>(b + s.count_table);
+  cd.flags = reinterpret_cast<uint64_t*>(b + s.flags);
+  cd.err = reinterpret_cast<int32_t*>(b + s.err);
+  cd.done = reinterpret_cast<unsigned*>(b + s.done);
+  cd.lists = reinterpret_cast<SegList*>(b + s.lists);
+  cd.local_delta = reinterpret_cast<int32_t*>(b + s.local_delta);
+  cd.recv_rows = reinterpret_cast<int64_t*>(b + s.recv_rows);
+  cd.scratch = reinterpret_cast<int32_t*>(b + s.scratch);
+}
+
+void set_peer(moe_ctx* c, int card, char* slab) {
+  const SlabLayout& s = c->lay;
+  PeerPtrs& p = c->peer[card];
+  p.slab = slab;
+  p.recv = slab + s.recv;
+  p.recv_tags = reinterpret_cast<int32_t*>(slab + s.recv_tags);
+  p.pre = slab + s.pre;
+  p.pre_tags = reinterpret_cast<int32_t*>(slab + s.pre_tags);
+  p.comb = slab + s.comb;
+  p.out = slab + s.out;
+  p.count_table = reinterpret_cast<int32_t*>(slab + s.count_table);
+  p.flags = reinterpret_cast<uint64_t*>(slab + s.flags);
+}
+
+inline int card_of(const moe_ctx* c, int node, int rho) { return node * c->d.t + rho; }
+inline int sig_chunk(const moe_ctx* c, int ps, int j) { return kSigChunkBase + ps * c->d.max_chunks + j; }
+
+// Flag word on `owner` that `sender` writes for signal `sig`.
+inline uint64_t* flag_at(moe_ctx* c, int owner, int sig, int sender) {
+  return c->peer[owner].flags + size_t(sig) * kMaxCards + sender;
+}
+
+SegList* list_of(const moe_ctx* c, const Card& cd, int phase, int j) {
+  char* base = reinterpret_cast<char*>(cd.lists);
+  return reinterpret_cast<SegList*>(base + (size_t(phase) * c->d.max_chunks + j) *
+                                               seglist_bytes(c->d.num_experts));
+}
+
+// ---- timing -------------------------------------------------------------
+void span_begin(moe_ctx* c, int stage, int chunk, cudaStream_t s, size_t* slot) {
+  *slot = SIZE_MAX;
+  if (!c->timing) return;
+  if (c->span_used == c->spans.size()) {
+    Span sp{stage, chunk, nullptr, nullptr};
+    cudaEventCreate(&sp.a);
+    cudaEventCreate(&sp.b);
+    c->spans.push_back(sp);
+  }
+  Span& sp = c->spans[c->span_used];
+  sp.stage = stage;
+  sp.chunk = chunk;
+  cudaEventRecord(sp.a, s);
+  *slot = c->span_used++;
+}
+void span_end(moe_ctx* c, size_t slot, cudaStream_t s) {
+  if (slot == SIZE_MAX) return;
+  cudaEventRecord(c->spans[slot].b, s);
+}
+
+int copy_grid(const moe_ctx* c, bool concurrent, bool aa) {
+  int g = c->sms * (concurrent ? 2 : 4);
+  if (aa && c->aa_ctas > 0) g = std::min(g, c->aa_ctas);
+  return g;
+}
+
+WaitList no_wait() {
+  WaitList w{};
+  w.n = 0;
+  w.epoch = 0;
+  return w;
+}
+SignalList no_signal() {
+  SignalList s{};
+  s.n = 0;
+  return s;
+}
+
+}  // namespace
+
+// ===========================================================================
+// creation / teardown
+// ===========================================================================
+static moe_status validate_desc(const moe_layer_desc* d) {
+  if (!d) return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: null descriptor");
+  if (d->e < 1 || d->t < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: e and t must be >= 1");
+  if (d->e * d->t > kMaxCards)
+    return fail(MOE_ERR_UNSUPPORTED, "ctx_create: at most %d cards", kMaxCards);
+  if (d->num_experts < 1 || d->num_experts % d->e != 0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: E must be a positive multiple of e");
+  if (d->top_k < 1 || d->top_k > d->num_experts)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: need 1 <= k <= E");
+  if (d->tokens < 0 || d->hidden < 1)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: bad token/hidden sizes");
+  if (dtype_size(d->dtype) == 0 || dtype_size(d->out_dtype) == 0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: bad dtype");
+  if (d->logit_dtype != MOE_F32 && d->logit_dtype != MOE_F64)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: logits must be f32 or f64");
+  if (d->max_chunks < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: max_chunks >= 1");
+  return MOE_OK;
+}
+
+}  // namespace monta
+
+using namespace monta;
+
+extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int rank,
+                                     int world_size, moe_ctx** out) {
+  if (!out) return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: null out");
+  *out = nullptr;
+  if (moe_status st = validate_desc(desc)) return st;
+  const int cards = desc->e * desc->t;
+  if (!(world_size == 1 || world_size == cards))
+    return fail(MOE_ERR_UNSUPPORTED, "ctx_create: world_size must be 1 or e*t (%d), got %d", cards,
+                world_size);
+  if (rank < 0 || rank >= world_size) return fail(MOE_ERR_INVALID_ARGUMENT, "ctx_create: bad rank");
+  MONTA_CUDA(cudaSetDevice(device));
+  moe_ctx* c = new moe_ctx();
+  c->d = *desc;
+  c->L = desc->num_experts / desc->e;
+  c->cards = cards;
+  c->device = device;
+  c->rank = rank;
+  c->world = world_size;
+  cudaDeviceGetAttribute(&c->sms, cudaDevAttrMultiProcessorCount, device);
+  c->xb = dtype_size(desc->dtype);
+  c->lb = dtype_size(desc->logit_dtype);
+  c->ob = dtype_size(desc->out_dtype);
+  c->R = desc->tokens * desc->top_k;
+  c->row_bytes = desc->hidden * int64_t(c->xb);
+  c->recv_cap = int64_t(desc->e) * desc->tokens * std::min<int64_t>(desc->top_k, c->L);
+  c->n_flag_sigs = kSigChunkBase + kNumPhaseSignals * desc->max_chunks;
+  c->lay = make_layout(c);
+  const int first = world_size == 1 ? 0 : rank;
+  const int nlocal = world_size == 1 ? cards : 1;
+  for (int i = 0; i < nlocal; ++i) {
+    Card cd;
+    cd.id = first + i;
+    cd.node = cd.id / desc->t;
+    cd.rho = cd.id % desc->t;
+    cudaError_t err = cudaMalloc(&cd.slab, c->lay.total);
+    if (err != cudaSuccess) {
+      for (auto& o : c->local) cudaFree(o.slab);
+      delete c;
+      return cuda_fail(err, "ctx_create: slab allocation");
+    }
+    cudaMemset(cd.slab, 0, c->lay.total);
+    bind_card(c, cd);
+    c->local.push_back(cd);
+    set_peer(c, cd.id, cd.slab);
+  }
+  // default token ids: i + node * 100000 (dataplane::make_batch, dataplane.hpp:48-57)
+  {
+    std::vector<int32_t> ids(size_t(desc->tokens));
+    for (auto& cd : c->local) {
+      for (int64_t i = 0; i < desc->tokens; ++i) ids[size_t(i)] = int32_t(i + cd.node * 100000);
+      if (desc->tokens > 0)
+        cudaMemcpy(cd.v.token_ids, ids.data(), ids.size() * 4, cudaMemcpyHostToDevice);
+    }
+  }
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi is the numerically smallest (highest) priority
+  cudaStreamCreateWithPriority(&c->s_aa, cudaStreamNonBlocking, hi);
+  cudaStreamCreateWithPriority(&c->s_ag, cudaStreamNonBlocking, lo);
+  cudaStreamCreateWithPriority(&c->s_d2d, cudaStreamNonBlocking, lo);
+  cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join_aa, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join_ag, cudaEventDisableTiming);
+  cudaEventCreateWithFlags(&c->ev_join_d2d, cudaEventDisableTiming);
+  c->ev_aa.resize(size_t(desc->max_chunks));
+  c->ev_ag.resize(size_t(desc->max_chunks));
+  for (int j = 0; j < desc->max_chunks; ++j) {
+    cudaEventCreateWithFlags(&c->ev_aa[j], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_ag[j], cudaEventDisableTiming);
+  }
+  cudaEventCreate(&c->ev_base);
+  cudaError_t err = cudaDeviceSynchronize();
+  if (err != cudaSuccess) {
+    moe_ctx_destroy(c);
+    return cuda_fail(err, "ctx_create");
+  }
+  c->connected = world_size == 1;
+  *out = c;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_destroy(moe_ctx* c) {
+  if (!c) return MOE_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  for (auto& cd : c->local) cudaFree(cd.slab);
+  for (auto& sp : c->spans) {
+    cudaEventDestroy(sp.a);
+    cudaEventDestroy(sp.b);
+  }
+  for (auto ev : c->ev_aa) cudaEventDestroy(ev);
+  for (auto ev : c->ev_ag) cudaEventDestroy(ev);
+  if (c->ev_base) cudaEventDestroy(c->ev_base);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join_aa) cudaEventDestroy(c->ev_join_aa);
+  if (c->ev_join_ag) cudaEventDestroy(c->ev_join_ag);
+  if (c->ev_join_d2d) cudaEventDestroy(c->ev_join_d2d);
+  if (c->s_aa) cudaStreamDestroy(c->s_aa);
+  if (c->s_ag) cudaStreamDestroy(c->s_ag);
+  if (c->s_d2d) cudaStreamDestroy(c->s_d2d);
+  delete c;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_card_view(moe_ctx* c, int card, moe_card_view* out) {
+  if (!c || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "card_view: null argument");
+  for (auto& cd : c->local)
+    if (cd.id == card) {
+      *out = cd.v;
+      return MOE_OK;
+    }
+  return fail(MOE_ERR_INVALID_ARGUMENT, "card_view: card %d is not local to this context", card);
+}
+
+extern "C" int moe_ctx_num_local_cards(const moe_ctx* c) { return c ? int(c->local.size()) : 0; }
+extern "C" int moe_ctx_first_card(const moe_ctx* c) { return c && !c->local.empty() ? c->local[0].id : -1; }
+
+extern "C" moe_status moe_ctx_bind_expert_out(moe_ctx* c, int card, void* expert_out) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "bind_expert_out: null ctx");
+  for (auto& cd : c->local)
+    if (cd.id == card) {
+      cd.v.expert_out = expert_out ? expert_out : cd.v.recv;
+      return MOE_OK;
+    }
+  return fail(MOE_ERR_INVALID_ARGUMENT, "bind_expert_out: card %d is not local", card);
+}
+
+// ---- IPC -----------------------------------------------------------------
+namespace {
+struct IpcBlob {
+  uint32_t magic;
+  int32_t card;
+  uint64_t slab_bytes;
+  cudaIpcMemHandle_t handle;
+  char pad[128 - 16 - sizeof(cudaIpcMemHandle_t)];
+};
+static_assert(sizeof(IpcBlob) == 128, "ipc blob");
+constexpr uint32_t kMagic = 0x4d4f4e54;  // "MONT"
+}  // namespace
+
+extern "C" size_t moe_ctx_ipc_handle_size(void) { return sizeof(IpcBlob); }
+
+extern "C" moe_status moe_ctx_ipc_export(moe_ctx* c, void* blob) {
+  if (!c || !blob) return fail(MOE_ERR_INVALID_ARGUMENT, "ipc_export: null argument");
+  if (c->local.size() != 1) return fail(MOE_ERR_INVALID_ARGUMENT, "ipc_export: multi-process contexts only");
+  MONTA_CUDA(cudaSetDevice(c->device));
+  IpcBlob b{};
+  b.magic = kMagic;
+  b.card = c->local[0].id;
+  b.slab_bytes = c->lay.total;
+  MONTA_CUDA(cudaIpcGetMemHandle(&b.handle, c->local[0].slab));
+  std::memcpy(blob, &b, sizeof(b));
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_ipc_connect(moe_ctx* c, const void* all_blobs) {
+  if (!c || !all_blobs) return fail(MOE_ERR_INVALID_ARGUMENT, "ipc_connect: null argument");
+  if (c->world == 1) return MOE_OK;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  const IpcBlob* blobs = static_cast<const IpcBlob*>(all_blobs);
+  for (int r = 0; r < c->world; ++r) {
+    const IpcBlob& b = blobs[r];
+    if (b.magic != kMagic || b.card != r || b.slab_bytes != c->lay.total)
+      return fail(MOE_ERR_TRANSPORT, "ipc_connect: blob %d does not describe card %d of this layer", r, r);
+    if (r == c->rank) continue;
+    void* p = nullptr;
+    cudaError_t err = cudaIpcOpenMemHandle(&p, b.handle, cudaIpcMemLazyEnablePeerAccess);
+    if (err != cudaSuccess) return cuda_fail(err, "ipc_connect: cudaIpcOpenMemHandle");
+    c->opened.push_back(p);
+    set_peer(c, r, static_cast<char*>(p));
+  }
+  c->connected = true;
+  return MOE_OK;
+}
+
+// ===========================================================================
+// phases
+// ===========================================================================
+namespace {
+
+moe_status check_ready(moe_ctx* c) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "null context");
+  if (!c->connected) return fail(MOE_ERR_TRANSPORT, "context not connected (call moe_ctx_ipc_connect)");
+  return MOE_OK;
+}
+
+moe_status do_route(moe_ctx* c, cudaStream_t s) {
+  for (auto& cd : c->local) {
+    size_t sl;
+    span_begin(c, MOE_STAGE_ROUTE, 0, s, &sl);
+    if (moe_status st = route_topk(cd.v.logits, c->d.logit_dtype, c->d.tokens, c->d.num_experts,
+                                   c->d.top_k, cd.v.experts, cd.v.probs, s))
+      return st;
+    span_end(c, sl, s);
+    ++c->launches;
+  }
+  return MOE_OK;
+}
+
+moe_status do_index(moe_ctx* c, int n, cudaStream_t s) {
+  for (auto& cd : c->local) {
+    size_t sl;
+    span_begin(c, MOE_STAGE_INDEX, 0, s, &sl);
+    if (moe_status st = build_index(cd.v.experts, c->d.tokens, c->d.top_k, c->d.num_experts, n,
+                                    cd.v.perm_src, cd.v.expert_of, cd.v.slot_pos, cd.v.counts,
+                                    cd.v.expert_offsets, cd.err, s))
+      return st;
+    span_end(c, sl, s);
+    ++c->launches;
+  }
+  return MOE_OK;
+}
+
+// Count exchange + plan.  Each card pushes its node's per-chunk counts into
+// the count table of every card of its expert-parallel group (same rho).
+moe_status do_counts_and_plan(moe_ctx* c, int level, int n, int landing, cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  for (auto& cd : c->local) {
+    PushCountsArgs pa{};
+    pa.counts = cd.v.counts;
+    pa.n = n;
+    pa.E = d.num_experts;
+    pa.max_chunks = d.max_chunks;
+    pa.node = cd.node;
+    pa.n_dst = 0;
+    pa.sig = no_signal();
+    pa.sig.epoch = c->epoch;
+    for (int x = 0; x < d.e; ++x) {
+      const int dst = card_of(c, x, cd.rho);
+      pa.dst_tables[pa.n_dst++] = c->peer[dst].count_table;
+      if (!is_virtual(c) && dst != cd.id) pa.sig.flags[pa.sig.n++] = flag_at(c, dst, kSigCounts, cd.id);
+    }
+    MONTA_CUDA(launch_push_counts(pa, s));
+    ++c->launches;
+  }
+  for (auto& cd : c->local) {
+    PlanArgs a{};
+    a.count_table = cd.count_table;
+    a.e = d.e;
+    a.t = d.t;
+    a.E = d.num_experts;
+    a.L = c->L;
+    a.n = n;
+    a.max_chunks = d.max_chunks;
+    a.node = cd.node;
+    a.rho = cd.rho;
+    a.level = level;
+    a.landing = landing;
+    a.row_bytes = c->row_bytes;
+    a.seg_cap = d.num_experts;
+    a.lists = cd.lists;
+    a.local_delta = cd.local_delta;
+    a.recv_rows = cd.recv_rows;
+    a.err = cd.err;
+    a.wait = no_wait();
+    a.wait.epoch = c->epoch;
+    if (!is_virtual(c))
+      for (int x = 0; x < d.e; ++x) {
+        const int src = card_of(c, x, cd.rho);
+        if (src != cd.id) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, kSigCounts, src);
+      }
+    MONTA_CUDA(launch_plan_with_scratch(a, cd.scratch, s));
+    ++c->launches;
+  }
+  return MOE_OK;
+}
+
+int copy_vec(const moe_ctx* c, bool dedup) {
+  return vec_bytes(c->row_bytes, dedup ? c->row_bytes / c->d.t : c->row_bytes);
+}
+
+// One chunk of the fused permute + AllToAll, for one card.
+moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaStream_t s, bool concurrent) {
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  CopyArgs a{};
+  a.list = list_of(c, cd, kPhaseAA, j);
+  a.src = static_cast<const char*>(cd.v.x);
+  a.src_stride = c->row_bytes;
+  a.gather = cd.v.perm_src;
+  a.src_tags = nullptr;
+  a.token_ids = cd.v.token_ids;
+  a.source_card = card_of(c, cd.node, 0);
+  a.synth_tags = 1;
+  a.dst_stride = c->row_bytes;
+  a.dst_mask = 0;
+  for (int q = 0; q < c->cards; ++q) {
+    if (!c->peer[q].slab) continue;
+    a.dst[q] = landing == MOE_LAND_STAGED ? c->peer[q].pre : c->peer[q].recv;
+    a.dst_tags[q] = landing == MOE_LAND_STAGED ? c->peer[q].pre_tags : c->peer[q].recv_tags;
+  }
+  a.wait = no_wait();
+  a.sig = no_signal();
+  a.sig.epoch = c->epoch;
+  a.sig.done = cd.done + kPsAA * d.max_chunks + j;
+  if (!is_virtual(c))
+    for (int x = 0; x < d.e; ++x)
+      if (x != cd.node) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, x, cd.rho), sig_chunk(c, kPsAA, j), cd.id);
+  a.err = cd.err;
+  size_t sl;
+  span_begin(c, MOE_STAGE_AA, j, s, &sl);
+  MONTA_CUDA(launch_seg_copy(a, copy_vec(c, dedup), copy_grid(c, concurrent, true), s));
+  span_end(c, sl, s);
+  ++c->launches;
+  return MOE_OK;
+}
+
+// One chunk of the intra-node AllGather (forward this rank's slice of the
+// rows that arrived from other nodes to every TP peer).
+moe_status launch_ag(moe_ctx* c, Card& cd, int j, int landing, cudaStream_t s, bool concurrent) {
+  const moe_layer_desc& d = c->d;
+  CopyArgs a{};
+  a.list = list_of(c, cd, kPhaseAG, j);
+  const bool staged = landing == MOE_LAND_STAGED;
+  a.src = staged ? static_cast<const char*>(cd.v.pre) : static_cast<const char*>(cd.v.recv);
+  a.src_stride = c->row_bytes;
+  a.gather = nullptr;
+  a.src_tags = staged ? cd.v.pre_tags : cd.v.recv_tags;
+  a.synth_tags = 0;
+  a.dst_stride = c->row_bytes;
+  a.dst_mask = 0;
+  for (int r = 0; r < d.t; ++r) {
+    const int q = card_of(c, cd.node, r);
+    if (q == cd.id) continue;
+    a.dst_mask |= 1ull << q;
+    a.dst[q] = staged ? c->peer[q].pre : c->peer[q].recv;
+    a.dst_tags[q] = staged ? c->peer[q].pre_tags : c->peer[q].recv_tags;
+  }
+  a.wait = no_wait();
+  a.wait.epoch = c->epoch;
+  a.sig = no_signal();
+  a.sig.epoch = c->epoch;
+  a.sig.done = cd.done + kPsAG * d.max_chunks + j;
+  if (!is_virtual(c)) {
+    for (int g = 0; g < d.e; ++g)
+      if (g != cd.node) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, sig_chunk(c, kPsAA, j), card_of(c, g, cd.rho));
+    for (int r = 0; r < d.t; ++r)
+      if (r != cd.rho) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, cd.node, r), sig_chunk(c, kPsAG, j), cd.id);
+  }
+  a.err = cd.err;
+  size_t sl;
+  span_begin(c, MOE_STAGE_AG, j, s, &sl);
+  MONTA_CUDA(launch_seg_copy(a, copy_vec(c, true), copy_grid(c, concurrent, false), s));
+  span_end(c, sl, s);
+  ++c->launches;
+  return MOE_OK;
+}
+
+moe_status launch_d2d(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bool concurrent) {
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  CopyArgs a{};
+  a.list = list_of(c, cd, kPhaseD2D, j);
+  a.src = static_cast<const char*>(cd.v.pre);
+  a.src_stride = c->row_bytes;
+  a.src_tags = cd.v.pre_tags;
+  a.synth_tags = 0;
+  a.dst_stride = c->row_bytes;
+  a.dst[cd.id] = static_cast<char*>(cd.v.recv);
+  a.dst_tags[cd.id] = cd.v.recv_tags;
+  a.wait = no_wait();
+  a.wait.epoch = c->epoch;
+  if (!is_virtual(c)) {
+    for (int g = 0; g < d.e; ++g)
+      if (g != cd.node) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, sig_chunk(c, kPsAA, j), card_of(c, g, cd.rho));
+    if (dedup)
+      for (int r = 0; r < d.t; ++r)
+        if (r != cd.rho) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, sig_chunk(c, kPsAG, j), card_of(c, cd.node, r));
+  }
+  a.sig = no_signal();
+  a.err = cd.err;
+  size_t sl;
+  span_begin(c, MOE_STAGE_D2D, j, s, &sl);
+  MONTA_CUDA(launch_seg_copy(a, copy_vec(c, false), copy_grid(c, concurrent, false), s));
+  span_end(c, sl, s);
+  ++c->launches;
+  return MOE_OK;
+}
+
+// Wait (on stream s) until every remote contribution of the dispatch landed.
+moe_status dispatch_tail_wait(moe_ctx* c, Card& cd, int level, int n, int landing, cudaStream_t s) {
+  if (is_virtual(c)) return MOE_OK;
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  if (landing == MOE_LAND_STAGED) return MOE_OK;  // every D2D already waited
+  WaitList w = no_wait();
+  w.epoch = c->epoch;
+  for (int j = 0; j < n; ++j) {
+    const int need = dedup ? d.t - 1 : d.e - 1;
+    if (w.n + need > kMaxCards) {
+      MONTA_CUDA(launch_wait(w, cd.err, s));
+      ++c->launches;
+      w.n = 0;
+    }
+    if (dedup) {
+      for (int r = 0; r < d.t; ++r)
+        if (r != cd.rho) w.flags[w.n++] = flag_at(c, cd.id, sig_chunk(c, kPsAG, j), card_of(c, cd.node, r));
+    } else {
+      for (int g = 0; g < d.e; ++g)
+        if (g != cd.node) w.flags[w.n++] = flag_at(c, cd.id, sig_chunk(c, kPsAA, j), card_of(c, g, cd.rho));
+    }
+  }
+  if (w.n) {
+    MONTA_CUDA(launch_wait(w, cd.err, s));
+    ++c->launches;
+  }
+  return MOE_OK;
+}
+
+moe_status validate_dispatch(moe_ctx* c, int level, int n, int landing) {
+  const moe_layer_desc& d = c->d;
+  if (level == MOE_BASELINE) {
+    if (n != 1) return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_monolithic is unchunked (n = 1)");
+  } else {
+    if (level != MOE_O1 && level != MOE_O2 && level != MOE_O3)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_chunked: level must be O1, O2 or O3");
+    if (n < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_chunked: n must be >= 1");
+    if (level == MOE_O1 && n != 1)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_chunked: O1 is unchunked (n = 1)");
+  }
+  if (n > d.max_chunks)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch: n = %d exceeds the context's max_chunks %d", n, d.max_chunks);
+  if (d.tokens % n != 0) return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_chunked: n does not divide the sequence");
+  if (level != MOE_BASELINE && d.hidden % d.t != 0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_chunked: tensor group must evenly split the payload");
+  if (landing != MOE_LAND_FINAL && landing != MOE_LAND_STAGED)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch: bad landing mode");
+  return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" moe_status moe_ctx_route(moe_ctx* c, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  return do_route(c, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" moe_status moe_ctx_permute(moe_ctx* c, int32_t n, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (n < 1 || n > c->d.max_chunks || c->d.tokens % n != 0)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "permute: bad chunk count %d", n);
+  if (moe_status st = do_index(c, n, s)) return st;
+  for (auto& cd : c->local) {
+    MONTA_CUDA(launch_gather_rows(cd.v.x, c->row_bytes, 0, c->row_bytes, cd.v.perm_src, c->R, cd.v.permuted,
+                                  c->row_bytes, s));
+    ++c->launches;
+  }
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_dispatch(moe_ctx* c, int level, int32_t n, int landing, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const moe_layer_desc& d = c->d;
+  if (level == MOE_BASELINE) landing = MOE_LAND_FINAL;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  const bool staged = landing == MOE_LAND_STAGED;
+  ++c->epoch;
+  c->last_level = level;
+  c->last_n = n;
+  c->last_landing = landing;
+  if (c->timing && !c->in_forward) {
+    c->span_used = 0;
+    cudaEventRecord(c->ev_base, s);
+  }
+  if (moe_status st = do_index(c, n, s)) return st;
+  if (moe_status st = do_counts_and_plan(c, level, n, landing, s)) return st;
+
+  if (is_virtual(c)) {
+    for (int j = 0; j < n; ++j) {
+      for (auto& cd : c->local)
+        if (moe_status st = launch_aa(c, cd, level, j, landing, s, false)) return st;
+      if (dedup)
+        for (auto& cd : c->local)
+          if (moe_status st = launch_ag(c, cd, j, landing, s, false)) return st;
+      if (staged)
+        for (auto& cd : c->local)
+          if (moe_status st = launch_d2d(c, cd, level, j, s, false)) return st;
+    }
+    return MOE_OK;
+  }
+  // multi-GPU: one card per rank; AllToAll on the high-priority stream,
+  // AllGather on its own stream, reorder copies on the AllGather stream (O2)
+  // or their own (O3).
+  Card& cd = c->local[0];
+  cudaStream_t s_d2d = level == MOE_O3 ? c->s_d2d : c->s_ag;
+  MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_aa, c->ev_fork, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_ag, c->ev_fork, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_d2d, c->ev_fork, 0));
+  for (int j = 0; j < n; ++j) {
+    if (moe_status st = launch_aa(c, cd, level, j, landing, c->s_aa, true)) return st;
+    MONTA_CUDA(cudaEventRecord(c->ev_aa[j], c->s_aa));
+    if (dedup) {
+      if (moe_status st = launch_ag(c, cd, j, landing, c->s_ag, true)) return st;
+      MONTA_CUDA(cudaEventRecord(c->ev_ag[j], c->s_ag));
+    }
+    if (staged) {
+      MONTA_CUDA(cudaStreamWaitEvent(s_d2d, c->ev_aa[j], 0));
+      if (dedup) MONTA_CUDA(cudaStreamWaitEvent(s_d2d, c->ev_ag[j], 0));
+      if (moe_status st = launch_d2d(c, cd, level, j, s_d2d, true)) return st;
+    }
+  }
+  MONTA_CUDA(cudaEventRecord(c->ev_join_aa, c->s_aa));
+  MONTA_CUDA(cudaEventRecord(c->ev_join_ag, c->s_ag));
+  MONTA_CUDA(cudaEventRecord(c->ev_join_d2d, c->s_d2d));
+  MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_aa, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_ag, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_d2d, 0));
+  return dispatch_tail_wait(c, cd, level, n, landing, s);
+}
+
+namespace {
+
+moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bool concurrent) {
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  CopyArgs a{};
+  a.list = list_of(c, cd, kPhaseCAA, j);
+  a.src = static_cast<const char*>(cd.v.expert_out);
+  a.src_stride = c->row_bytes;
+  a.synth_tags = 0;
+  a.dst_stride = c->row_bytes;
+  for (int q = 0; q < c->cards; ++q)
+    if (c->peer[q].slab) a.dst[q] = c->peer[q].comb;
+  a.wait = no_wait();
+  a.sig = no_signal();
+  a.sig.epoch = c->epoch;
+  a.sig.done = cd.done + kPsCAA * d.max_chunks + j;
+  if (!is_virtual(c))
+    for (int g = 0; g < d.e; ++g)
+      if (g != cd.node) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, g, cd.rho), sig_chunk(c, kPsCAA, j), cd.id);
+  a.err = cd.err;
+  size_t sl;
+  span_begin(c, MOE_STAGE_CAA, j, s, &sl);
+  MONTA_CUDA(launch_seg_copy(a, copy_vec(c, dedup), copy_grid(c, concurrent, true), s));
+  span_end(c, sl, s);
+  ++c->launches;
+  return MOE_OK;
+}
+
+moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStream_t s, bool concurrent) {
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  UnpermArgs a{};
+  a.comb = static_cast<const char*>(cd.v.comb);
+  a.local_y = static_cast<const char*>(cd.v.expert_out);
+  a.local_delta = cd.local_delta;
+  a.local_lo = cd.node * c->L;
+  a.local_hi = (cd.node + 1) * c->L;
+  a.y_stride = c->row_bytes;
+  a.slot_pos = cd.v.slot_pos;
+  a.experts = cd.v.experts;
+  a.probs = cd.v.probs;
+  a.k = d.top_k;
+  const int64_t ct = d.tokens / n;
+  a.tok_begin = int64_t(j) * ct;
+  a.tok_end = a.tok_begin + ct;
+  a.col_begin = dedup ? int64_t(cd.rho) * (d.hidden / d.t) : 0;
+  a.cols = dedup ? d.hidden / d.t : d.hidden;
+  a.out_stride = d.hidden * int64_t(c->ob);
+  a.n_out = 0;
+  if (dedup) {
+    for (int r = 0; r < d.t; ++r) a.out[a.n_out++] = c->peer[card_of(c, cd.node, r)].out;
+  } else {
+    a.out[a.n_out++] = static_cast<char*>(cd.v.out);
+  }
+  a.wait = no_wait();
+  a.wait.epoch = c->epoch;
+  a.sig = no_signal();
+  a.sig.epoch = c->epoch;
+  a.sig.done = cd.done + kPsCAG * d.max_chunks + j;
+  if (!is_virtual(c)) {
+    for (int x = 0; x < d.e; ++x)
+      if (x != cd.node) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, sig_chunk(c, kPsCAA, j), card_of(c, x, cd.rho));
+    if (dedup)
+      for (int r = 0; r < d.t; ++r)
+        if (r != cd.rho) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, cd.node, r), sig_chunk(c, kPsCAG, j), cd.id);
+  }
+  a.err = cd.err;
+  int grid = c->sms * (concurrent ? 2 : 4);
+  const int64_t need = (ct + 7) / 8;
+  if (need < grid) grid = int(std::max<int64_t>(need, 1));
+  size_t sl;
+  span_begin(c, MOE_STAGE_UNPERMUTE, j, s, &sl);
+  bool ok = true;
+  MONTA_CUDA(launch_unpermute(a, d.dtype, d.logit_dtype, d.out_dtype, grid, s, &ok));
+  if (!ok) return fail(MOE_ERR_UNSUPPORTED, "combine: unsupported dtype combination (payload %d -> out %d)",
+                       d.dtype, d.out_dtype);
+  span_end(c, sl, s);
+  ++c->launches;
+  return MOE_OK;
+}
+
+}  // namespace
+
+extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  if (c->last_level < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "combine: no dispatch to mirror");
+  if (n != c->last_n) return fail(MOE_ERR_INVALID_ARGUMENT, "combine: n = %d differs from the dispatch's %d", n, c->last_n);
+  const bool dedup_d = c->last_level != MOE_BASELINE && c->d.t > 1;
+  const bool dedup = level != MOE_BASELINE && c->d.t > 1;
+  if (dedup != dedup_d)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine: level must mirror the dispatch (baseline vs deduplicated)");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const moe_layer_desc& d = c->d;
+  ++c->epoch;
+  if (is_virtual(c)) {
+    for (int j = 0; j < n; ++j) {
+      for (auto& cd : c->local)
+        if (moe_status st = launch_caa(c, cd, level, j, s, false)) return st;
+      for (auto& cd : c->local)
+        if (moe_status st = launch_unperm(c, cd, level, n, j, s, false)) return st;
+    }
+    return MOE_OK;
+  }
+  Card& cd = c->local[0];
+  if (dedup && d.e == 1) {
+    // Nothing orders a TP peer's output stores after this rank's previous
+    // read of `out` when there is no cross-node leg: barrier the node.
+    SignalList sg = no_signal();
+    sg.epoch = c->epoch;
+    WaitList w = no_wait();
+    w.epoch = c->epoch;
+    for (int r = 0; r < d.t; ++r)
+      if (r != cd.rho) {
+        sg.flags[sg.n++] = flag_at(c, card_of(c, cd.node, r), kSigBarrier, cd.id);
+        w.flags[w.n++] = flag_at(c, cd.id, kSigBarrier, card_of(c, cd.node, r));
+      }
+    MONTA_CUDA(launch_signal(sg, s));
+    MONTA_CUDA(launch_wait(w, cd.err, s));
+    c->launches += 2;
+  }
+  MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_aa, c->ev_fork, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_ag, c->ev_fork, 0));
+  for (int j = 0; j < n; ++j) {
+    if (moe_status st = launch_caa(c, cd, level, j, c->s_aa, true)) return st;
+    if (moe_status st = launch_unperm(c, cd, level, n, j, c->s_ag, true)) return st;
+  }
+  MONTA_CUDA(cudaEventRecord(c->ev_join_aa, c->s_aa));
+  MONTA_CUDA(cudaEventRecord(c->ev_join_ag, c->s_ag));
+  MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_aa, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_ag, 0));
+  if (dedup) {
+    WaitList w = no_wait();
+    w.epoch = c->epoch;
+    for (int j = 0; j < n; ++j) {
+      if (w.n + d.t - 1 > kMaxCards) {
+        MONTA_CUDA(launch_wait(w, cd.err, s));
+        ++c->launches;
+        w.n = 0;
+      }
+      for (int r = 0; r < d.t; ++r)
+        if (r != cd.rho) w.flags[w.n++] = flag_at(c, cd.id, sig_chunk(c, kPsCAG, j), card_of(c, cd.node, r));
+    }
+    if (w.n) {
+      MONTA_CUDA(launch_wait(w, cd.err, s));
+      ++c->launches;
+    }
+  }
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_forward(moe_ctx* c, int level, int32_t n, int landing, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->timing) {
+    c->span_used = 0;
+    cudaEventRecord(c->ev_base, s);
+  }
+  c->in_forward = true;
+  moe_status st = do_route(c, s);
+  if (st == MOE_OK) st = moe_ctx_dispatch(c, level, n, landing, stream);
+  c->in_forward = false;
+  if (st != MOE_OK) return st;
+  return moe_ctx_combine(c, level, n, stream);
+}
+
+extern "C" moe_status moe_ctx_forward_host(moe_ctx* c, int level, int32_t n, int landing,
+                                           const void* host_x, const void* host_logits, void* host_out,
+                                           void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (!host_x || !host_logits || !host_out) return fail(MOE_ERR_INVALID_ARGUMENT, "forward_host: null buffer");
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const moe_layer_desc& d = c->d;
+  const size_t xbytes = size_t(d.tokens) * c->row_bytes;
+  const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;
+  const size_t obytes = size_t(d.tokens) * d.hidden * c->ob;
+  for (size_t i = 0; i < c->local.size(); ++i) {
+    MONTA_CUDA(cudaMemcpyAsync(c->local[i].v.x, static_cast<const char*>(host_x) + i * xbytes, xbytes,
+                               cudaMemcpyHostToDevice, s));
+    MONTA_CUDA(cudaMemcpyAsync(c->local[i].v.logits, static_cast<const char*>(host_logits) + i * lbytes,
+                               lbytes, cudaMemcpyHostToDevice, s));
+  }
+  if (moe_status st = moe_ctx_forward(c, level, n, landing, stream)) return st;
+  for (size_t i = 0; i < c->local.size(); ++i)
+    MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(host_out) + i * obytes, c->local[i].v.out, obytes,
+                               cudaMemcpyDeviceToHost, s));
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_recv_rows(moe_ctx* c, int card, int64_t* rows) {
+  if (!c || !rows) return fail(MOE_ERR_INVALID_ARGUMENT, "recv_rows: null argument");
+  MONTA_CUDA(cudaSetDevice(c->device));
+  for (auto& cd : c->local)
+    if (cd.id == card) {
+      MONTA_CUDA(cudaDeviceSynchronize());
+      MONTA_CUDA(cudaMemcpy(rows, cd.recv_rows, 8, cudaMemcpyDeviceToHost));
+      return MOE_OK;
+    }
+  return fail(MOE_ERR_INVALID_ARGUMENT, "recv_rows: card %d is not local", card);
+}
+
+extern "C" moe_status moe_ctx_sync(moe_ctx* c) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "sync: null ctx");
+  MONTA_CUDA(cudaSetDevice(c->device));
+  MONTA_CUDA(cudaDeviceSynchronize());
+  for (auto& cd : c->local) {
+    int32_t e = 0;
+    MONTA_CUDA(cudaMemcpy(&e, cd.err, 4, cudaMemcpyDeviceToHost));
+    if (e != 0) {
+      const int32_t zero = 0;
+      cudaMemcpy(cd.err, &zero, 4, cudaMemcpyHostToDevice);
+      if (e == MOE_ERR_TIMEOUT) return fail(MOE_ERR_TIMEOUT, "card %d: cross-GPU flag wait timed out", cd.id);
+      if (e == MOE_ERR_INVALID_ARGUMENT)
+        return fail(MOE_ERR_INVALID_ARGUMENT, "card %d: expert id out of range in the routing", cd.id);
+      return fail(moe_status(e), "card %d: device error %d", cd.id, e);
+    }
+  }
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_enable_timing(moe_ctx* c, int enable) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "enable_timing: null ctx");
+  c->timing = enable != 0;
+  c->span_used = 0;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_spans(moe_ctx* c, moe_span* spans, int32_t capacity, int32_t* n_spans) {
+  if (!c || !n_spans) return fail(MOE_ERR_INVALID_ARGUMENT, "spans: null argument");
+  *n_spans = 0;
+  if (!c->timing) return MOE_OK;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  MONTA_CUDA(cudaDeviceSynchronize());
+  for (size_t i = 0; i < c->span_used && int32_t(i) < capacity; ++i) {
+    const Span& sp = c->spans[i];
+    float a = 0, b = 0;
+    MONTA_CUDA(cudaEventElapsedTime(&a, c->ev_base, sp.a));
+    MONTA_CUDA(cudaEventElapsedTime(&b, c->ev_base, sp.b));
+    spans[i] = moe_span{sp.stage, sp.chunk, a, b};
+    ++*n_spans;
+  }
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_set_aa_ctas(moe_ctx* c, int32_t ctas) {
+  if (!c || ctas < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "set_aa_ctas: bad argument");
+  c->aa_ctas = ctas;
+  return MOE_OK;
+}
+
+extern "C" int64_t moe_ctx_launch_count(const moe_ctx* c) { return c ? c->launches : 0; }

@@ -1,0 +1,125 @@
+// Data structures shared by the layer context (ctx.cu) and the movement /
+// combine kernels (copy.cu, combine.cu, plan.cu).
+#pragma once
+
+#include "common.cuh"
+
+namespace monta {
+
+// One contiguous run of rows moved by a copy kernel.  A list of these (built
+// on the device by the plan kernel from the exchanged counts) describes one
+// (phase, chunk) of the exchange, so no host round trip is needed to learn
+// the dynamic row counts.
+struct Seg {
+  int64_t row_begin;  // exclusive prefix of `rows` over the list
+  int64_t src_row;    // first source row (AA: index into the sender's permuted order)
+  int64_t dst_row;    // first destination row
+  int32_t rows;
+  int32_t dst;        // destination card id, or -1: every card in dst_mask
+  int32_t col_off;    // byte offset of the moved column slice
+  int32_t width;      // bytes moved per row
+  int32_t expert;     // global expert id (tag synthesis)
+  int32_t pad;
+};
+static_assert(sizeof(Seg) == 48, "Seg layout");
+
+struct SegList {
+  int32_t nseg;
+  int32_t pad;
+  int64_t total_rows;
+  Seg segs[1];  // [capacity]
+};
+__host__ __device__ inline size_t seglist_bytes(int cap) { return 16 + size_t(cap) * sizeof(Seg); }
+
+enum SegPhase { kPhaseAA = 0, kPhaseAG = 1, kPhaseD2D = 2, kPhaseCAA = 3, kNumPhases = 4 };
+
+// Signals carried in each card's flag array: flags[(sig) * kMaxCards + sender].
+enum Signal {
+  kSigCounts = 0,
+  kSigBarrier = 1,
+  kSigChunkBase = 2,  // + phase_signal * max_chunks + j
+};
+enum PhaseSignal { kPsAA = 0, kPsAG = 1, kPsCAA = 2, kPsCAG = 3, kNumPhaseSignals = 4 };
+
+struct CopyArgs {
+  const SegList* list;
+  const char* src;
+  int64_t src_stride;        // bytes per source row
+  const int32_t* gather;     // AA: perm_src; row = gather[seg.src_row + i]
+  const int32_t* src_tags;   // int4 per source row (COPY), or null
+  const int32_t* token_ids;  // AA tag synthesis
+  int32_t source_card;       // AA tag synthesis
+  int32_t synth_tags;        // 1: AA synthesises tags, 0: copy src_tags (if any)
+  int64_t dst_stride;        // bytes per destination row
+  uint64_t dst_mask;         // seg.dst == -1 targets
+  char* dst[kMaxCards];
+  int32_t* dst_tags[kMaxCards];
+  WaitList wait;
+  SignalList sig;
+  int32_t* err;
+};
+
+struct UnpermArgs {
+  const char* comb;          // [R, h] landing buffer (sender-permuted order)
+  const char* local_y;       // expert outputs of this card's own node (final layout), or null
+  const int32_t* local_delta;  // [E] row delta permuted->final for own-node experts, or null
+  int32_t local_lo, local_hi;  // own-node experts [lo, hi)
+  int64_t y_stride;          // bytes per row (comb and local_y)
+  const int32_t* slot_pos;   // [T, k]
+  const int32_t* experts;    // [T, k]
+  const void* probs;         // [T, k]
+  int32_t k;
+  int64_t tok_begin, tok_end;
+  int64_t col_begin, cols;   // element columns to produce
+  int64_t out_stride;        // bytes per output row
+  int32_t n_out;
+  char* out[kMaxCards];      // every destination (fused all-gather)
+  WaitList wait;
+  SignalList sig;
+  int32_t* err;
+};
+
+// Launchers (return cudaGetLastError()).
+cudaError_t launch_seg_copy(const CopyArgs& a, int vec, int grid, cudaStream_t s);
+cudaError_t launch_gather_rows(const void* src, int64_t src_stride, int64_t col_off, int64_t width,
+                               const int32_t* perm, int64_t R, void* out, int64_t out_stride,
+                               cudaStream_t s);
+cudaError_t launch_unpermute(const UnpermArgs& a, int y_dtype, int probs_dtype, int out_dtype,
+                             int grid, cudaStream_t s, bool* supported);
+cudaError_t launch_wait(const WaitList& w, int32_t* err, cudaStream_t s);
+cudaError_t launch_signal(const SignalList& sg, cudaStream_t s);
+
+// Plan kernel (plan.cu).
+struct PlanArgs {
+  const int32_t* count_table;  // [e][max_chunks][E]
+  int32_t e, t, E, L, n, max_chunks;
+  int32_t node, rho;
+  int32_t level, landing;
+  int64_t row_bytes;           // full row bytes (h * elem)
+  int32_t seg_cap;             // capacity of each list
+  SegList* lists;              // [kNumPhases][max_chunks] lists, stride seglist_bytes(seg_cap)
+  int32_t* local_delta;        // [E]
+  int64_t* recv_rows;          // [1]
+  WaitList wait;
+  int32_t* err;
+};
+size_t plan_scratch_ints(int e, int E, int max_chunks);
+cudaError_t launch_plan_with_scratch(const PlanArgs& a, int32_t* scratch, cudaStream_t s);
+size_t index_smem_bytes(int E);
+// Push this card's per-chunk counts into the count tables of its peers.
+struct PushCountsArgs {
+  const int32_t* counts;      // [n][E]
+  int32_t n, E, max_chunks, node;
+  int32_t n_dst;
+  int32_t* dst_tables[kMaxCards];
+  SignalList sig;
+};
+cudaError_t launch_push_counts(const PushCountsArgs& a, cudaStream_t s);
+
+moe_status route_topk(const void* logits, int logit_dtype, int64_t T, int E, int k, int32_t* experts,
+                      void* probs, cudaStream_t stream);
+moe_status build_index(const int32_t* experts, int64_t T, int k, int E, int n_chunks,
+                       int32_t* perm_src, int32_t* expert_of, int32_t* slot_pos, int32_t* counts,
+                       int32_t* expert_offsets, int32_t* dev_error, cudaStream_t stream);
+
+}  // namespace monta

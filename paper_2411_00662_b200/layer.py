@@ -1,0 +1,208 @@
+"""Device-level API: one MoE layer's dispatch + combine over e x t cards.
+
+`MoeLayer` owns a `moe_ctx` from the C ABI.  Every buffer lives in the
+context's per-card HBM slab; the properties below are zero-copy torch views
+of it (via __cuda_array_interface__) so callers fill inputs and read outputs
+in place.  Views must not outlive the layer.
+
+    world_size == 1      : all e*t cards on one GPU (virtual mode — the
+                           reference's single-process emulation)
+    world_size == e*t    : one card per process/GPU; `connect()` exchanges
+                           CUDA IPC handles through torch.distributed so every
+                           card can store into its peers over NVLink.
+
+Reference mapping (dataplane.hpp):  route -> route_topk,  permute -> permute,
+dispatch(BASELINE) -> dispatch_monolithic,  dispatch(O1/O2/O3, n) ->
+dispatch_chunked,  combine -> combine_unpermute.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import BASELINE, O1, O2, O3, LAND_FINAL, LAND_STAGED, check
+
+_TYPESTR = {torch.float32: "<f4", torch.float64: "<f8", torch.int64: "<i8", torch.int32: "<i4",
+            torch.bfloat16: "<i2", torch.float16: "<f2", torch.uint8: "|u1"}
+
+
+class _CudaArray:
+    def __init__(self, ptr: int, shape, typestr: str):
+        self.__cuda_array_interface__ = {"shape": tuple(int(s) for s in shape), "typestr": typestr,
+                                         "data": (int(ptr), False), "version": 2, "strides": None}
+
+
+def device_view(ptr: int, shape, dtype: torch.dtype, device: int) -> torch.Tensor:
+    """Zero-copy torch view of device memory owned elsewhere."""
+    n = 1
+    for s in shape:
+        n *= int(s)
+    if n == 0:
+        return torch.empty(tuple(shape), dtype=dtype, device=f"cuda:{device}")
+    with torch.cuda.device(device):
+        t = torch.as_tensor(_CudaArray(ptr, shape, _TYPESTR[dtype]), device=f"cuda:{device}")
+    return t.view(dtype) if dtype is torch.bfloat16 else t
+
+
+@dataclass
+class CardTensors:
+    card: int
+    node: int
+    rho: int
+    x: torch.Tensor
+    logits: torch.Tensor
+    token_ids: torch.Tensor
+    experts: torch.Tensor
+    probs: torch.Tensor
+    perm_src: torch.Tensor
+    expert_of: torch.Tensor
+    slot_pos: torch.Tensor
+    counts: torch.Tensor
+    expert_offsets: torch.Tensor
+    permuted: torch.Tensor
+    recv: torch.Tensor
+    recv_tags: torch.Tensor
+    pre: torch.Tensor
+    pre_tags: torch.Tensor
+    comb: torch.Tensor
+    out: torch.Tensor
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        return torch.cuda.current_stream().cuda_stream
+    return stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream)
+
+
+class MoeLayer:
+    def __init__(self, e: int, t: int, num_experts: int, top_k: int, tokens: int, hidden: int,
+                 dtype: torch.dtype = torch.bfloat16, logit_dtype: torch.dtype = torch.float32,
+                 out_dtype: torch.dtype | None = None, max_chunks: int = 64, device: int = 0,
+                 rank: int = 0, world_size: int = 1):
+        self.lib = _lib.load()
+        self.e, self.t, self.E, self.k = e, t, num_experts, top_k
+        self.T, self.h = tokens, hidden
+        self.dtype, self.logit_dtype = dtype, logit_dtype
+        self.out_dtype = out_dtype or dtype
+        self.max_chunks = max_chunks
+        self.device, self.rank, self.world_size = device, rank, world_size
+        self.L = num_experts // e if e else 0
+        desc = _lib.LayerDesc(e, t, num_experts, top_k, tokens, hidden, _lib.dtype_code(dtype),
+                              _lib.dtype_code(logit_dtype), _lib.dtype_code(self.out_dtype), max_chunks)
+        self._ctx = C.c_void_p()
+        check(self.lib.moe_ctx_create(C.byref(desc), device, rank, world_size, C.byref(self._ctx)))
+        n_local = self.lib.moe_ctx_num_local_cards(self._ctx)
+        first = self.lib.moe_ctx_first_card(self._ctx)
+        self.local_cards = list(range(first, first + n_local))
+        self._cards = {c: self._make_card(c) for c in self.local_cards}
+
+    # ------------------------------------------------------------------ views
+    def _make_card(self, card: int) -> CardTensors:
+        v = _lib.CardView()
+        check(self.lib.moe_ctx_card_view(self._ctx, card, C.byref(v)))
+        T, h, E, k, dev = self.T, self.h, self.E, self.k, self.device
+        R, cap = v.rows_permuted, v.recv_cap
+        i32 = torch.int32
+        mk = lambda p, shape, dt: device_view(p, shape, dt, dev)  # noqa: E731
+        return CardTensors(
+            card=card, node=card // self.t, rho=card % self.t,
+            x=mk(v.x, (T, h), self.dtype), logits=mk(v.logits, (T, E), self.logit_dtype),
+            token_ids=mk(v.token_ids, (T,), i32), experts=mk(v.experts, (T, k), i32),
+            probs=mk(v.probs, (T, k), self.logit_dtype), perm_src=mk(v.perm_src, (R,), i32),
+            expert_of=mk(v.expert_of, (R,), i32), slot_pos=mk(v.slot_pos, (T, k), i32),
+            counts=mk(v.counts, (self.max_chunks, E), i32), expert_offsets=mk(v.expert_offsets, (E + 1,), i32),
+            permuted=mk(v.permuted, (R, h), self.dtype), recv=mk(v.recv, (cap, h), self.dtype),
+            recv_tags=mk(v.recv_tags, (cap, 4), i32), pre=mk(v.pre, (cap, h), self.dtype),
+            pre_tags=mk(v.pre_tags, (cap, 4), i32), comb=mk(v.comb, (R, h), self.dtype),
+            out=mk(v.out, (T, h), self.out_dtype))
+
+    def card(self, c: int) -> CardTensors:
+        return self._cards[c]
+
+    @property
+    def cards(self) -> list[CardTensors]:
+        return [self._cards[c] for c in self.local_cards]
+
+    # ------------------------------------------------------------ multi-GPU
+    def connect(self, group=None) -> None:
+        """Exchange IPC handles with every rank (torch.distributed must be up)."""
+        if self.world_size == 1:
+            return
+        import torch.distributed as dist
+        size = self.lib.moe_ctx_ipc_handle_size()
+        blob = (C.c_char * size)()
+        check(self.lib.moe_ctx_ipc_export(self._ctx, blob))
+        mine = bytes(blob)
+        allb: list = [None] * self.world_size
+        dist.all_gather_object(allb, mine, group=group)
+        joined = b"".join(allb)
+        buf = (C.c_char * len(joined)).from_buffer_copy(joined)
+        check(self.lib.moe_ctx_ipc_connect(self._ctx, buf))
+
+    # ------------------------------------------------------------------ ops
+    def route(self, stream=None) -> None:
+        check(self.lib.moe_ctx_route(self._ctx, _stream_ptr(stream)))
+
+    def permute(self, n: int = 1, stream=None) -> None:
+        check(self.lib.moe_ctx_permute(self._ctx, n, _stream_ptr(stream)))
+
+    def dispatch(self, level: int = O1, n: int = 1, landing: int = LAND_FINAL, stream=None) -> None:
+        check(self.lib.moe_ctx_dispatch(self._ctx, level, n, landing, _stream_ptr(stream)))
+
+    def combine(self, level: int = O1, n: int = 1, stream=None) -> None:
+        check(self.lib.moe_ctx_combine(self._ctx, level, n, _stream_ptr(stream)))
+
+    def forward(self, level: int = O1, n: int = 1, landing: int = LAND_FINAL, stream=None) -> None:
+        check(self.lib.moe_ctx_forward(self._ctx, level, n, landing, _stream_ptr(stream)))
+
+    def forward_host(self, host_x: torch.Tensor, host_logits: torch.Tensor, host_out: torch.Tensor,
+                     level: int = O1, n: int = 1, landing: int = LAND_FINAL, stream=None) -> None:
+        """End to end from host buffers (pinned for async copies)."""
+        check(self.lib.moe_ctx_forward_host(self._ctx, level, n, landing, host_x.data_ptr(),
+                                            host_logits.data_ptr(), host_out.data_ptr(), _stream_ptr(stream)))
+
+    def bind_expert_out(self, card: int, tensor: torch.Tensor | None) -> None:
+        check(self.lib.moe_ctx_bind_expert_out(self._ctx, card, tensor.data_ptr() if tensor is not None else None))
+
+    def recv_rows(self, card: int) -> int:
+        r = C.c_int64()
+        check(self.lib.moe_ctx_recv_rows(self._ctx, card, C.byref(r)))
+        return int(r.value)
+
+    def sync(self) -> None:
+        check(self.lib.moe_ctx_sync(self._ctx))
+
+    def enable_timing(self, on: bool = True) -> None:
+        check(self.lib.moe_ctx_enable_timing(self._ctx, int(on)))
+
+    def spans(self) -> list[tuple[str, int, float, float]]:
+        cap = 4096
+        arr = (_lib.Span * cap)()
+        n = C.c_int32()
+        check(self.lib.moe_ctx_spans(self._ctx, arr, cap, C.byref(n)))
+        return [(_lib.STAGES[arr[i].stage], arr[i].chunk, arr[i].start_ms, arr[i].end_ms) for i in range(n.value)]
+
+    def set_aa_ctas(self, ctas: int) -> None:
+        check(self.lib.moe_ctx_set_aa_ctas(self._ctx, ctas))
+
+    @property
+    def launch_count(self) -> int:
+        return int(self.lib.moe_ctx_launch_count(self._ctx))
+
+    def close(self) -> None:
+        if getattr(self, "_ctx", None) and self._ctx.value:
+            self._cards = {}
+            self.lib.moe_ctx_destroy(self._ctx)
+            self._ctx = C.c_void_p()
+
+    def __del__(self):  # pragma: no cover
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+__all__ = ["MoeLayer", "CardTensors", "device_view", "BASELINE", "O1", "O2", "O3", "LAND_FINAL", "LAND_STAGED"]

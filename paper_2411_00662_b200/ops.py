@@ -1,0 +1,102 @@
+"""Stateless device ops over torch CUDA tensors (C ABI family 1).
+
+    route_topk        dataplane::route_topk       (dataplane.hpp:72-106)
+    build_index       dataplane::permute, index form (dataplane.hpp:118-140)
+    permute_rows      gather-permute of rows (or a hidden_shard column slice)
+    unpermute_combine weighted un-permute (dataplane.hpp:325-342)
+
+All run on the current CUDA stream; nothing here synchronises unless
+`check=True` asks for the device-side validation result.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import check
+
+
+def _stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def route_topk(logits: torch.Tensor, k: int):
+    """logits [T, E] fp32/fp64 (CUDA) -> (experts int32 [T, k] ascending, probs [T, k] logit dtype)."""
+    if logits.dim() != 2:
+        raise ValueError("route_topk: logits must be [T, E]")
+    logits = logits.contiguous()
+    T, E = logits.shape
+    experts = torch.empty((T, max(k, 0)), dtype=torch.int32, device=logits.device)
+    probs = torch.empty((T, max(k, 0)), dtype=logits.dtype, device=logits.device)
+    lib = _lib.load()
+    check(lib.moe_route_topk(logits.data_ptr(), _lib.dtype_code(logits.dtype), T, E, k, experts.data_ptr(),
+                             probs.data_ptr(), _stream()))
+    return experts, probs
+
+
+@dataclass
+class Index:
+    perm_src: torch.Tensor       # [T*k] int32 source token of permuted row r
+    expert_of: torch.Tensor      # [T*k] int32
+    slot_pos: torch.Tensor       # [T, k] int32 permuted row of (token, slot)
+    counts: torch.Tensor         # [n, E] int32 rows per (chunk, expert)
+    expert_offsets: torch.Tensor  # [E+1] int32
+
+
+def build_index(experts: torch.Tensor, num_experts: int, n_chunks: int = 1, check_range: bool = False,
+                check: bool | None = None) -> Index:
+    """Stable expert-major counting sort of the (token, slot) pairs."""
+    if check is not None:
+        check_range = check
+    experts = experts.contiguous().to(torch.int32)
+    T, k = experts.shape
+    dev = experts.device
+    R = T * k
+    idx = Index(torch.empty(R, dtype=torch.int32, device=dev), torch.empty(R, dtype=torch.int32, device=dev),
+                torch.empty((T, k), dtype=torch.int32, device=dev),
+                torch.empty((n_chunks, num_experts), dtype=torch.int32, device=dev),
+                torch.empty(num_experts + 1, dtype=torch.int32, device=dev))
+    err = torch.zeros(1, dtype=torch.int32, device=dev)
+    lib = _lib.load()
+    _lib.check(lib.moe_build_index(experts.data_ptr(), T, k, num_experts, n_chunks, idx.perm_src.data_ptr(),
+                                   idx.expert_of.data_ptr(), idx.slot_pos.data_ptr(), idx.counts.data_ptr(),
+                                   idx.expert_offsets.data_ptr(), err.data_ptr(), _stream()))
+    if check_range and int(err.item()) != 0:
+        raise _lib.InvalidArgument(int(err.item()), "build_index: expert id out of range")
+    return idx
+
+
+def permute_rows(x: torch.Tensor, perm_src: torch.Tensor, col_off: int = 0, width: int | None = None,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[r] = x[perm_src[r], col_off:col_off+width] (elements)."""
+    x = x.contiguous()
+    T, h = x.shape
+    width = h - col_off if width is None else width
+    R = perm_src.numel()
+    if out is None:
+        out = torch.empty((R, width), dtype=x.dtype, device=x.device)
+    es = x.element_size()
+    check(_lib.load().moe_permute_rows(x.data_ptr(), h * es, col_off * es, width * es,
+                                       perm_src.contiguous().data_ptr(), R, out.data_ptr(), out.stride(0) * es,
+                                       _stream()))
+    return out
+
+
+def unpermute_combine(y: torch.Tensor, slot_pos: torch.Tensor, probs: torch.Tensor,
+                      out_dtype: torch.dtype | None = None, out: torch.Tensor | None = None) -> torch.Tensor:
+    """out[i] = sum_s probs[i, s] * y[slot_pos[i, s]]  (fp32 acc; fp64 for f64/i64)."""
+    y = y.contiguous()
+    R, h = y.shape
+    T, k = slot_pos.shape
+    if out_dtype is None:
+        out_dtype = torch.float64 if y.dtype in (torch.float64, torch.int64) else y.dtype
+    if out is None:
+        out = torch.empty((T, h), dtype=out_dtype, device=y.device)
+    probs = probs.contiguous()
+    check(_lib.load().moe_unpermute_combine(y.data_ptr(), _lib.dtype_code(y.dtype), h, h,
+                                            slot_pos.contiguous().data_ptr(), probs.data_ptr(),
+                                            _lib.dtype_code(probs.dtype), T, k, out.data_ptr(),
+                                            _lib.dtype_code(out.dtype), out.stride(0), _stream()))
+    return out
