@@ -242,6 +242,15 @@ moe_status moe_ctx_spans(moe_ctx* ctx, moe_span* spans, int32_t capacity, int32_
 /* Cap the SMs used by the cross-group (AllToAll) copy kernels, emulating a
  * slow inter-node link ("B1-throttled" mode).  0 = no cap. */
 moe_status moe_ctx_set_aa_ctas(moe_ctx* ctx, int32_t ctas);
+/* Transport primitive (calibration / microbenchmarks, config 5): card-local
+ * rows [0, sum) of this card's `recv` buffer are stored, rows_per_card[c]
+ * of them to card c (consecutive source rows per destination), each row
+ * `row_bytes` wide, with the exchange's copy kernel on `grid` CTAs
+ * (0 = default).  A peer destination receives into its `recv` buffer over
+ * NVLink; this card itself receives into its `pre` buffer (a local D2D
+ * copy).  Only local + peer-mapped cards may be named. */
+moe_status moe_ctx_xfer(moe_ctx* ctx, const int64_t* rows_per_card, int32_t row_bytes, int32_t grid,
+                        void* stream);
 /* Number of kernels this context launched since creation. */
 int64_t moe_ctx_launch_count(const moe_ctx* ctx);
 

@@ -94,6 +94,8 @@ struct moe_ctx {
   std::vector<monta::Span> spans;
   size_t span_used = 0;
   int64_t launches = 0;
+  monta::SegList* xfer_list = nullptr;       // device
+  monta::SegList* xfer_host = nullptr;       // pinned staging
 };
 
 namespace monta {
@@ -354,6 +356,8 @@ extern "C" moe_status moe_ctx_destroy(moe_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
+  if (c->xfer_list) cudaFree(c->xfer_list);
+  if (c->xfer_host) cudaFreeHost(c->xfer_host);
   for (auto& cd : c->local) cudaFree(cd.slab);
   for (auto& sp : c->spans) {
     cudaEventDestroy(sp.a);
@@ -1038,6 +1042,70 @@ extern "C" moe_status moe_ctx_spans(moe_ctx* c, moe_span* spans, int32_t capacit
 extern "C" moe_status moe_ctx_set_aa_ctas(moe_ctx* c, int32_t ctas) {
   if (!c || ctas < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "set_aa_ctas: bad argument");
   c->aa_ctas = ctas;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_xfer(moe_ctx* c, const int64_t* rows_per_card, int32_t row_bytes, int32_t grid,
+                                   void* stream) {
+  if (!c || !rows_per_card) return fail(MOE_ERR_INVALID_ARGUMENT, "xfer: null argument");
+  if (c->local.size() != 1) return fail(MOE_ERR_UNSUPPORTED, "xfer: one local card per context only");
+  if (row_bytes <= 0 || row_bytes > c->row_bytes) return fail(MOE_ERR_INVALID_ARGUMENT, "xfer: bad row width");
+  if (!c->connected) return fail(MOE_ERR_TRANSPORT, "xfer: context not connected");
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  Card& cd = c->local[0];
+  if (!c->xfer_list) {
+    MONTA_CUDA(cudaMalloc(&c->xfer_list, seglist_bytes(kMaxCards)));
+    MONTA_CUDA(cudaHostAlloc(&c->xfer_host, seglist_bytes(kMaxCards), cudaHostAllocDefault));
+    std::memset(c->xfer_host, 0, seglist_bytes(kMaxCards));
+    c->xfer_host->nseg = -1;
+  }
+  // Build the list on the host; upload only when it changed (so repeated
+  // calls time the copy kernel alone).
+  SegList* L = c->xfer_host;
+  std::vector<Seg> segs;
+  int64_t total = 0;
+  for (int q = 0; q < c->cards; ++q) {
+    if (rows_per_card[q] <= 0) continue;
+    if (!c->peer[q].slab) return fail(MOE_ERR_TRANSPORT, "xfer: card %d is not mapped", q);
+    if (rows_per_card[q] > c->recv_cap) return fail(MOE_ERR_INVALID_ARGUMENT, "xfer: too many rows for card %d", q);
+    Seg sg{};
+    sg.row_begin = total;
+    sg.src_row = total;
+    sg.dst_row = 0;
+    sg.rows = int32_t(rows_per_card[q]);
+    sg.dst = q;
+    sg.col_off = 0;
+    sg.width = row_bytes;
+    sg.expert = 0;
+    segs.push_back(sg);
+    total += rows_per_card[q];
+  }
+  if (total > c->recv_cap) return fail(MOE_ERR_INVALID_ARGUMENT, "xfer: %lld rows exceed the buffer", (long long)total);
+  const bool same = L->nseg == int32_t(segs.size()) && L->total_rows == total &&
+                    std::memcmp(L->segs, segs.data(), segs.size() * sizeof(Seg)) == 0;
+  if (!same) {
+    MONTA_CUDA(cudaStreamSynchronize(s));  // the pinned staging may still feed a previous upload
+    L->nseg = int32_t(segs.size());
+    L->total_rows = total;
+    if (!segs.empty()) std::memcpy(L->segs, segs.data(), segs.size() * sizeof(Seg));
+    MONTA_CUDA(cudaMemcpyAsync(c->xfer_list, L, seglist_bytes(L->nseg), cudaMemcpyHostToDevice, s));
+  }
+  CopyArgs a{};
+  a.list = c->xfer_list;
+  a.src = static_cast<const char*>(cd.v.recv);
+  a.src_stride = c->row_bytes;
+  a.dst_stride = c->row_bytes;
+  for (int q = 0; q < c->cards; ++q) {
+    if (!c->peer[q].slab) continue;
+    a.dst[q] = q == cd.id ? static_cast<char*>(cd.v.pre) : c->peer[q].recv;
+  }
+  a.wait = no_wait();
+  a.sig = no_signal();
+  a.err = cd.err;
+  const int g = grid > 0 ? grid : c->sms * 2;
+  MONTA_CUDA(launch_seg_copy(a, vec_bytes(row_bytes, c->row_bytes), g, s));
+  ++c->launches;
   return MOE_OK;
 }
 

@@ -188,6 +188,11 @@ class MoeLayer:
     def set_aa_ctas(self, ctas: int) -> None:
         check(self.lib.moe_ctx_set_aa_ctas(self._ctx, ctas))
 
+    def xfer(self, rows_per_card, row_bytes: int, grid: int = 0, stream=None) -> None:
+        """Transport primitive: rows_per_card[c] rows of `row_bytes` stored to card c."""
+        arr = (C.c_int64 * len(rows_per_card))(*[int(r) for r in rows_per_card])
+        check(self.lib.moe_ctx_xfer(self._ctx, arr, int(row_bytes), int(grid), _stream_ptr(stream)))
+
     @property
     def launch_count(self) -> int:
         return int(self.lib.moe_ctx_launch_count(self._ctx))
