@@ -34,6 +34,7 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
 
 CONFIG = {"workload": "mixtral-8x7b-moe-layer", "tokens_per_node": 4096, "hidden": 4096, "experts": 8,
           "top_k": 2, "dtype": "bf16", "logits": "f32"}
@@ -135,55 +136,59 @@ def exposed(aa, other):
 
 
 # ---------------------------------------------------------------------------
-def cpu_port_sample(e, t, E, k, T, h, tokens_sample, seed=0):
-    """The oracle port (C restatement of the reference data plane) on a bounded
-    sample of the workload, single-threaded; returns us/layer scaled to T."""
+def cpu_port_layer(e, t, E, k, T, h, seed=0):
+    """One full layer of the oracle port (oracle/moe_oracle.c: the C
+    restatement of the reference data plane, E > e generalised) on the host,
+    single-threaded: route_topk + permute + dispatch + combine of every node.
+    Returns seconds (input generation excluded)."""
     import numpy as np
     import oracle
     rng = np.random.default_rng(seed)
-    Ts = tokens_sample
-    x = rng.standard_normal((e, Ts, h)).astype(np.float32)
-    xb = x.view(np.uint32)
-    bf = (xb >> 16).astype(np.uint16)  # bf16 bit patterns
-    xbytes = bf.view(np.uint8).reshape(e, Ts, h * 2)
-    logits = rng.standard_normal((e, Ts, E))
+    x = rng.standard_normal((e, T, h)).astype(np.float32)
+    xbytes = (x.view(np.uint32) >> 16).astype(np.uint16).view(np.uint8).reshape(e, T, h * 2)  # bf16 bits
+    logits = rng.standard_normal((e, T, E))
     t0 = time.perf_counter()
-    experts = np.zeros((e, Ts, k), np.int32)
-    probs = np.zeros((e, Ts, k), np.float64)
+    experts = np.zeros((e, T, k), np.int32)
+    probs = np.zeros((e, T, k), np.float64)
     for g in range(e):
         experts[g], probs[g] = oracle.route_topk(logits[g], k)
     nodes = oracle.Nodes(e, t, E, xbytes, experts)
-    if t > 1:
-        fin, _ = nodes.dispatch_chunked(oracle.O1, 1, 2)
-    else:
-        fin = nodes.dispatch_monolithic()
+    fin = nodes.dispatch_chunked(oracle.O1, 1, 2)[0] if t > 1 else nodes.dispatch_monolithic()
     nodes.combine(oracle.BF16, fin, probs)
-    dt = time.perf_counter() - t0
-    return dt * 1e6 * (T / Ts), dt
+    return time.perf_counter() - t0
+
+
+def cpu_baseline_value(e, t, E, k, T, h, budget_s=10.0, max_reps=100):
+    vals, spent = [], 0.0
+    while spent < budget_s and len(vals) < max_reps:
+        dt = cpu_port_layer(e, t, E, k, T, h, seed=len(vals))
+        vals.append(dt)
+        spent += dt
+    return statistics.mean(vals) * 1e6, len(vals), spent
 
 
 def run_reference(args):
-    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    """--impl reference: the reference's CPU path on this host (rank 0 only).
+    The reference headers (oracle/_ref) cannot run this workload — with E = 8
+    experts on e < 8 nodes its dispatch drops records and its combine indexes
+    out of bounds (SURVEY.md §7 decision 1) — so the arm times the oracle port,
+    the C restatement of the same algorithm generalised to E > e."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     e, t = topo_for(args.gpus)
     T, h, E, k = CONFIG["tokens_per_node"], CONFIG["hidden"], CONFIG["experts"], CONFIG["top_k"]
-    sample = args.ref_sample_tokens
-    vals = []
     for _ in range(max(1, args.warmup)):
-        cpu_port_sample(e, t, E, k, T, h, sample)
-    for s in range(max(1, args.steps)):
-        us, _ = cpu_port_sample(e, t, E, k, T, h, sample, seed=s)
-        vals.append(us)
+        cpu_port_layer(e, t, E, k, T, h)
+    vals = [cpu_port_layer(e, t, E, k, T, h, seed=s) * 1e6 for s in range(max(1, args.steps))]
     v = statistics.mean(vals)
     line = {"metric": METRIC, "value": v, "unit": "us/layer", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "impl": "reference",
             "config": dict(CONFIG, topology=f"{e}x{t}", level="O1" if t > 1 else "Baseline"),
             "cpu_baseline": {"value": v, "unit": "us/layer", "cores": 1, "kind": "port",
-                             "sample": f"{sample} of {T} tokens per node x {e} nodes, scaled linearly; "
-                                       f"oracle/moe_oracle.c (C restatement of dataplane.hpp, E>e generalised)"},
+                             "sample": f"full layer ({T} tokens x {e} nodes) per step, {args.steps} steps; "
+                                       f"oracle/moe_oracle.c, 1 thread of {os.cpu_count()}"},
             "e2e": {"value": v, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -198,9 +203,8 @@ def main():
     ap.add_argument("--level", default="auto", help="auto|baseline|o1|o2|o3")
     ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--landing", default="final", choices=["final", "staged"])
-    ap.add_argument("--ref-sample-tokens", type=int, default=512)
-    ap.add_argument("--cpu-sample-tokens", type=int, default=256)
     ap.add_argument("--quick", action="store_true", help="skip naive/e2e/cpu extras (profiling runs)")
+    ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -252,6 +256,7 @@ def main():
     layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, logit_dtype=torch.float32, max_chunks=16,
                      device=local, rank=rank if world > 1 else 0, world_size=world)
     layer.connect()
+    layer.enable_graphs(not args.no_graphs)
     cd = layer.cards[0]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + node)
     x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(torch.bfloat16)
@@ -421,16 +426,16 @@ def main():
 
     cpu = None
     if rank == 0 and world == 1 and not args.quick:
-        cpu_us, secs = cpu_port_sample(e, t, E, k, T, h, args.cpu_sample_tokens)
+        cpu_us, reps, secs = cpu_baseline_value(e, t, E, k, T, h)
         cpu = {"value": cpu_us, "unit": "us/layer", "cores": 1, "kind": "port",
-               "sample": f"{args.cpu_sample_tokens} of {T} tokens ({secs:.2f} s CPU), scaled linearly; "
-                         f"oracle/moe_oracle.c route+permute+dispatch+combine, 1 thread of {os.cpu_count()}"}
+               "sample": f"{reps} full layers ({T} tokens, {secs:.1f} s CPU); oracle/moe_oracle.c "
+                         f"route+permute+dispatch+combine, 1 thread of {os.cpu_count()} host threads"}
 
     line = {"metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn x, randn f32 gate logits)",
             "config": dict(CONFIG, topology=f"{e}x{t}", level=_lib.LEVEL_NAMES[level], chunks=n,
-                           landing=args.landing, parallelism=f"ep{e}xtp{t}",
+                           landing=args.landing, parallelism=f"ep{e}xtp{t}", cuda_graphs=not args.no_graphs,
                            l2="flushed between steps (256 MiB memset outside the events)",
                            planner=None if decision is None else
                            {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,

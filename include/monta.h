@@ -238,6 +238,11 @@ typedef struct moe_span {
   float end_ms;
 } moe_span;
 moe_status moe_ctx_enable_timing(moe_ctx* ctx, int enable);
+/* Replay moe_ctx_forward / moe_ctx_forward_host as CUDA graphs: each
+ * (level, n, landing, host buffers) is captured once (every stream of the
+ * step) and replayed; flags carry a device-resident epoch so replays stay in
+ * lockstep across ranks.  Ignored while timing is enabled. */
+moe_status moe_ctx_enable_graphs(moe_ctx* ctx, int enable);
 moe_status moe_ctx_spans(moe_ctx* ctx, moe_span* spans, int32_t capacity, int32_t* n_spans);
 /* Cap the SMs used by the cross-group (AllToAll) copy kernels, emulating a
  * slow inter-node link ("B1-throttled" mode).  0 = no cap. */
@@ -251,6 +256,9 @@ moe_status moe_ctx_set_aa_ctas(moe_ctx* ctx, int32_t ctas);
  * copy).  Only local + peer-mapped cards may be named. */
 moe_status moe_ctx_xfer(moe_ctx* ctx, const int64_t* rows_per_card, int32_t row_bytes, int32_t grid,
                         void* stream);
+/* Debug: record phase timestamps of the fused front kernel (enable != 0);
+ * with out8 != NULL, synchronise and copy card's 8 globaltimer stamps (ns). */
+moe_status moe_ctx_debug_front(moe_ctx* ctx, int enable, int card, uint64_t* out8);
 /* Number of kernels this context launched since creation. */
 int64_t moe_ctx_launch_count(const moe_ctx* ctx);
 

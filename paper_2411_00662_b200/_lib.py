@@ -181,10 +181,12 @@ SIGNATURES = {
     "moe_ctx_recv_rows": (C.c_int, [_P, C.c_int, _PI64]),
     "moe_ctx_sync": (C.c_int, [_P]),
     "moe_ctx_enable_timing": (C.c_int, [_P, C.c_int]),
+    "moe_ctx_enable_graphs": (C.c_int, [_P, C.c_int]),
     "moe_ctx_spans": (C.c_int, [_P, C.POINTER(Span), _I32, _PI32]),
     "moe_ctx_set_aa_ctas": (C.c_int, [_P, _I32]),
     "moe_ctx_launch_count": (C.c_int64, [_P]),
     "moe_ctx_xfer": (C.c_int, [_P, _PI64, _I32, _I32, _P]),
+    "moe_ctx_debug_front": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     "moe_lookup_efficiency": (C.c_int, [C.POINTER(Curve), _D, _PD]),
     "moe_traffic_volume": (C.c_double, [C.POINTER(ModelSpec)]),
     "moe_chunk_alltoall_time": (C.c_int, [_D, _I32, _I32, _I32, _D, C.POINTER(Curve), C.POINTER(Overhead), _PD]),

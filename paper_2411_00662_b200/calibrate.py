@@ -80,6 +80,9 @@ def main():
             dist.all_reduce(bar)
             torch.cuda.synchronize()
             s, f = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            # keep the stream busy while the host enqueues, so the events see
+            # device time only (no host launch latency)
+            torch.cuda._sleep(100000)
             s.record(stream)
             fn()
             f.record(stream)

@@ -70,22 +70,40 @@ __global__ void __launch_bounds__(kThreads) k_unpermute(const UnpermArgs a) {
       }
     }
     __syncwarp();
-    for (int64_t v = lane; v < nvec; v += 32) {
-      const int64_t col = a.col_begin + v * N;
-      TAcc acc[N];
+    // UV column vectors per lane per batch; for every slot the UV loads are
+    // independent, and no store intervenes, so k*UV loads are in flight.
+    constexpr int UV = N >= 8 ? 4 : 2;
+    for (int64_t v0 = lane; v0 < nvec; v0 += 32 * UV) {
+      TAcc acc[UV][N];
 #pragma unroll
-      for (int u = 0; u < N; ++u) acc[u] = TAcc(0);
+      for (int w = 0; w < UV; ++w)
+#pragma unroll
+        for (int u = 0; u < N; ++u) acc[w][u] = TAcc(0);
       for (int s = 0; s < a.k; ++s) {
         const TAcc p = s_p[wib][s];
-        const Pack<TIn, N> y = *reinterpret_cast<const Pack<TIn, N>*>(s_row[wib][s] + col * sizeof(TIn));
+        const char* row = s_row[wib][s];
+        Pack<TIn, N> y[UV];
 #pragma unroll
-        for (int u = 0; u < N; ++u) acc[u] = madd<TAcc>(acc[u], p, widen<TIn, TAcc>(y.v[u]));
+        for (int w = 0; w < UV; ++w) {
+          const int64_t v = v0 + w * 32;
+          if (v < nvec) y[w] = *reinterpret_cast<const Pack<TIn, N>*>(row + (a.col_begin + v * N) * sizeof(TIn));
+        }
+#pragma unroll
+        for (int w = 0; w < UV; ++w)
+#pragma unroll
+          for (int u = 0; u < N; ++u) acc[w][u] = madd<TAcc>(acc[w][u], p, widen<TIn, TAcc>(y[w].v[u]));
       }
-      Pack<TOut, N> o;
 #pragma unroll
-      for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[u]);
-      for (int d = 0; d < a.n_out; ++d)
-        *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + i * a.out_stride + col * sizeof(TOut)) = o;
+      for (int w = 0; w < UV; ++w) {
+        const int64_t v = v0 + w * 32;
+        if (v >= nvec) continue;
+        const int64_t col = a.col_begin + v * N;
+        Pack<TOut, N> o;
+#pragma unroll
+        for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[w][u]);
+        for (int d = 0; d < a.n_out; ++d)
+          *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + i * a.out_stride + col * sizeof(TOut)) = o;
+      }
     }
     __syncwarp();
   }

@@ -103,15 +103,20 @@ __device__ __forceinline__ void st_vec(char* p, const char& v) { *p = v; }
 // of every CTA, bounded by a timeout) before touching it; a kernel that
 // produces remote data has its LAST CTA publish the flags after a
 // system-scope fence.
+// The epoch is read from device memory (`epoch_ptr`, bumped once per
+// dispatch by the front kernel) so a captured CUDA graph replays correctly;
+// `epoch` is used when epoch_ptr is null.
 struct WaitList {
   const uint64_t* flags[kMaxCards];  // local flag words to watch
   int n;
   uint64_t epoch;
+  const uint64_t* epoch_ptr;
 };
 struct SignalList {
   uint64_t* flags[kMaxCards];  // peer (or local) flag words to set
   int n;
   uint64_t epoch;
+  const uint64_t* epoch_ptr;
   unsigned int* done;  // per-launch CTA completion counter (local, zeroed)
 };
 
@@ -137,9 +142,10 @@ __device__ __forceinline__ bool cta_wait(const WaitList& w, int* err) {
   if (threadIdx.x == 0) {
     ok = 1;
     if (w.n > 0) {
+      const uint64_t epoch = w.epoch_ptr ? *w.epoch_ptr : w.epoch;
       const unsigned long long t0 = globaltimer();
       for (int i = 0; i < w.n; ++i) {
-        while (ld_acquire_sys(w.flags[i]) < w.epoch) {
+        while (ld_acquire_sys(w.flags[i]) < epoch) {
           if (globaltimer() - t0 > kWaitTimeoutNs) {
             atomicExch(err, (int)MOE_ERR_TIMEOUT);
             ok = 0;
@@ -163,7 +169,8 @@ __device__ __forceinline__ void cta_signal(const SignalList& s) {
     const unsigned int prev = atomicAdd(s.done, 1u);
     if (prev == gridDim.x - 1) {
       __threadfence_system();
-      for (int i = 0; i < s.n; ++i) st_release_sys(s.flags[i], s.epoch);
+      const uint64_t epoch = s.epoch_ptr ? *s.epoch_ptr : s.epoch;
+      for (int i = 0; i < s.n; ++i) st_release_sys(s.flags[i], epoch);
       *s.done = 0u;  // ready for the next launch that reuses this counter
     }
   }

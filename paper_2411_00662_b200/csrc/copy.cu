@@ -20,45 +20,60 @@ namespace {
 constexpr int kCopyThreads = 256;
 constexpr int kSegSmem = 1024;  // segment starts cached in shared memory
 
+template <int V> struct CopyUnroll { static constexpr int value = V >= 8 ? 8 : 4; };
+
+// One batch per warp: up to U vectors per lane, every load issued before any
+// store (predicated, so short rows and tails keep all loads in flight).
 template <int V>
-__device__ __forceinline__ void copy_row(const char* __restrict__ s, char* const* d, int nd,
-                                         int64_t bytes, int lane) {
+__device__ __forceinline__ void copy_bytes(const char* __restrict__ s, char* const* d, int nd, int64_t bytes,
+                                           int lane) {
   using Vec = typename VecT<V>::type;
+  constexpr int U = CopyUnroll<V>::value;
   const Vec* sv = reinterpret_cast<const Vec*>(s);
   const int64_t nvec = bytes / V;
-  constexpr int U = V >= 8 ? 8 : 4;
-  int64_t i = lane;
-  for (; i + (U - 1) * 32 < nvec; i += U * 32) {
+  for (int64_t i0 = 0; i0 < nvec; i0 += U * 32) {
     Vec r[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) r[u] = ld_stream(sv + i + u * 32);
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = i0 + u * 32 + lane;
+      if (i < nvec) r[u] = ld_stream(sv + i);
+    }
     for (int q = 0; q < nd; ++q) {
       Vec* dv = reinterpret_cast<Vec*>(d[q]);
 #pragma unroll
-      for (int u = 0; u < U; ++u) st_vec(dv + i + u * 32, r[u]);
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = i0 + u * 32 + lane;
+        if (i < nvec) st_vec(dv + i, r[u]);
+      }
     }
-  }
-  for (; i < nvec; i += 32) {
-    const Vec r = ld_stream(sv + i);
-    for (int q = 0; q < nd; ++q) st_vec(reinterpret_cast<Vec*>(d[q]) + i, r);
   }
 }
 
+// Work item = (row, chunk of kItemBytes): a wide row is spread over several
+// warps, so latency per row does not serialise small transfers.
 template <int V>
 __global__ void __launch_bounds__(kCopyThreads) k_seg_copy(const CopyArgs a) {
-  if (!cta_wait(a.wait, a.err)) return;
+  if (!cta_wait(a.wait, a.err)) {
+    return;
+  }
+  constexpr int kItemBytes = 32 * V * CopyUnroll<V>::value;
   __shared__ int64_t sbeg[kSegSmem];
-  const SegList* L = a.list;
+  const bool second = a.list2 != nullptr && int(blockIdx.x) >= a.split;
+  const SegList* L = second ? a.list2 : a.list;
+  const int64_t cta = second ? int64_t(blockIdx.x) - a.split : int64_t(blockIdx.x);
+  const int64_t ctas = a.list2 ? (second ? int64_t(gridDim.x) - a.split : int64_t(a.split)) : int64_t(gridDim.x);
   const int nseg = L->nseg;
-  const int64_t total = L->total_rows;
+  const int64_t cpr = a.chunks_per_row > 0 ? a.chunks_per_row : 1;
+  const int64_t total = L->total_rows * cpr;
   const bool cached = nseg <= kSegSmem;
   if (cached)
     for (int i = threadIdx.x; i < nseg; i += blockDim.x) sbeg[i] = L->segs[i].row_begin;
   __syncthreads();
   const int lane = threadIdx.x & 31;
-  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
-  for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; r < total; r += warps) {
-    // segment lookup: last seg with row_begin <= r
+  const int64_t wpc = blockDim.x / 32;
+  for (int64_t item = cta * wpc + (threadIdx.x >> 5); item < total; item += ctas * wpc) {
+    const int64_t r = item / cpr;
+    const int64_t chunk = item - r * cpr;
     int lo = 0, hi = nseg - 1;
     while (lo < hi) {
       const int mid = (lo + hi + 1) >> 1;
@@ -66,25 +81,28 @@ __global__ void __launch_bounds__(kCopyThreads) k_seg_copy(const CopyArgs a) {
       if (b <= r) lo = mid; else hi = mid - 1;
     }
     const Seg sg = L->segs[lo];
+    const int64_t off = chunk * kItemBytes;
+    if (off >= sg.width) continue;
+    const int64_t bytes = sg.width - off < kItemBytes ? sg.width - off : kItemBytes;
     const int64_t i = r - sg.row_begin;
     const int64_t src_row = a.gather ? int64_t(__ldg(a.gather + sg.src_row + i)) : sg.src_row + i;
     const int64_t dst_row = sg.dst_row + i;
-    const char* sp = a.src + src_row * a.src_stride + sg.col_off;
-    char* dps[kMaxCards];
+    const char* sp = a.src + src_row * a.src_stride + sg.col_off + off;
+    char* dps[8];
     int nd = 0;
     if (sg.dst >= 0) {
-      dps[nd++] = a.dst[sg.dst] + dst_row * a.dst_stride + sg.col_off;
+      dps[nd++] = a.dst[sg.dst] + dst_row * a.dst_stride + sg.col_off + off;
     } else {
       uint64_t m = a.dst_mask;
-      while (m) {
+      while (m && nd < 8) {
         const int c = __ffsll(m) - 1;
         m &= m - 1;
-        dps[nd++] = a.dst[c] + dst_row * a.dst_stride + sg.col_off;
+        dps[nd++] = a.dst[c] + dst_row * a.dst_stride + sg.col_off + off;
       }
     }
-    copy_row<V>(sp, dps, nd, sg.width, lane);
+    copy_bytes<V>(sp, dps, nd, bytes, lane);
     // tags ride along with the row: {token_id, source_card, source_position, expert}
-    if (lane == 0) {
+    if (chunk == 0 && lane == 0) {
       int4 tag;
       bool have = true;
       if (a.synth_tags) {
@@ -121,7 +139,7 @@ __global__ void __launch_bounds__(kCopyThreads)
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; r < R; r += warps) {
     const int64_t s = __ldg(perm + r);
     char* d = out + r * out_stride;
-    copy_row<V>(src + s * src_stride + col_off, &d, 1, width, lane);
+    copy_bytes<V>(src + s * src_stride + col_off, &d, 1, width, lane);
   }
 }
 
@@ -130,25 +148,14 @@ __global__ void k_wait(const WaitList w, int32_t* err) { cta_wait(w, err); }
 __global__ void k_signal(const SignalList s) {
   if (threadIdx.x == 0) {
     __threadfence_system();
-    for (int i = 0; i < s.n; ++i) st_release_sys(s.flags[i], s.epoch);
-  }
-}
-
-__global__ void k_push_counts(const PushCountsArgs a) {
-  // Each destination table row for this node: [max_chunks][E]; only n rows used.
-  const int total = a.n * a.E;
-  for (int q = 0; q < a.n_dst; ++q) {
-    int32_t* dst = a.dst_tables[q] + int64_t(a.node) * a.max_chunks * a.E;
-    for (int i = threadIdx.x; i < total; i += blockDim.x) dst[i] = a.counts[i];
-  }
-  __syncthreads();
-  if (threadIdx.x == 0 && a.sig.n > 0) {
-    __threadfence_system();
-    for (int i = 0; i < a.sig.n; ++i) st_release_sys(a.sig.flags[i], a.sig.epoch);
+    const uint64_t epoch = s.epoch_ptr ? *s.epoch_ptr : s.epoch;
+    for (int i = 0; i < s.n; ++i) st_release_sys(s.flags[i], epoch);
   }
 }
 
 }  // namespace
+
+int copy_item_bytes(int vec) { return 32 * vec * (vec >= 8 ? 8 : 4); }
 
 cudaError_t launch_seg_copy(const CopyArgs& a, int vec, int grid, cudaStream_t s) {
   switch (vec) {
@@ -194,11 +201,6 @@ cudaError_t launch_wait(const WaitList& w, int32_t* err, cudaStream_t s) {
 cudaError_t launch_signal(const SignalList& sg, cudaStream_t s) {
   if (sg.n == 0) return cudaSuccess;
   k_signal<<<1, 32, 0, s>>>(sg);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_push_counts(const PushCountsArgs& a, cudaStream_t s) {
-  k_push_counts<<<1, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -45,7 +45,8 @@ struct PeerPtrs {
 struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
-  size_t lists, local_delta, recv_rows, scratch, total;
+  size_t lists, local_delta, recv_rows, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
+      ready, total;
 };
 
 struct Card {
@@ -60,6 +61,14 @@ struct Card {
   int32_t* local_delta = nullptr;
   int64_t* recv_rows = nullptr;
   int32_t* scratch = nullptr;
+  uint64_t* epoch_dev = nullptr;   // bumped by the front kernel once per dispatch
+  unsigned long long* dbg = nullptr;  // front-kernel phase timestamps (debug)
+  int32_t* tile_hist = nullptr;       // [n_tiles][E]
+  int32_t* tile_base = nullptr;       // [n_tiles][E]
+  int32_t* counts_acc = nullptr;      // [max_chunks][E]
+  unsigned* arrive = nullptr;         // front grid barrier
+  unsigned long long* ready = nullptr;
+  unsigned* front_done = nullptr;  // CTA election counter of the front kernel
 };
 
 struct Span {
@@ -80,11 +89,21 @@ struct moe_ctx {
   std::vector<monta::Card> local;
   monta::PeerPtrs peer[monta::kMaxCards];
   std::vector<void*> opened;
-  cudaStream_t s_aa = nullptr, s_ag = nullptr, s_d2d = nullptr;
+  cudaStream_t s_aa = nullptr, s_ag = nullptr, s_d2d = nullptr, s_cap = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join_aa = nullptr, ev_join_ag = nullptr, ev_join_d2d = nullptr;
   std::vector<cudaEvent_t> ev_aa, ev_ag;
-  uint64_t epoch = 0;
   int aa_ctas = 0;
+  bool combine_ready = false;  // a dispatch whose combine has not run yet
+  bool debug = false;          // record front-kernel phase timestamps
+  bool use_graphs = false;
+  struct GraphEntry {
+    int level, n, landing;
+    const void *hx, *hl;
+    void* ho;
+    cudaGraphExec_t exec;
+    int64_t kernels;  // this context's kernels inside the graph
+  };
+  std::vector<GraphEntry> graphs;
   bool connected = false;
   // last dispatch (the combine replays its plan)
   int last_level = -1, last_n = 0, last_landing = 0;
@@ -138,6 +157,15 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.local_delta = take(size_t(E) * 4);
   s.recv_rows = take(8);
   s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
+  s.epoch = take(8);
+  s.front_done = take(16);
+  s.dbg = take(64);
+  const int64_t tiles = (T + front_router_tokens(int(E)) - 1) / front_router_tokens(int(E));
+  s.tile_hist = take(size_t(tiles) * E * 4);
+  s.tile_base = take(size_t(tiles) * E * 4);
+  s.counts_acc = take(size_t(d.max_chunks) * E * 4);
+  s.arrive = take(16);
+  s.ready = take(16);
   s.total = off;
   return s;
 }
@@ -174,6 +202,14 @@ void bind_card(moe_ctx* c, Card& cd) {
   cd.local_delta = reinterpret_cast<int32_t*>(b + s.local_delta);
   cd.recv_rows = reinterpret_cast<int64_t*>(b + s.recv_rows);
   cd.scratch = reinterpret_cast<int32_t*>(b + s.scratch);
+  cd.epoch_dev = reinterpret_cast<uint64_t*>(b + s.epoch);
+  cd.front_done = reinterpret_cast<unsigned*>(b + s.front_done);
+  cd.dbg = reinterpret_cast<unsigned long long*>(b + s.dbg);
+  cd.tile_hist = reinterpret_cast<int32_t*>(b + s.tile_hist);
+  cd.tile_base = reinterpret_cast<int32_t*>(b + s.tile_base);
+  cd.counts_acc = reinterpret_cast<int32_t*>(b + s.counts_acc);
+  cd.arrive = reinterpret_cast<unsigned*>(b + s.arrive);
+  cd.ready = reinterpret_cast<unsigned long long*>(b + s.ready);
 }
 
 void set_peer(moe_ctx* c, int card, char* slab) {
@@ -330,6 +366,11 @@ extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int
   cudaStreamCreateWithPriority(&c->s_aa, cudaStreamNonBlocking, hi);
   cudaStreamCreateWithPriority(&c->s_ag, cudaStreamNonBlocking, lo);
   cudaStreamCreateWithPriority(&c->s_d2d, cudaStreamNonBlocking, lo);
+  cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking);
+  if (moe_status st = configure_front(desc->num_experts, desc->logit_dtype)) {
+    moe_ctx_destroy(c);
+    return st;
+  }
   cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_join_aa, cudaEventDisableTiming);
   cudaEventCreateWithFlags(&c->ev_join_ag, cudaEventDisableTiming);
@@ -373,6 +414,9 @@ extern "C" moe_status moe_ctx_destroy(moe_ctx* c) {
   if (c->s_aa) cudaStreamDestroy(c->s_aa);
   if (c->s_ag) cudaStreamDestroy(c->s_ag);
   if (c->s_d2d) cudaStreamDestroy(c->s_d2d);
+  if (c->s_cap) cudaStreamDestroy(c->s_cap);
+  for (auto& g : c->graphs)
+    if (g.exec) cudaGraphExecDestroy(g.exec);
   delete c;
   return MOE_OK;
 }
@@ -472,69 +516,106 @@ moe_status do_route(moe_ctx* c, cudaStream_t s) {
   return MOE_OK;
 }
 
-moe_status do_index(moe_ctx* c, int n, cudaStream_t s) {
+PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
+  const moe_layer_desc& d = c->d;
+  PlanArgs a{};
+  a.count_table = cd.count_table;
+  a.e = d.e;
+  a.t = d.t;
+  a.E = d.num_experts;
+  a.L = c->L;
+  a.n = n;
+  a.max_chunks = d.max_chunks;
+  a.node = cd.node;
+  a.rho = cd.rho;
+  a.level = level;
+  a.landing = landing;
+  a.row_bytes = c->row_bytes;
+  a.seg_cap = d.num_experts;
+  a.lists = cd.lists;
+  a.local_delta = cd.local_delta;
+  a.recv_rows = cd.recv_rows;
+  a.err = cd.err;
+  a.wait = no_wait();
+  a.wait.epoch_ptr = cd.epoch_dev;
+  if (!is_virtual(c))
+    for (int x = 0; x < d.e; ++x) {
+      const int src = card_of(c, x, cd.rho);
+      if (src != cd.id) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, kSigCounts, src);
+    }
+  return a;
+}
+
+// Front end of a dispatch: (route) + index + epoch bump + count exchange +
+// plan.  Multi-GPU: one fused launch per card.  Virtual mode: every card's
+// counts must land before any card plans, so the plan runs as a second
+// lockstep launch.
+moe_status do_front(moe_ctx* c, bool route, int level, int n, int landing, cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  // one local card: nothing to wait for between the count push and the plan
+  const bool fused_plan = !is_virtual(c) || c->local.size() == 1;
   for (auto& cd : c->local) {
+    FrontArgs f{};
+    f.logits = cd.v.logits;
+    f.route = route ? 1 : 0;
+    f.T = d.tokens;
+    f.E = d.num_experts;
+    f.k = d.top_k;
+    f.n = n;
+    f.experts = cd.v.experts;
+    f.probs = cd.v.probs;
+    f.perm_src = cd.v.perm_src;
+    f.expert_of = cd.v.expert_of;
+    f.slot_pos = cd.v.slot_pos;
+    f.counts = cd.v.counts;
+    f.expert_offsets = cd.v.expert_offsets;
+    f.err = cd.err;
+    f.tile_tokens = front_tile_tokens(d.num_experts, d.tokens, n);
+    f.n_tiles = int32_t((d.tokens + f.tile_tokens - 1) / f.tile_tokens);
+    f.aligned = (d.tokens / n) % f.tile_tokens == 0 ? 1 : 0;
+    f.tile_hist = cd.tile_hist;
+    f.tile_base = cd.tile_base;
+    f.counts_acc = cd.counts_acc;
+    f.arrive = cd.arrive;
+    f.ready = cd.ready;
+    f.epoch_dev = cd.epoch_dev;
+    f.node = cd.node;
+    f.max_chunks = d.max_chunks;
+    f.n_dst = 0;
+    f.n_sig = 0;
+    for (int x = 0; x < d.e; ++x) {
+      const int dst = card_of(c, x, cd.rho);
+      f.dst_tables[f.n_dst++] = c->peer[dst].count_table;
+      if (!is_virtual(c) && dst != cd.id) f.sig_flags[f.n_sig++] = flag_at(c, dst, kSigCounts, cd.id);
+    }
+    f.do_plan = fused_plan ? 1 : 0;
+    f.plan = make_plan_args(c, cd, level, n, landing);
+    f.plan_scratch = cd.scratch;
+    f.plan_in_smem = plan_fits_smem(d.e, d.num_experts, n) ? 1 : 0;
+    f.dbg = c->debug ? cd.dbg : nullptr;
     size_t sl;
-    span_begin(c, MOE_STAGE_INDEX, 0, s, &sl);
-    if (moe_status st = build_index(cd.v.experts, c->d.tokens, c->d.top_k, c->d.num_experts, n,
-                                    cd.v.perm_src, cd.v.expert_of, cd.v.slot_pos, cd.v.counts,
-                                    cd.v.expert_offsets, cd.err, s))
-      return st;
+    span_begin(c, route ? MOE_STAGE_ROUTE : MOE_STAGE_INDEX, 0, s, &sl);
+    if (moe_status st = launch_front(f, d.logit_dtype, s)) return st;
     span_end(c, sl, s);
     ++c->launches;
   }
+  if (!fused_plan)
+    for (auto& cd : c->local) {
+      PlanArgs a = make_plan_args(c, cd, level, n, landing);
+      size_t sl;
+      span_begin(c, MOE_STAGE_INDEX, 0, s, &sl);
+      MONTA_CUDA(launch_plan_with_scratch(a, cd.scratch, s));
+      span_end(c, sl, s);
+      ++c->launches;
+    }
   return MOE_OK;
 }
 
-// Count exchange + plan.  Each card pushes its node's per-chunk counts into
-// the count table of every card of its expert-parallel group (same rho).
-moe_status do_counts_and_plan(moe_ctx* c, int level, int n, int landing, cudaStream_t s) {
-  const moe_layer_desc& d = c->d;
+moe_status do_index(moe_ctx* c, int n, cudaStream_t s) {
   for (auto& cd : c->local) {
-    PushCountsArgs pa{};
-    pa.counts = cd.v.counts;
-    pa.n = n;
-    pa.E = d.num_experts;
-    pa.max_chunks = d.max_chunks;
-    pa.node = cd.node;
-    pa.n_dst = 0;
-    pa.sig = no_signal();
-    pa.sig.epoch = c->epoch;
-    for (int x = 0; x < d.e; ++x) {
-      const int dst = card_of(c, x, cd.rho);
-      pa.dst_tables[pa.n_dst++] = c->peer[dst].count_table;
-      if (!is_virtual(c) && dst != cd.id) pa.sig.flags[pa.sig.n++] = flag_at(c, dst, kSigCounts, cd.id);
-    }
-    MONTA_CUDA(launch_push_counts(pa, s));
-    ++c->launches;
-  }
-  for (auto& cd : c->local) {
-    PlanArgs a{};
-    a.count_table = cd.count_table;
-    a.e = d.e;
-    a.t = d.t;
-    a.E = d.num_experts;
-    a.L = c->L;
-    a.n = n;
-    a.max_chunks = d.max_chunks;
-    a.node = cd.node;
-    a.rho = cd.rho;
-    a.level = level;
-    a.landing = landing;
-    a.row_bytes = c->row_bytes;
-    a.seg_cap = d.num_experts;
-    a.lists = cd.lists;
-    a.local_delta = cd.local_delta;
-    a.recv_rows = cd.recv_rows;
-    a.err = cd.err;
-    a.wait = no_wait();
-    a.wait.epoch = c->epoch;
-    if (!is_virtual(c))
-      for (int x = 0; x < d.e; ++x) {
-        const int src = card_of(c, x, cd.rho);
-        if (src != cd.id) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, kSigCounts, src);
-      }
-    MONTA_CUDA(launch_plan_with_scratch(a, cd.scratch, s));
+    if (moe_status st = build_index(cd.v.experts, c->d.tokens, c->d.top_k, c->d.num_experts, n, cd.v.perm_src,
+                                    cd.v.expert_of, cd.v.slot_pos, cd.v.counts, cd.v.expert_offsets, cd.err, s))
+      return st;
     ++c->launches;
   }
   return MOE_OK;
@@ -545,11 +626,32 @@ int copy_vec(const moe_ctx* c, bool dedup) {
 }
 
 // One chunk of the fused permute + AllToAll, for one card.
+// Work items per row for the copy kernel.
+int items_per_row(int vec, int64_t max_width) {
+  const int64_t ib = copy_item_bytes(vec);
+  return int((max_width + ib - 1) / ib);
+}
+
+// One chunk of the fused permute + AllToAll, for one card.  Cross-node legs
+// (NVLink) and own-node legs (HBM, full rows) are separate lists run by
+// disjoint CTA sets, sized so both finish together.
 moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaStream_t s, bool concurrent) {
   const moe_layer_desc& d = c->d;
   const bool dedup = level != MOE_BASELINE && d.t > 1;
   CopyArgs a{};
-  a.list = list_of(c, cd, kPhaseAA, j);
+  const int grid = copy_grid(c, concurrent, true);
+  if (d.e > 1) {
+    a.list = list_of(c, cd, kPhaseAA, j);
+    a.list2 = list_of(c, cd, kPhaseAAL, j);
+    // time(local) / time(remote) ~= (full / width) * 0.2 / (e - 1)  (HBM copy vs NVLink store)
+    const double r = (dedup ? double(d.t) : 1.0) * 0.2 / double(d.e - 1);
+    const double frac = std::min(0.5, std::max(0.1, r / (1.0 + r)));
+    a.split = std::max(1, grid - std::max(1, int(grid * frac + 0.5)));
+  } else {
+    a.list = list_of(c, cd, kPhaseAAL, j);
+    a.list2 = nullptr;
+    a.split = grid;
+  }
   a.src = static_cast<const char*>(cd.v.x);
   a.src_stride = c->row_bytes;
   a.gather = cd.v.perm_src;
@@ -564,9 +666,11 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
     a.dst[q] = landing == MOE_LAND_STAGED ? c->peer[q].pre : c->peer[q].recv;
     a.dst_tags[q] = landing == MOE_LAND_STAGED ? c->peer[q].pre_tags : c->peer[q].recv_tags;
   }
+  const int vec = copy_vec(c, dedup);
+  a.chunks_per_row = items_per_row(vec, c->row_bytes);
   a.wait = no_wait();
   a.sig = no_signal();
-  a.sig.epoch = c->epoch;
+  a.sig.epoch_ptr = cd.epoch_dev;
   a.sig.done = cd.done + kPsAA * d.max_chunks + j;
   if (!is_virtual(c))
     for (int x = 0; x < d.e; ++x)
@@ -574,7 +678,7 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
   a.err = cd.err;
   size_t sl;
   span_begin(c, MOE_STAGE_AA, j, s, &sl);
-  MONTA_CUDA(launch_seg_copy(a, copy_vec(c, dedup), copy_grid(c, concurrent, true), s));
+  MONTA_CUDA(launch_seg_copy(a, vec, grid, s));
   span_end(c, sl, s);
   ++c->launches;
   return MOE_OK;
@@ -601,10 +705,12 @@ moe_status launch_ag(moe_ctx* c, Card& cd, int j, int landing, cudaStream_t s, b
     a.dst[q] = staged ? c->peer[q].pre : c->peer[q].recv;
     a.dst_tags[q] = staged ? c->peer[q].pre_tags : c->peer[q].recv_tags;
   }
+  a.chunks_per_row = items_per_row(copy_vec(c, true), c->row_bytes / d.t);
+  a.split = copy_grid(c, concurrent, false);
   a.wait = no_wait();
-  a.wait.epoch = c->epoch;
+  a.wait.epoch_ptr = cd.epoch_dev;
   a.sig = no_signal();
-  a.sig.epoch = c->epoch;
+  a.sig.epoch_ptr = cd.epoch_dev;
   a.sig.done = cd.done + kPsAG * d.max_chunks + j;
   if (!is_virtual(c)) {
     for (int g = 0; g < d.e; ++g)
@@ -633,8 +739,10 @@ moe_status launch_d2d(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bo
   a.dst_stride = c->row_bytes;
   a.dst[cd.id] = static_cast<char*>(cd.v.recv);
   a.dst_tags[cd.id] = cd.v.recv_tags;
+  a.chunks_per_row = items_per_row(copy_vec(c, false), c->row_bytes);
+  a.split = copy_grid(c, concurrent, false);
   a.wait = no_wait();
-  a.wait.epoch = c->epoch;
+  a.wait.epoch_ptr = cd.epoch_dev;
   if (!is_virtual(c)) {
     for (int g = 0; g < d.e; ++g)
       if (g != cd.node) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, sig_chunk(c, kPsAA, j), card_of(c, g, cd.rho));
@@ -659,7 +767,7 @@ moe_status dispatch_tail_wait(moe_ctx* c, Card& cd, int level, int n, int landin
   const bool dedup = level != MOE_BASELINE && d.t > 1;
   if (landing == MOE_LAND_STAGED) return MOE_OK;  // every D2D already waited
   WaitList w = no_wait();
-  w.epoch = c->epoch;
+  w.epoch_ptr = cd.epoch_dev;
   for (int j = 0; j < n; ++j) {
     const int need = dedup ? d.t - 1 : d.e - 1;
     if (w.n + need > kMaxCards) {
@@ -726,25 +834,22 @@ extern "C" moe_status moe_ctx_permute(moe_ctx* c, int32_t n, void* stream) {
   return MOE_OK;
 }
 
-extern "C" moe_status moe_ctx_dispatch(moe_ctx* c, int level, int32_t n, int landing, void* stream) {
-  if (moe_status st = check_ready(c)) return st;
-  if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
-  MONTA_CUDA(cudaSetDevice(c->device));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+namespace {
+
+moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t s, bool route) {
   const moe_layer_desc& d = c->d;
   if (level == MOE_BASELINE) landing = MOE_LAND_FINAL;
   const bool dedup = level != MOE_BASELINE && d.t > 1;
   const bool staged = landing == MOE_LAND_STAGED;
-  ++c->epoch;
   c->last_level = level;
   c->last_n = n;
   c->last_landing = landing;
+  c->combine_ready = true;
   if (c->timing && !c->in_forward) {
     c->span_used = 0;
     cudaEventRecord(c->ev_base, s);
   }
-  if (moe_status st = do_index(c, n, s)) return st;
-  if (moe_status st = do_counts_and_plan(c, level, n, landing, s)) return st;
+  if (moe_status st = do_front(c, route, level, n, landing, s)) return st;
 
   if (is_virtual(c)) {
     for (int j = 0; j < n; ++j) {
@@ -790,10 +895,20 @@ extern "C" moe_status moe_ctx_dispatch(moe_ctx* c, int level, int32_t n, int lan
   return dispatch_tail_wait(c, cd, level, n, landing, s);
 }
 
+}  // namespace
+
+extern "C" moe_status moe_ctx_dispatch(moe_ctx* c, int level, int32_t n, int landing, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  return dispatch_impl(c, level, n, landing, static_cast<cudaStream_t>(stream), false);
+}
+
 namespace {
 
 moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bool concurrent) {
   const moe_layer_desc& d = c->d;
+  if (d.e == 1) return MOE_OK;  // no other node: the un-permute reads every row in place
   const bool dedup = level != MOE_BASELINE && d.t > 1;
   CopyArgs a{};
   a.list = list_of(c, cd, kPhaseCAA, j);
@@ -803,9 +918,11 @@ moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bo
   a.dst_stride = c->row_bytes;
   for (int q = 0; q < c->cards; ++q)
     if (c->peer[q].slab) a.dst[q] = c->peer[q].comb;
+  a.chunks_per_row = items_per_row(copy_vec(c, dedup), dedup ? c->row_bytes / d.t : c->row_bytes);
+  a.split = copy_grid(c, concurrent, true);
   a.wait = no_wait();
   a.sig = no_signal();
-  a.sig.epoch = c->epoch;
+  a.sig.epoch_ptr = cd.epoch_dev;
   a.sig.done = cd.done + kPsCAA * d.max_chunks + j;
   if (!is_virtual(c))
     for (int g = 0; g < d.e; ++g)
@@ -846,9 +963,9 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
     a.out[a.n_out++] = static_cast<char*>(cd.v.out);
   }
   a.wait = no_wait();
-  a.wait.epoch = c->epoch;
+  a.wait.epoch_ptr = cd.epoch_dev;
   a.sig = no_signal();
-  a.sig.epoch = c->epoch;
+  a.sig.epoch_ptr = cd.epoch_dev;
   a.sig.done = cd.done + kPsCAG * d.max_chunks + j;
   if (!is_virtual(c)) {
     for (int x = 0; x < d.e; ++x)
@@ -874,18 +991,18 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
 
 }  // namespace
 
-extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* stream) {
-  if (moe_status st = check_ready(c)) return st;
-  MONTA_CUDA(cudaSetDevice(c->device));
-  if (c->last_level < 0) return fail(MOE_ERR_INVALID_ARGUMENT, "combine: no dispatch to mirror");
+namespace {
+
+moe_status combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
+  if (c->last_level < 0 || !c->combine_ready)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine: no pending dispatch to mirror (one combine per dispatch)");
   if (n != c->last_n) return fail(MOE_ERR_INVALID_ARGUMENT, "combine: n = %d differs from the dispatch's %d", n, c->last_n);
   const bool dedup_d = c->last_level != MOE_BASELINE && c->d.t > 1;
   const bool dedup = level != MOE_BASELINE && c->d.t > 1;
   if (dedup != dedup_d)
     return fail(MOE_ERR_INVALID_ARGUMENT, "combine: level must mirror the dispatch (baseline vs deduplicated)");
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
   const moe_layer_desc& d = c->d;
-  ++c->epoch;
+  c->combine_ready = false;
   if (is_virtual(c)) {
     for (int j = 0; j < n; ++j) {
       for (auto& cd : c->local)
@@ -900,9 +1017,9 @@ extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* st
     // Nothing orders a TP peer's output stores after this rank's previous
     // read of `out` when there is no cross-node leg: barrier the node.
     SignalList sg = no_signal();
-    sg.epoch = c->epoch;
+    sg.epoch_ptr = cd.epoch_dev;
     WaitList w = no_wait();
-    w.epoch = c->epoch;
+    w.epoch_ptr = cd.epoch_dev;
     for (int r = 0; r < d.t; ++r)
       if (r != cd.rho) {
         sg.flags[sg.n++] = flag_at(c, card_of(c, cd.node, r), kSigBarrier, cd.id);
@@ -925,7 +1042,7 @@ extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* st
   MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_ag, 0));
   if (dedup) {
     WaitList w = no_wait();
-    w.epoch = c->epoch;
+    w.epoch_ptr = cd.epoch_dev;
     for (int j = 0; j < n; ++j) {
       if (w.n + d.t - 1 > kMaxCards) {
         MONTA_CUDA(launch_wait(w, cd.err, s));
@@ -943,44 +1060,112 @@ extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* st
   return MOE_OK;
 }
 
-extern "C" moe_status moe_ctx_forward(moe_ctx* c, int level, int32_t n, int landing, void* stream) {
+}  // namespace
+
+extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* stream) {
   if (moe_status st = check_ready(c)) return st;
-  if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
   MONTA_CUDA(cudaSetDevice(c->device));
-  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  return combine_impl(c, level, n, static_cast<cudaStream_t>(stream));
+}
+
+namespace {
+
+// route + dispatch + combine, optionally wrapped in host<->device copies.
+moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
+                        cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  const size_t xbytes = size_t(d.tokens) * c->row_bytes;
+  const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;
+  const size_t obytes = size_t(d.tokens) * d.hidden * c->ob;
+  if (hx)
+    for (size_t i = 0; i < c->local.size(); ++i) {
+      MONTA_CUDA(cudaMemcpyAsync(c->local[i].v.x, static_cast<const char*>(hx) + i * xbytes, xbytes,
+                                 cudaMemcpyHostToDevice, s));
+      MONTA_CUDA(cudaMemcpyAsync(c->local[i].v.logits, static_cast<const char*>(hl) + i * lbytes, lbytes,
+                                 cudaMemcpyHostToDevice, s));
+    }
   if (c->timing) {
     c->span_used = 0;
     cudaEventRecord(c->ev_base, s);
   }
   c->in_forward = true;
-  moe_status st = do_route(c, s);
-  if (st == MOE_OK) st = moe_ctx_dispatch(c, level, n, landing, stream);
+  moe_status st = dispatch_impl(c, level, n, landing, s, true);
   c->in_forward = false;
   if (st != MOE_OK) return st;
-  return moe_ctx_combine(c, level, n, stream);
+  if (moe_status st2 = combine_impl(c, level, n, s)) return st2;
+  if (ho)
+    for (size_t i = 0; i < c->local.size(); ++i)
+      MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(ho) + i * obytes, c->local[i].v.out, obytes,
+                                 cudaMemcpyDeviceToHost, s));
+  return MOE_OK;
 }
 
-extern "C" moe_status moe_ctx_forward_host(moe_ctx* c, int level, int32_t n, int landing,
-                                           const void* host_x, const void* host_logits, void* host_out,
-                                           void* stream) {
+// CUDA-graph path: the whole step (every stream of it) is captured once per
+// (level, n, landing, host buffers) and replayed; flags carry the device
+// epoch, so replays stay in lockstep across ranks.
+moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
+                         cudaStream_t s) {
+  for (auto& g : c->graphs)
+    if (g.level == level && g.n == n && g.landing == landing && g.hx == hx && g.hl == hl && g.ho == ho) {
+      if (!g.exec) return forward_impl(c, level, n, landing, hx, hl, ho, s);
+      c->last_level = level;
+      c->last_n = n;
+      c->last_landing = level == MOE_BASELINE ? MOE_LAND_FINAL : landing;
+      c->combine_ready = false;
+      MONTA_CUDA(cudaGraphLaunch(g.exec, s));
+      c->launches += g.kernels;
+      return MOE_OK;
+    }
+  // capture on the context's own stream (the legacy stream cannot be captured)
+  moe_ctx::GraphEntry e{level, n, landing, hx, hl, ho, nullptr, 0};
+  const int64_t before = c->launches;
+  MONTA_CUDA(cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal));
+  moe_status st = forward_impl(c, level, n, landing, hx, hl, ho, c->s_cap);
+  cudaGraph_t graph = nullptr;
+  cudaError_t err = cudaStreamEndCapture(c->s_cap, &graph);
+  e.kernels = c->launches - before;
+  c->launches = before;
+  if (st != MOE_OK) {
+    if (graph) cudaGraphDestroy(graph);
+    return st;
+  }
+  if (err != cudaSuccess || !graph || cudaGraphInstantiate(&e.exec, graph, 0) != cudaSuccess) {
+    cudaGetLastError();  // capture unsupported here (e.g. pageable host memory): run eagerly from now on
+    if (graph) cudaGraphDestroy(graph);
+    e.exec = nullptr;
+    c->graphs.push_back(e);
+    return forward_impl(c, level, n, landing, hx, hl, ho, s);
+  }
+  cudaGraphDestroy(graph);
+  c->graphs.push_back(e);
+  return forward_graph(c, level, n, landing, hx, hl, ho, s);
+}
+
+}  // namespace
+
+extern "C" moe_status moe_ctx_forward(moe_ctx* c, int level, int32_t n, int landing, void* stream) {
   if (moe_status st = check_ready(c)) return st;
-  if (!host_x || !host_logits || !host_out) return fail(MOE_ERR_INVALID_ARGUMENT, "forward_host: null buffer");
+  if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
   MONTA_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  const moe_layer_desc& d = c->d;
-  const size_t xbytes = size_t(d.tokens) * c->row_bytes;
-  const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;
-  const size_t obytes = size_t(d.tokens) * d.hidden * c->ob;
-  for (size_t i = 0; i < c->local.size(); ++i) {
-    MONTA_CUDA(cudaMemcpyAsync(c->local[i].v.x, static_cast<const char*>(host_x) + i * xbytes, xbytes,
-                               cudaMemcpyHostToDevice, s));
-    MONTA_CUDA(cudaMemcpyAsync(c->local[i].v.logits, static_cast<const char*>(host_logits) + i * lbytes,
-                               lbytes, cudaMemcpyHostToDevice, s));
-  }
-  if (moe_status st = moe_ctx_forward(c, level, n, landing, stream)) return st;
-  for (size_t i = 0; i < c->local.size(); ++i)
-    MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(host_out) + i * obytes, c->local[i].v.out, obytes,
-                               cudaMemcpyDeviceToHost, s));
+  if (c->use_graphs && !c->timing) return forward_graph(c, level, n, landing, nullptr, nullptr, nullptr, s);
+  return forward_impl(c, level, n, landing, nullptr, nullptr, nullptr, s);
+}
+
+extern "C" moe_status moe_ctx_forward_host(moe_ctx* c, int level, int32_t n, int landing, const void* host_x,
+                                           const void* host_logits, void* host_out, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (!host_x || !host_logits || !host_out) return fail(MOE_ERR_INVALID_ARGUMENT, "forward_host: null buffer");
+  if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (c->use_graphs && !c->timing) return forward_graph(c, level, n, landing, host_x, host_logits, host_out, s);
+  return forward_impl(c, level, n, landing, host_x, host_logits, host_out, s);
+}
+
+extern "C" moe_status moe_ctx_enable_graphs(moe_ctx* c, int enable) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "enable_graphs: null ctx");
+  c->use_graphs = enable != 0;
   return MOE_OK;
 }
 
@@ -1104,9 +1289,26 @@ extern "C" moe_status moe_ctx_xfer(moe_ctx* c, const int64_t* rows_per_card, int
   a.sig = no_signal();
   a.err = cd.err;
   const int g = grid > 0 ? grid : c->sms * 2;
-  MONTA_CUDA(launch_seg_copy(a, vec_bytes(row_bytes, c->row_bytes), g, s));
+  const int vec = vec_bytes(row_bytes, c->row_bytes);
+  a.chunks_per_row = items_per_row(vec, row_bytes);
+  a.split = g;
+  MONTA_CUDA(launch_seg_copy(a, vec, g, s));
   ++c->launches;
   return MOE_OK;
 }
 
 extern "C" int64_t moe_ctx_launch_count(const moe_ctx* c) { return c ? c->launches : 0; }
+
+extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint64_t* out8) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: null ctx");
+  c->debug = enable != 0;
+  if (!out8) return MOE_OK;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  for (auto& cd : c->local)
+    if (cd.id == card) {
+      MONTA_CUDA(cudaDeviceSynchronize());
+      MONTA_CUDA(cudaMemcpy(out8, cd.dbg, 64, cudaMemcpyDeviceToHost));
+      return MOE_OK;
+    }
+  return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: card %d is not local", card);
+}

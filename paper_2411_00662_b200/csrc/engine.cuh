@@ -31,7 +31,10 @@ struct SegList {
 };
 __host__ __device__ inline size_t seglist_bytes(int cap) { return 16 + size_t(cap) * sizeof(Seg); }
 
-enum SegPhase { kPhaseAA = 0, kPhaseAG = 1, kPhaseD2D = 2, kPhaseCAA = 3, kNumPhases = 4 };
+// AA = cross-node legs of the fused permute+AllToAll, AAL = its local
+// (own-node, full-row) legs — separate lists so the copy kernel can run them
+// on disjoint CTA sets and overlap NVLink with HBM traffic.
+enum SegPhase { kPhaseAA = 0, kPhaseAG = 1, kPhaseD2D = 2, kPhaseCAA = 3, kPhaseAAL = 4, kNumPhases = 5 };
 
 // Signals carried in each card's flag array: flags[(sig) * kMaxCards + sender].
 enum Signal {
@@ -43,6 +46,9 @@ enum PhaseSignal { kPsAA = 0, kPsAG = 1, kPsCAA = 2, kPsCAG = 3, kNumPhaseSignal
 
 struct CopyArgs {
   const SegList* list;
+  const SegList* list2;      // optional second list, run by CTAs [split, grid)
+  int32_t split;             // CTAs [0, split) run `list`
+  int32_t chunks_per_row;    // work items per row (kItemBytes each)
   const char* src;
   int64_t src_stride;        // bytes per source row
   const int32_t* gather;     // AA: perm_src; row = gather[seg.src_row + i]
@@ -81,6 +87,7 @@ struct UnpermArgs {
 
 // Launchers (return cudaGetLastError()).
 cudaError_t launch_seg_copy(const CopyArgs& a, int vec, int grid, cudaStream_t s);
+int copy_item_bytes(int vec);  // bytes one warp moves per work item
 cudaError_t launch_gather_rows(const void* src, int64_t src_stride, int64_t col_off, int64_t width,
                                const int32_t* perm, int64_t R, void* out, int64_t out_stride,
                                cudaStream_t s);
@@ -104,17 +111,59 @@ struct PlanArgs {
   int32_t* err;
 };
 size_t plan_scratch_ints(int e, int E, int max_chunks);
+bool plan_fits_smem(int e, int E, int n);
+moe_status configure_plan();
 cudaError_t launch_plan_with_scratch(const PlanArgs& a, int32_t* scratch, cudaStream_t s);
-size_t index_smem_bytes(int E);
-// Push this card's per-chunk counts into the count tables of its peers.
-struct PushCountsArgs {
-  const int32_t* counts;      // [n][E]
-  int32_t n, E, max_chunks, node;
+// Index-build shared memory (ints): hist [nwarps][E] | offs [E+1] | counts [n][E]
+inline size_t index_smem_ints(int nwarps, int E, int n, bool count_in_smem) {
+  return size_t(nwarps) * E + E + 1 + (count_in_smem ? size_t(n) * E : 0);
+}
+// Fused front end (front.cu), one cooperative launch over token tiles:
+// route each tile, histogram it, elect the last CTA to scan tile bases /
+// offsets / chunk counts, bump the device epoch and push this node's counts
+// to its expert-parallel peers (NVLink stores + flags), release the grid,
+// rank every tile's pairs in parallel, then (do_plan) plan.
+struct FrontArgs {
+  const void* logits;   // [T, E] (route != 0)
+  int32_t route;
+  int64_t T;
+  int32_t E, k, n;
+  int32_t* experts;     // [T, k]
+  void* probs;          // [T, k]
+  int32_t* perm_src;
+  int32_t* expert_of;
+  int32_t* slot_pos;
+  int32_t* counts;      // [n, E]
+  int32_t* expert_offsets;
+  int32_t* err;
+  int32_t tile_tokens;  // tokens per tile (= kFrontThreads / G when routing)
+  int32_t n_tiles;
+  int32_t aligned;      // (T / n) % tile_tokens == 0: chunk counts from tile histograms
+  int32_t* tile_hist;   // [n_tiles][E]
+  int32_t* tile_base;   // [n_tiles][E]
+  int32_t* counts_acc;  // [n][E] atomically accumulated when !aligned (zero between launches)
+  unsigned int* arrive; // grid-barrier arrival counter (zero between launches)
+  unsigned long long* ready;  // grid-barrier release flag (= epoch)
+  uint64_t* epoch_dev;  // bumped once per dispatch
+  int32_t node, max_chunks;
   int32_t n_dst;
   int32_t* dst_tables[kMaxCards];
-  SignalList sig;
+  int32_t n_sig;
+  uint64_t* sig_flags[kMaxCards];
+  int32_t do_plan;
+  PlanArgs plan;        // its wait list is satisfied at the bumped epoch
+  int32_t* plan_scratch;
+  int32_t plan_in_smem; // plan tables in (reused) dynamic shared memory
+  unsigned long long* dbg;  // optional phase timestamps [8] (globaltimer ns)
 };
-cudaError_t launch_push_counts(const PushCountsArgs& a, cudaStream_t s);
+constexpr int kFrontThreads = 512;
+moe_status launch_front(const FrontArgs& a, int logit_dtype, cudaStream_t s);
+// Set the front kernel's shared-memory attribute ahead of graph capture.
+moe_status configure_front(int E, int logit_dtype);
+// Router tokens per front CTA, and the index tile length for (E, T, n).
+int front_router_tokens(int E);
+int front_tile_tokens(int E, int64_t T, int n);
+moe_status check_route_args(int64_t T, int E, int k);
 
 moe_status route_topk(const void* logits, int logit_dtype, int64_t T, int E, int k, int32_t* experts,
                       void* probs, cudaStream_t stream);

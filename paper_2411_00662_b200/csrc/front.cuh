@@ -1,0 +1,464 @@
+// Device-side building blocks of the dispatch front end, shared by the
+// standalone kernels (router.cu, index.cu, plan.cu) and the fused front
+// kernel (front.cu):
+//   route_tokens  — top-k gating of the tokens owned by this CTA
+//                   (dataplane::route_topk, dataplane.hpp:72-106);
+//   index_block   — one CTA's stable counting sort of the (token, slot)
+//                   pairs (dataplane::permute, dataplane.hpp:118-140) plus
+//                   per-chunk counts (dataplane.hpp:224-240);
+//   plan_block    — counts -> every offset / segment list of the exchange.
+#pragma once
+
+#include "engine.cuh"
+
+namespace monta {
+
+template <class T> __device__ __forceinline__ T dev_exp(T x);
+template <> __device__ __forceinline__ float dev_exp<float>(float x) { return expf(x); }
+template <> __device__ __forceinline__ double dev_exp<double>(double x) { return exp(x); }
+
+template <class T> __device__ __forceinline__ T neg_inf();
+template <> __device__ __forceinline__ float neg_inf<float>() { return -INFINITY; }
+template <> __device__ __forceinline__ double neg_inf<double>() { return -(double)INFINITY; }
+
+// ---------------------------------------------------------------------------
+// Router: G lanes per token (G = next pow2 >= E, <= 32), PER elements per
+// lane.  Token index = global sub-warp group id.  Softmax in T precision;
+// k rounds of group argmax over RAW scores, ties -> lower index; experts
+// written ascending, probs = softmax values of the selected experts.
+template <class T, int G, int PER>
+__device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64_t T_tokens, int E, int k,
+                                             int32_t* __restrict__ experts, T* __restrict__ probs,
+                                             int64_t token) {
+  const int lane = threadIdx.x & (kWarp - 1);
+  const int sub = lane % G;
+  const bool active = token < T_tokens;
+  const unsigned gmask = (G == 32) ? 0xffffffffu : (((1u << G) - 1u) << ((lane / G) * G));
+  constexpr unsigned kNone = 0x7fffffff;
+  T v[PER];
+  const T* row = logits + (active ? token : 0) * int64_t(E);
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    const int x = sub + m * G;
+    v[m] = (active && x < E) ? row[x] : neg_inf<T>();
+  }
+  T mx = v[0];
+#pragma unroll
+  for (int m = 1; m < PER; ++m) mx = v[m] > mx ? v[m] : mx;
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) {
+    const T o = __shfl_xor_sync(gmask, mx, off, G);
+    mx = o > mx ? o : mx;
+  }
+  T ex[PER];
+  T sum = T(0);
+#pragma unroll
+  for (int m = 0; m < PER; ++m) {
+    const int x = sub + m * G;
+    ex[m] = (x < E) ? dev_exp<T>(v[m] - mx) : T(0);
+    sum += ex[m];
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(gmask, sum, off, G);
+  unsigned taken = 0;
+  int my_sel = -1;
+  T my_soft = T(0);
+  for (int s = 0; s < k; ++s) {
+    T bv = neg_inf<T>();
+    int bi = int(kNone);
+    T bs = T(0);
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int x = sub + m * G;
+      if (x < E && !((taken >> m) & 1u)) {
+        if (bi == int(kNone) || v[m] > bv || (v[m] == bv && x < bi)) {
+          bv = v[m];
+          bi = x;
+          bs = ex[m];
+        }
+      }
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) {
+      const T ov = __shfl_xor_sync(gmask, bv, off, G);
+      const int oi = __shfl_xor_sync(gmask, bi, off, G);
+      const T os = __shfl_xor_sync(gmask, bs, off, G);
+      const bool take = (oi != int(kNone)) && (bi == int(kNone) || ov > bv || (ov == bv && oi < bi));
+      if (take) {
+        bv = ov;
+        bi = oi;
+        bs = os;
+      }
+    }
+    if (bi != int(kNone) && (bi % G) == sub) taken |= 1u << (bi / G);
+    if (sub == s) {
+      my_sel = bi;
+      my_soft = bs / sum;
+    }
+  }
+  int rank = 0;
+  for (int s = 0; s < k; ++s) {
+    const int other = __shfl_sync(gmask, my_sel, (lane / G) * G + s, kWarp);
+    if (other < my_sel) ++rank;
+  }
+  if (active && sub < k) {
+    experts[token * k + rank] = my_sel;
+    probs[token * k + rank] = my_soft;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Index build by one CTA (any warp count).  smem layout (ints):
+//   hist [nw][E] | offs [E+1] | ccount [n][E] (when count_in_smem)
+// Loads of `experts` use the L2-coherent path (.cg): in the fused kernel the
+// router CTAs of the same launch wrote them.
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+
+__device__ __forceinline__ void index_block(const int32_t* experts, int64_t T, int k, int E, int n,
+                                            int32_t* __restrict__ perm_src, int32_t* __restrict__ expert_of,
+                                            int32_t* __restrict__ slot_pos, int32_t* __restrict__ counts,
+                                            int32_t* __restrict__ expert_offsets, int32_t* __restrict__ err,
+                                            int* smem, bool count_in_smem) {
+  constexpr int kUnroll = 8;
+  const int nw = blockDim.x >> 5;
+  int* hist = smem;
+  int* offs = smem + nw * E;
+  int* ccount = count_in_smem ? offs + E + 1 : counts;
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  const int64_t R = T * k;
+  const int64_t ct = T / n;
+  const int64_t per_warp = ((R + nw - 1) / nw + 31) / 32 * 32;
+  const int64_t begin = int64_t(w) * per_warp;
+  const int64_t end = begin + per_warp < R ? begin + per_warp : R;
+  for (int i = tid; i < nw * E + E + 1; i += blockDim.x) smem[i] = 0;
+  for (int i = tid; i < n * E; i += blockDim.x) ccount[i] = 0;
+  __syncthreads();
+  int* my_hist = hist + w * E;
+  for (int64_t base = begin; base < end; base += 32 * kUnroll) {
+    int key[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t p = base + u * 32 + lane;
+      key[u] = p < end ? __ldcg(experts + p) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (base + u * 32 >= end) break;  // warp-uniform
+      const int64_t p = base + u * 32 + lane;
+      int x = key[u];
+      if (p < end && (x >= E || x < 0)) {
+        atomicExch(err, (int)MOE_ERR_INVALID_ARGUMENT);
+        x = -1;
+      }
+      const unsigned peers = __match_any_sync(0xffffffffu, x);
+      if (x >= 0 && lane == __ffs(peers) - 1) my_hist[x] += __popc(peers);
+      // per-(chunk, expert) counts: aggregate lanes with the same key
+      const int ck = x >= 0 ? int((p / k) / ct) * E + x : -1;
+      const unsigned cpeers = __match_any_sync(0xffffffffu, ck);
+      if (ck >= 0 && lane == __ffs(cpeers) - 1) atomicAdd(ccount + ck, __popc(cpeers));
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < E; x += blockDim.x) {
+    int run = 0;
+    for (int ww = 0; ww < nw; ++ww) {
+      const int c = hist[ww * E + x];
+      hist[ww * E + x] = run;
+      run += c;
+    }
+    offs[x] = run;
+  }
+  __syncthreads();
+  if (w == 0) {
+    int carry = 0;
+    for (int x0 = 0; x0 < E; x0 += 32) {
+      const int x = x0 + lane;
+      const int v = x < E ? offs[x] : 0;
+      int inc = v;
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        const int o = __shfl_up_sync(0xffffffffu, inc, off);
+        if (lane >= off) inc += o;
+      }
+      if (x < E) offs[x] = carry + inc - v;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+    if (lane == 0) offs[E] = carry;
+  }
+  __syncthreads();
+  for (int i = tid; i < nw * E; i += blockDim.x) hist[i] += offs[i % E];
+  __syncthreads();
+  for (int64_t base = begin; base < end; base += 32 * kUnroll) {
+    int key[kUnroll];
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      const int64_t p = base + u * 32 + lane;
+      key[u] = p < end ? __ldcg(experts + p) : -1;
+    }
+#pragma unroll
+    for (int u = 0; u < kUnroll; ++u) {
+      if (base + u * 32 >= end) break;
+      const int64_t p = base + u * 32 + lane;
+      int x = key[u];
+      if (x >= E) x = -1;
+      const unsigned peers = __match_any_sync(0xffffffffu, x);
+      int pos = 0;
+      if (x >= 0) pos = my_hist[x] + __popc(peers & lanemask_lt());
+      __syncwarp();
+      if (x >= 0 && lane == __ffs(peers) - 1) my_hist[x] += __popc(peers);
+      __syncwarp();
+      if (x >= 0 && p < end) {
+        expert_of[pos] = x;
+        perm_src[pos] = int32_t(p / k);
+        slot_pos[p] = pos;
+      } else if (p < end) {
+        slot_pos[p] = -1;
+      }
+    }
+  }
+  __syncthreads();
+  if (count_in_smem)
+    for (int i = tid; i < n * E; i += blockDim.x) counts[i] = ccount[i];
+  for (int x = tid; x <= E; x += blockDim.x) expert_offsets[x] = offs[x];
+}
+
+// ---------------------------------------------------------------------------
+// Plan: counts -> every offset / segment list of the exchange, one CTA.
+//
+// Tables (ints), in shared memory when they fit (plan_smem_ints), else in the
+// card's global scratch — same code, different pointers:
+//   ct   [e][n][E]    the exchanged counts (copied once, coalesced)
+//   cum  [e][n+1][E]  rows of (g, x) in chunks < j   (cum[g][n][x] = total)
+//   eo   [e][E+1]     sender-permuted expert offsets per node
+//   fin  [xg][L][e]   final-layout segment base (l-major, then source g)
+//   pre  [xg][n][e*L] staged-layout segment base (chunk-major, g, l)
+//   cb   [xg][n+1]    staged chunk bases
+// Every scan is a warp-level scan (shuffles) so the critical path is a few
+// hundred cycles per table instead of a serial global-memory chain.
+struct PlanTables {
+  int32_t* ct;
+  int32_t* cum;
+  int32_t* eo;
+  int32_t* fin;
+  int32_t* pre;
+  int32_t* cb;
+};
+
+__host__ __device__ inline size_t plan_smem_ints(int e, int E, int n) {
+  return size_t(e) * n * E + size_t(e) * (n + 1) * E + size_t(e) * (E + 1) + size_t(e) * E + size_t(e) * n * E +
+         size_t(e) * (n + 1);
+}
+
+__host__ __device__ inline PlanTables plan_tables(int32_t* base, int e, int E, int n) {
+  PlanTables tb;
+  tb.ct = base;
+  tb.cum = tb.ct + size_t(e) * n * E;
+  tb.eo = tb.cum + size_t(e) * (n + 1) * E;
+  tb.fin = tb.eo + size_t(e) * (E + 1);
+  tb.pre = tb.fin + size_t(e) * E;
+  tb.cb = tb.pre + size_t(e) * n * E;
+  return tb;
+}
+
+__device__ __forceinline__ SegList* plan_list_at(const PlanArgs& a, int phase, int j) {
+  char* base = reinterpret_cast<char*>(a.lists);
+  return reinterpret_cast<SegList*>(base + (size_t(phase) * a.max_chunks + j) * seglist_bytes(a.seg_cap));
+}
+
+// Warp-wide exclusive scan of v; returns the exclusive prefix, *total = sum.
+__device__ __forceinline__ int warp_exscan(int v, int lane, int* total) {
+  int inc = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += o;
+  }
+  *total = __shfl_sync(0xffffffffu, inc, 31);
+  return inc - v;
+}
+__device__ __forceinline__ int64_t warp_exscan64(int64_t v, int lane, int64_t* total) {
+  int64_t inc = v;
+#pragma unroll
+  for (int off = 1; off < 32; off <<= 1) {
+    const int64_t o = __shfl_up_sync(0xffffffffu, inc, off);
+    if (lane >= off) inc += o;
+  }
+  *total = __shfl_sync(0xffffffffu, inc, 31);
+  return inc - v;
+}
+
+__device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& tb) {
+  const int e = a.e, E = a.E, L = a.L, n = a.n, t = a.t;
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
+  // 1. counts (peers wrote them over NVLink: L2-coherent loads)
+  for (int i = tid; i < e * n * E; i += nth) {
+    const int g = i / (n * E), r = i % (n * E);
+    tb.ct[i] = __ldcg(a.count_table + int64_t(g) * a.max_chunks * E + r);
+  }
+  __syncthreads();
+  auto CT = [&](int g, int j, int x) { return tb.ct[(g * n + j) * E + x]; };
+  auto CUM = [&](int g, int j, int x) -> int& { return tb.cum[(g * (n + 1) + j) * E + x]; };
+  // 2. per-(g, x) chunk prefixes
+  for (int q = tid; q < e * E; q += nth) {
+    const int g = q / E, x = q % E;
+    int run = 0;
+    for (int j = 0; j < n; ++j) {
+      CUM(g, j, x) = run;
+      run += CT(g, j, x);
+    }
+    CUM(g, n, x) = run;
+  }
+  __syncthreads();
+  // 3. eo[g][x]: scan over x of totals; 4. fin[xg][l][g]: scan over (l, g)
+  for (int task = wid; task < 2 * e; task += nw) {
+    const int g = task % e;
+    int carry = 0;
+    if (task < e) {
+      for (int x0 = 0; x0 < E; x0 += 32) {
+        const int x = x0 + lane;
+        int tot;
+        const int ex = warp_exscan(x < E ? CUM(g, n, x) : 0, lane, &tot);
+        if (x < E) tb.eo[g * (E + 1) + x] = carry + ex;
+        carry += tot;
+      }
+      if (lane == 0) tb.eo[g * (E + 1) + E] = carry;
+    } else {
+      const int xg = g;
+      for (int u0 = 0; u0 < E; u0 += 32) {  // u = l*e + src, L*e == E
+        const int u = u0 + lane;
+        const int l = u / e, src = u % e;
+        int tot;
+        const int ex = warp_exscan(u < E ? CUM(src, n, xg * L + l) : 0, lane, &tot);
+        if (u < E) tb.fin[(xg * L + l) * e + src] = carry + ex;
+        carry += tot;
+      }
+      if (lane == 0 && xg == a.node) *a.recv_rows = carry;
+    }
+  }
+  // 5. staged bases: within-chunk scan over (g, l) per (xg, j)
+  for (int task = wid; task < e * n; task += nw) {
+    const int xg = task / n, j = task % n;
+    int carry = 0;
+    for (int u0 = 0; u0 < E; u0 += 32) {  // u = src*L + l, e*L == E
+      const int u = u0 + lane;
+      int tot;
+      const int ex = warp_exscan(u < E ? CT(u / L, j, xg * L + u % L) : 0, lane, &tot);
+      if (u < E) tb.pre[(xg * n + j) * E + u] = carry + ex;
+      carry += tot;
+    }
+    if (lane == 0) tb.cb[xg * (n + 1) + j] = carry;
+  }
+  __syncthreads();
+  for (int xg = tid; xg < e; xg += nth) {
+    int run = 0;
+    for (int j = 0; j < n; ++j) {
+      const int c = tb.cb[xg * (n + 1) + j];
+      tb.cb[xg * (n + 1) + j] = run;
+      run += c;
+    }
+    tb.cb[xg * (n + 1) + n] = run;
+  }
+  __syncthreads();
+  for (int i = tid; i < e * n * E; i += nth) tb.pre[i] += tb.cb[(i / (n * E)) * (n + 1) + (i / E) % n];
+  // 6. local permuted->final delta of this node's experts
+  for (int l = tid; l < L; l += nth) {
+    const int x = a.node * L + l;
+    a.local_delta[x] = tb.fin[(a.node * L + l) * e + a.node] - tb.eo[a.node * (E + 1) + x];
+  }
+  __syncthreads();
+  // 7. segment lists: one warp per (phase, chunk); candidates u in [0, E)
+  const bool dedup = a.level != MOE_BASELINE && t > 1;
+  const bool staged = a.landing == MOE_LAND_STAGED;
+  const int full = int(a.row_bytes);
+  const int slice = int(a.row_bytes / t);
+  const int slice_off = a.rho * slice;
+  const int g0 = a.node;
+  const int me = g0 * t + a.rho;
+  for (int task = wid; task < kNumPhases * n; task += nw) {
+    const int phase = task / n, j = task % n;
+    SegList* lst = plan_list_at(a, phase, j);
+    int pos = 0;
+    int64_t rowsum = 0;
+    for (int u0 = 0; u0 < E; u0 += 32) {
+      const int u = u0 + lane;
+      Seg sg;
+      sg.rows = 0;
+      sg.pad = 0;
+      if (u < E) {
+        if (phase == kPhaseAA || phase == kPhaseAAL) {
+          const bool local_list = phase == kPhaseAAL;
+          const int x = local_list ? g0 * L + u : u;
+          const int xg = x / L, l = x % L;
+          if ((local_list && u < L) || (!local_list && xg != g0)) {
+            sg.rows = CT(g0, j, x);
+            sg.src_row = tb.eo[g0 * (E + 1) + x] + CUM(g0, j, x);
+            sg.dst_row = staged ? int64_t(tb.pre[(xg * n + j) * E + g0 * L + l])
+                                : int64_t(tb.fin[(xg * L + l) * e + g0]) + CUM(g0, j, x);
+            const bool rs = dedup && !local_list;
+            sg.dst = xg * t + a.rho;
+            sg.col_off = rs ? slice_off : 0;
+            sg.width = rs ? slice : full;
+            sg.expert = x;
+          }
+        } else {
+          const int src = u / L, l = u % L, x = g0 * L + l;
+          const int rows = CT(src, j, x);
+          const int64_t fin_row = int64_t(tb.fin[(g0 * L + l) * e + src]) + CUM(src, j, x);
+          const int64_t pre_row = tb.pre[(g0 * n + j) * E + src * L + l];
+          if (phase == kPhaseAG) {
+            if (dedup && src != g0) {
+              sg.rows = rows;
+              sg.src_row = sg.dst_row = staged ? pre_row : fin_row;
+              sg.dst = -1;
+              sg.col_off = slice_off;
+              sg.width = slice;
+              sg.expert = x;
+            }
+          } else if (phase == kPhaseD2D) {
+            if (staged) {
+              sg.rows = rows;
+              sg.src_row = pre_row;
+              sg.dst_row = fin_row;
+              sg.dst = me;
+              sg.col_off = 0;
+              sg.width = full;
+              sg.expert = x;
+            }
+          } else {  // kPhaseCAA: expert outputs back to the sender's permuted order
+            if (src != g0) {
+              sg.rows = rows;
+              sg.src_row = fin_row;
+              sg.dst_row = int64_t(tb.eo[src * (E + 1) + x]) + CUM(src, j, x);
+              sg.dst = src * t + a.rho;
+              sg.col_off = dedup ? slice_off : 0;
+              sg.width = dedup ? slice : full;
+              sg.expert = x;
+            }
+          }
+        }
+      }
+      const bool keep = sg.rows > 0;
+      const unsigned ball = __ballot_sync(0xffffffffu, keep);
+      int64_t rtot;
+      const int64_t rex = warp_exscan64(keep ? sg.rows : 0, lane, &rtot);
+      if (keep) {
+        sg.row_begin = rowsum + rex;
+        lst->segs[pos + __popc(ball & ((1u << lane) - 1u))] = sg;
+      }
+      pos += __popc(ball);
+      rowsum += rtot;
+    }
+    if (lane == 0) {
+      lst->nseg = pos;
+      lst->total_rows = rowsum;
+    }
+  }
+}
+
+}  // namespace monta

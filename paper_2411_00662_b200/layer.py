@@ -178,6 +178,10 @@ class MoeLayer:
     def enable_timing(self, on: bool = True) -> None:
         check(self.lib.moe_ctx_enable_timing(self._ctx, int(on)))
 
+    def enable_graphs(self, on: bool = True) -> None:
+        """Replay forward()/forward_host() as captured CUDA graphs."""
+        check(self.lib.moe_ctx_enable_graphs(self._ctx, int(on)))
+
     def spans(self) -> list[tuple[str, int, float, float]]:
         cap = 4096
         arr = (_lib.Span * cap)()

@@ -1,0 +1,21 @@
+"""Phase timestamps of the fused front kernel (dev tool)."""
+import ctypes as C
+import sys
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+from paper_2411_00662_b200.layer import MoeLayer, O1, BASELINE
+
+for (e, t, E, k, T) in [(1, 1, 8, 2, 4096), (1, 1, 160, 6, 8192), (1, 1, 2, 1, 8192), (4, 2, 160, 6, 8192)]:
+    layer = MoeLayer(e, t, E, k, T, 1024, dtype=torch.bfloat16, max_chunks=8)
+    for cd in layer.cards:
+        cd.logits.normal_()
+    layer.lib.moe_ctx_debug_front(layer._ctx, 1, 0, None)
+    for rep in range(3):
+        layer.forward(BASELINE, 1)
+        out = (C.c_uint64 * 8)()
+        layer.lib.moe_ctx_debug_front(layer._ctx, 1, 0, out)
+        v = [out[i] for i in range(6)]
+        print(f"{e}x{t} E={E} k={k} T={T}: route+hist {(v[1]-v[0])/1e3:.1f}us  scan+push {(v[2]-v[1])/1e3:.1f}us  "
+              f"wait {(v[4]-v[3])/1e3:.1f}  plan {(v[5]-v[4])/1e3:.1f}us  to-plan-end {(v[5]-v[0])/1e3:.1f}us")
+    layer.close()

@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--runs", default="0:1:0")  # level:n:landing,...
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--graphs", type=int, default=0)
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -43,6 +44,7 @@ def main():
     layer = MoeLayer(a.e, a.t, a.E, a.k, a.T, a.h, dtype=dt, max_chunks=16, device=local, rank=rank,
                      world_size=world)
     layer.connect()
+    layer.enable_graphs(bool(a.graphs))
     cd = layer.cards[0]
     node = cd.node
     g = torch.Generator().manual_seed(a.seed * 1000 + node)
@@ -53,7 +55,7 @@ def main():
     results = {}
     for spec in a.runs.split(","):
         level, n, landing = (int(v) for v in spec.split(":"))
-        for _ in range(a.repeat):  # repeated steps exercise epoch flags and buffer reuse
+        for _ in range(a.repeat + (2 if a.graphs else 0)):  # repeated steps: epoch flags, buffer reuse, replays
             layer.forward(level, n, landing)
         layer.sync()
         rows = layer.recv_rows(cd.card)

@@ -166,3 +166,77 @@ def test_forward_host_round_trip(cuda):
             assert err < 1e-2
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("level,n,landing", [(BASELINE, 1, LAND_FINAL), (O1, 1, LAND_FINAL), (O3, 4, LAND_STAGED)])
+def test_cuda_graph_replay_matches_eager(cuda, level, n, landing):
+    """forward() captured as a CUDA graph and replayed gives the same bits."""
+    e, t, E, k, T, h = 2, 2, 8, 2, 128, 256
+    x, logits = _inputs(e, T, h, E, torch.bfloat16, 21)
+    outs = []
+    for graphs in (False, True):
+        layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, max_chunks=8)
+        try:
+            layer.enable_graphs(graphs)
+            for cd in layer.cards:
+                cd.x.copy_(x[cd.node])
+                cd.logits.copy_(logits[cd.node])
+            for _ in range(3):  # capture, then replays
+                layer.forward(level, n, landing)
+            layer.sync()
+            outs.append([(cd.recv[:layer.recv_rows(cd.card)].clone(), cd.recv_tags[:layer.recv_rows(cd.card)].clone(),
+                          cd.out.clone()) for cd in layer.cards])
+        finally:
+            layer.close()
+    for (r0, t0, o0), (r1, t1, o1) in zip(*outs):
+        assert torch.equal(r0.view(torch.int16), r1.view(torch.int16))
+        assert torch.equal(t0, t1)
+        assert torch.equal(o0.view(torch.int16), o1.view(torch.int16))
+
+
+def test_combine_requires_a_pending_dispatch(cuda):
+    layer = MoeLayer(2, 2, 4, 1, 16, 8, dtype=torch.float32, max_chunks=2)
+    try:
+        with pytest.raises(ValueError):
+            layer.combine(O1, 1)
+        layer.route()
+        layer.dispatch(O1, 1)
+        layer.combine(O1, 1)
+        with pytest.raises(ValueError):
+            layer.combine(O1, 1)  # one combine per dispatch
+    finally:
+        layer.close()
+
+
+@pytest.mark.parametrize("T,E,k,n", [(8192, 160, 6, 8), (8190, 160, 6, 5), (4096, 8, 2, 1), (8192, 2, 1, 64),
+                                     (3, 4, 2, 3), (0, 8, 2, 1)])
+def test_front_index_matches_oracle_full_size(cuda, T, E, k, n):
+    """The fused front kernel's index (cooperative grid: tile histograms,
+    elected scan, per-tile ranks) equals the oracle's permute at full size,
+    including chunk lengths that do not align with the tiles."""
+    layer = MoeLayer(1, 1, E, k, T, 64, dtype=torch.bfloat16, max_chunks=max(n, 1))
+    try:
+        cd = layer.cards[0]
+        g = torch.Generator(device="cuda").manual_seed(T + E)
+        if T:
+            cd.logits.copy_(torch.randn(T, E, generator=g, device="cuda"))
+        layer.route()
+        if n == 1:
+            layer.dispatch(BASELINE, 1)
+        else:
+            layer.dispatch(O2, n)
+        layer.sync()
+        experts = cd.experts.cpu().numpy()
+        ps, eo, inv, _ = oracle.permute(experts)
+        assert np.array_equal(cd.perm_src.cpu().numpy(), ps)
+        assert np.array_equal(cd.expert_of.cpu().numpy(), eo)
+        assert np.array_equal(cd.slot_pos.cpu().numpy(), inv)
+        want = np.zeros((n, E), np.int64)
+        ct = T // n if n else 0
+        for i in range(T):
+            for x in experts[i]:
+                want[i // ct, x] += 1
+        assert np.array_equal(cd.counts[:n].cpu().numpy(), want)
+        assert np.array_equal(cd.expert_offsets.cpu().numpy(), np.concatenate([[0], np.cumsum(want.sum(0))]))
+    finally:
+        layer.close()

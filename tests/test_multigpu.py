@@ -29,14 +29,14 @@ def _port():
     return p
 
 
-def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0):
+def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0):
     world = e * t
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs, have {torch.cuda.device_count()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--out", str(tmp), "--groups", str(e), "--tp", str(t), "--experts", str(E), "--topk", str(k), "--tokens", str(T),
-           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed)]
+           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
@@ -92,3 +92,9 @@ def test_four_gpus_4x1_finegrained(cuda, tmp_path):
 def test_four_gpus_1x4_fp32(cuda, tmp_path):
     runs = "1:1:0,3:4:1"
     _check(_launch(tmp_path, 1, 4, runs=runs, dtype="f32"), 1, 4, 8, runs, elem=4)
+
+
+def test_four_gpus_2x2_cuda_graphs(cuda, tmp_path):
+    # the captured step replays in lockstep across ranks (device-resident epoch)
+    runs = "0:1:0,3:4:0,2:2:1"
+    _check(_launch(tmp_path, 2, 2, runs=runs, T=512, h=512, graphs=1), 2, 2, 8, runs)
