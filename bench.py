@@ -231,7 +231,7 @@ def main():
 
     # ---- level / chunk count: MoNTA planner on the B200 NVLink curves
     levels = {"baseline": BASELINE, "o1": O1, "o2": O2, "o3": O3}
-    curves_dir = os.path.join(ROOT, "profiles", "curves_b200")
+    curves_dir = os.path.join(ROOT, "profiles", "curves_b200", f"{e}x{t}")
     decision = None
     if args.level != "auto":
         level = levels[args.level]

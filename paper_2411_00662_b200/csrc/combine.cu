@@ -63,7 +63,9 @@ __global__ void __launch_bounds__(kThreads) k_unpermute(const UnpermArgs a) {
       const int pos = __ldg(a.slot_pos + q);
       const int x = __ldg(a.experts + q);
       s_p[wib][lane] = TAcc(__ldg(probs + q));
-      if (a.local_y && x >= a.local_lo && x < a.local_hi) {
+      if (pos < 0) {
+        s_row[wib][lane] = nullptr;  // empty slot (negative expert id)
+      } else if (a.local_y && x >= a.local_lo && x < a.local_hi) {
         s_row[wib][lane] = a.local_y + (int64_t(pos) + __ldg(a.local_delta + x)) * a.y_stride;
       } else {
         s_row[wib][lane] = a.comb + int64_t(pos) * a.y_stride;
@@ -82,6 +84,7 @@ __global__ void __launch_bounds__(kThreads) k_unpermute(const UnpermArgs a) {
       for (int s = 0; s < a.k; ++s) {
         const TAcc p = s_p[wib][s];
         const char* row = s_row[wib][s];
+        if (!row) continue;
         Pack<TIn, N> y[UV];
 #pragma unroll
         for (int w = 0; w < UV; ++w) {

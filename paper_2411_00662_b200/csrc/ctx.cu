@@ -626,6 +626,17 @@ int copy_vec(const moe_ctx* c, bool dedup) {
 }
 
 // One chunk of the fused permute + AllToAll, for one card.
+// Bulk kernels never spin: a kernel that consumes remote data is preceded
+// on its stream by a one-CTA wait kernel.  (A spinning bulk grid can occupy
+// every SM and starve the local producer another GPU is waiting for.)
+moe_status hoist_wait(moe_ctx* c, WaitList& w, int32_t* err, cudaStream_t s) {
+  if (w.n == 0) return MOE_OK;
+  MONTA_CUDA(launch_wait(w, err, s));
+  ++c->launches;
+  w.n = 0;
+  return MOE_OK;
+}
+
 // Work items per row for the copy kernel.
 int items_per_row(int vec, int64_t max_width) {
   const int64_t ib = copy_item_bytes(vec);
@@ -719,6 +730,7 @@ moe_status launch_ag(moe_ctx* c, Card& cd, int j, int landing, cudaStream_t s, b
       if (r != cd.rho) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, cd.node, r), sig_chunk(c, kPsAG, j), cd.id);
   }
   a.err = cd.err;
+  if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;
   size_t sl;
   span_begin(c, MOE_STAGE_AG, j, s, &sl);
   MONTA_CUDA(launch_seg_copy(a, copy_vec(c, true), copy_grid(c, concurrent, false), s));
@@ -752,6 +764,7 @@ moe_status launch_d2d(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bo
   }
   a.sig = no_signal();
   a.err = cd.err;
+  if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;
   size_t sl;
   span_begin(c, MOE_STAGE_D2D, j, s, &sl);
   MONTA_CUDA(launch_seg_copy(a, copy_vec(c, false), copy_grid(c, concurrent, false), s));
@@ -978,6 +991,7 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
   int grid = c->sms * (concurrent ? 2 : 4);
   const int64_t need = (ct + 7) / 8;
   if (need < grid) grid = int(std::max<int64_t>(need, 1));
+  if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;
   size_t sl;
   span_begin(c, MOE_STAGE_UNPERMUTE, j, s, &sl);
   bool ok = true;

@@ -64,7 +64,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const FrontArgs a) {
     const int64_t j0 = i0 / ct;
     for (int64_t q = tid; q < np; q += blockDim.x) {
       const int x = a.experts[i0 * k + q];
-      if (x < 0 || x >= E) {
+      if (x < 0) continue;  // empty slot
+      if (x >= E) {
         atomicExch(a.err, (int)MOE_ERR_INVALID_ARGUMENT);
         continue;
       }
@@ -220,7 +221,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const FrontArgs a) {
     for (int g = wid; g < groups; g += nw) {
       const int q = g * 32 + lane;
       int x = q < np ? a.experts[i0 * k + q] : -1;
-      if (x >= E) x = -1;
+      if (x >= E || x < 0) x = -1;
       const unsigned peers = __match_any_sync(0xffffffffu, x);
       if (x >= 0 && lane == __ffs(peers) - 1) hg[g * E + x] = __popc(peers);
     }
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const FrontArgs a) {
     for (int g = wid; g < groups; g += nw) {
       const int q = g * 32 + lane;
       int x = q < np ? a.experts[i0 * k + q] : -1;
-      if (x >= E) x = -1;
+      if (x >= E || x < 0) x = -1;
       const unsigned peers = __match_any_sync(0xffffffffu, x);
       if (q < np) {
         if (x >= 0) {

@@ -151,10 +151,11 @@ __device__ __forceinline__ void index_block(const int32_t* experts, int64_t T, i
       if (base + u * 32 >= end) break;  // warp-uniform
       const int64_t p = base + u * 32 + lane;
       int x = key[u];
-      if (p < end && (x >= E || x < 0)) {
+      if (p < end && x >= E) {
         atomicExch(err, (int)MOE_ERR_INVALID_ARGUMENT);
         x = -1;
       }
+      if (x < 0) x = -1;  // negative id: an empty slot (the reference's permute never matches it)
       const unsigned peers = __match_any_sync(0xffffffffu, x);
       if (x >= 0 && lane == __ffs(peers) - 1) my_hist[x] += __popc(peers);
       // per-(chunk, expert) counts: aggregate lanes with the same key
@@ -205,7 +206,7 @@ __device__ __forceinline__ void index_block(const int32_t* experts, int64_t T, i
       if (base + u * 32 >= end) break;
       const int64_t p = base + u * 32 + lane;
       int x = key[u];
-      if (x >= E) x = -1;
+      if (x >= E || x < 0) x = -1;
       const unsigned peers = __match_any_sync(0xffffffffu, x);
       int pos = 0;
       if (x >= 0) pos = my_hist[x] + __popc(peers & lanemask_lt());

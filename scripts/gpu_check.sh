@@ -16,3 +16,9 @@ case $what in
   calib8) timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29534 -m paper_2411_00662_b200.calibrate --out gpurun_out/calib > gpurun_out/calib8.log 2>&1; echo "calib8 rc=$?";;
 esac
 done
+for what in "$@"; do
+case $what in
+  sweep4) timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29535 scripts/sweep_levels.py > gpurun_out/sweep4.jsonl 2> gpurun_out/sweep4.err; echo "sweep4 rc=$?";;
+  sweep2) timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29536 scripts/sweep_levels.py > gpurun_out/sweep2.jsonl 2> gpurun_out/sweep2.err; echo "sweep2 rc=$?";;
+esac
+done

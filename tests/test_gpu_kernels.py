@@ -172,3 +172,23 @@ def test_unpermute_combine_matches_oracle(cuda, dtype, out_dtype, rtol):
     got = out.cpu().double().numpy()
     scale = np.abs(want).max()
     assert np.abs(got - want).max() <= rtol * scale + 1e-300
+
+
+def test_build_index_empty_slots_are_skipped(cuda):
+    """Negative expert ids are empty slots (ragged routing padded with -1):
+    like the reference's permute, which only matches experts >= 0."""
+    rng = np.random.default_rng(12)
+    T, E, k = 777, 16, 4
+    experts = np.sort(np.argsort(rng.random((T, E)), axis=1)[:, :k], axis=1).astype(np.int32)
+    drop = rng.random((T, k)) < 0.3
+    experts[drop] = -1
+    ps_ref, eo_ref, inv_ref, il_ref = oracle.permute(experts)
+    idx = ops.build_index(torch.from_numpy(experts).cuda(), E, 1, check=True)
+    torch.cuda.synchronize()
+    valid = int(il_ref.sum())
+    np.testing.assert_array_equal(idx.perm_src.cpu().numpy()[:valid], ps_ref[:valid])
+    np.testing.assert_array_equal(idx.expert_of.cpu().numpy()[:valid], eo_ref[:valid])
+    sp = idx.slot_pos.cpu().numpy()
+    assert (sp[drop] == -1).all()
+    for i in range(T):
+        np.testing.assert_array_equal(np.sort(sp[i][sp[i] >= 0]), inv_ref[i][:il_ref[i]])

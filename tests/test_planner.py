@@ -292,3 +292,26 @@ def test_curve_csv_round_trip(tmp_path):
     (tmp_path / "bad.csv").write_text("volume_bytes,efficiency\n2,0.5\n1,0.5\n")
     with pytest.raises(ValueError):
         P.read_curve_csv(tmp_path / "bad.csv")
+
+
+def test_planner_matches_reference_golden_fixtures():
+    """Fixture form of the exhaustive parity (runs where oracle/_ref is absent)."""
+    import os
+    d = dict(np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "planner.npz")))
+    cl = ClusterSpec(2, 8, 25e9, 200e9, 1.6e12, 312e12, 16)
+    for c in range(int(d["count"])):
+        p = f"c{c}_"
+        cs = CurveSet(*[EfficiencyCurve([CurvePoint(v, e) for v, e in zip(d[p + f"curve{i}_v"], d[p + f"curve{i}_e"])],
+                                        float(d[p + f"curve{i}_imin"])) for i in range(3)])
+        b, s, h, bpe = (int(v) for v in d[p + "model"])
+        t, e, n_cap = (int(v) for v in d[p + "par"])
+        ov = OverheadModel(*[float(v) for v in d[p + "ov"]])
+        m = ModelSpec(b=b, s=s, h=h, bpe=bpe)
+        par = ParallelSpec(t=t, e=e)
+        dec = P.select_strategy(m, par, cl, cs, ov, n_cap)
+        assert (int(dec.level), dec.n) == (int(d[p + "decision"][0]), int(d[p + "decision"][1]))
+        assert dec.t_pred == pytest.approx(float(d[p + "decision"][2]), rel=1e-12)
+        for key, fn in (("o2", P.o2_search), ("o3", P.o3_search)):
+            r = fn(m, par, cl, cs, ov, n_cap)
+            assert (r.n_opt, r.feasible) == (int(d[p + key][0]), bool(d[p + key][2]))
+            assert r.t_pred == pytest.approx(float(d[p + key][1]), rel=1e-12)
