@@ -135,6 +135,20 @@ def exposed(aa, other):
     return tot
 
 
+def role_stats(trace):
+    """From a persistent-kernel role trace [(role, chunk, start_us, end_us)]:
+    busy time per role (union of its chunk intervals) and the exposed
+    AllToAll: AA legs not overlapped by the AllGather/reorder legs, plus the
+    combine's reverse AllToAll not overlapped by the un-permute."""
+    by = {}
+    for r, j, a, b in trace:
+        by.setdefault(r, []).append((a, b))
+    busy = {r: sum(y - x for x, y in interval_union(v)) for r, v in by.items()}
+    exp = exposed(by.get("aa", []), by.get("ag", []) + by.get("d2d", [])) + \
+        exposed(by.get("caa", []), by.get("unpermute", []))
+    return busy, exp
+
+
 # ---------------------------------------------------------------------------
 def cpu_port_layer(e, t, E, k, T, h, seed=0):
     """One full layer of the oracle port (oracle/moe_oracle.c: the C
@@ -306,12 +320,13 @@ def main():
 
     # ---- per-kernel spans (separate pass, events per launch on its stream)
     layer.enable_timing(True)
-    span_sets = []
+    span_sets, traces = [], []
     for _ in range(3):
         flush.zero_()
         barrier()
         step()
         span_sets.append(layer.spans())
+        traces.append(layer.xchg_trace() if world > 1 else [])
     layer.enable_timing(False)
     layer.sync()
 
@@ -323,7 +338,9 @@ def main():
         return {s: {"launches_per_step": len(v) // len(spans_list), "avg_us": 1e3 * sum(v) / len(v),
                     "sum_us_per_step": 1e3 * sum(v) / len(spans_list)} for s, v in out.items()}
 
-    def exposed_aa(spans_list):
+    def exposed_aa(spans_list, traces=None):
+        if traces and any(traces):
+            return statistics.mean(role_stats(tr)[1] for tr in traces)
         vals = []
         for spans in spans_list:
             aa = [(a, b) for st, j, a, b in spans if st == "aa"]
@@ -334,7 +351,11 @@ def main():
         return 1e3 * statistics.mean(vals)
 
     stages = stage_stats(span_sets)
-    exp_aa = exposed_aa(span_sets)
+    exp_aa = exposed_aa(span_sets, traces)
+    roles = None
+    if any(traces):
+        rs = [role_stats(tr)[0] for tr in traces]
+        roles = {r: statistics.mean(x.get(r, 0.0) for x in rs) for r in set().union(*rs)}
 
     # ---- naive TP-redundant exchange at the same N (for the headline ratio)
     naive = None
@@ -344,16 +365,20 @@ def main():
         layer.sync()
         ntot, _ = timed(lambda: step(BASELINE, 1), args.steps)
         layer.enable_timing(True)
-        nspans = []
+        nspans, ntr = [], []
         for _ in range(3):
             flush.zero_()
             barrier()
             step(BASELINE, 1)
             nspans.append(layer.spans())
+            ntr.append(layer.xchg_trace() if world > 1 else [])
         layer.enable_timing(False)
         layer.sync()
-        naive = {"us_per_layer": ntot * 1e3 / args.steps, "exposed_alltoall_us": exposed_aa(nspans),
+        naive = {"us_per_layer": ntot * 1e3 / args.steps, "exposed_alltoall_us": exposed_aa(nspans, ntr),
                  "stages": stage_stats(nspans)}
+        if any(ntr):
+            rs = [role_stats(tr)[0] for tr in ntr]
+            naive["roles_busy_us"] = {r: statistics.mean(x.get(r, 0.0) for x in rs) for r in set().union(*rs)}
 
     # ---- e2e through the C ABI with host buffers
     e2e = None
@@ -441,7 +466,8 @@ def main():
                            {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
                             "t_pred_us": decision.t_pred * 1e6}),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
-            "clocks": clk.summary(), "stages": stages, "exposed_alltoall_us": exp_aa, "naive": naive,
+            "clocks": clk.summary(), "stages": stages, "roles_busy_us": roles, "exposed_alltoall_us": exp_aa,
+            "naive": naive,
             "nvlink": nvlink, "check_max_rel_err": err}
     if rank == 0:
         print(json.dumps(line), flush=True)

@@ -259,6 +259,16 @@ moe_status moe_ctx_xfer(moe_ctx* ctx, const int64_t* rows_per_card, int32_t row_
 /* Debug: record phase timestamps of the fused front kernel (enable != 0);
  * with out8 != NULL, synchronise and copy card's 8 globaltimer stamps (ns). */
 moe_status moe_ctx_debug_front(moe_ctx* ctx, int enable, int card, uint64_t* out8);
+/* Multi-GPU contexts run each phase (dispatch, combine) as ONE persistent,
+ * role-specialised cooperative kernel with per-chunk flags (default on);
+ * enable = 0 selects one launch per (leg, chunk) on prioritised streams. */
+moe_status moe_ctx_set_persistent(moe_ctx* ctx, int enable);
+/* Role trace of the last persistent dispatch/combine (timing enabled):
+ * out[((kernel * 4 + role) * max_chunks + j) * 2 + {0,1}] = globaltimer ns of
+ * the first CTA starting / the last CTA finishing chunk j of the role;
+ * kernel 0 = dispatch (roles AA, AAL, AG, D2D), 1 = combine (CAA, UNP).
+ * Unused entries hold UINT64_MAX / 0xff.. patterns. */
+moe_status moe_ctx_xchg_trace(moe_ctx* ctx, int card, uint64_t* out, int32_t capacity, int32_t* max_chunks);
 /* Number of kernels this context launched since creation. */
 int64_t moe_ctx_launch_count(const moe_ctx* ctx);
 

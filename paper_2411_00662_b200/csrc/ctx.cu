@@ -46,7 +46,7 @@ struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
   size_t lists, local_delta, recv_rows, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
-      ready, total;
+      ready, xchg_counters, xchg_flags, xtrace, total;
 };
 
 struct Card {
@@ -68,6 +68,9 @@ struct Card {
   int32_t* counts_acc = nullptr;      // [max_chunks][E]
   unsigned* arrive = nullptr;         // front grid barrier
   unsigned long long* ready = nullptr;
+  unsigned* xchg_counters = nullptr;  // [4][max_chunks] persistent-exchange chunk counters
+  uint64_t* xchg_flags = nullptr;     // [max_chunks] own-node chunk completion
+  unsigned long long* xtrace = nullptr;  // [2 kernels][4 roles][max_chunks][2] role trace (ns)
   unsigned* front_done = nullptr;  // CTA election counter of the front kernel
 };
 
@@ -96,6 +99,7 @@ struct moe_ctx {
   bool combine_ready = false;  // a dispatch whose combine has not run yet
   bool debug = false;          // record front-kernel phase timestamps
   bool use_graphs = false;
+  bool use_xchg = true;  // persistent role-specialised exchange kernels (multi-GPU)
   struct GraphEntry {
     int level, n, landing;
     const void *hx, *hl;
@@ -166,6 +170,9 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.counts_acc = take(size_t(d.max_chunks) * E * 4);
   s.arrive = take(16);
   s.ready = take(16);
+  s.xchg_counters = take(size_t(8) * d.max_chunks * 17 * 4);  // [dispatch 4 + combine 2 legs][chunk][1 + 16 groups]
+  s.xchg_flags = take(size_t(d.max_chunks) * 8);
+  s.xtrace = take(size_t(2) * 4 * d.max_chunks * 2 * 8);
   s.total = off;
   return s;
 }
@@ -210,6 +217,9 @@ void bind_card(moe_ctx* c, Card& cd) {
   cd.counts_acc = reinterpret_cast<int32_t*>(b + s.counts_acc);
   cd.arrive = reinterpret_cast<unsigned*>(b + s.arrive);
   cd.ready = reinterpret_cast<unsigned long long*>(b + s.ready);
+  cd.xchg_counters = reinterpret_cast<unsigned*>(b + s.xchg_counters);
+  cd.xchg_flags = reinterpret_cast<uint64_t*>(b + s.xchg_flags);
+  cd.xtrace = reinterpret_cast<unsigned long long*>(b + s.xtrace);
 }
 
 void set_peer(moe_ctx* c, int card, char* slab) {
@@ -803,6 +813,106 @@ moe_status dispatch_tail_wait(moe_ctx* c, Card& cd, int level, int n, int landin
   return MOE_OK;
 }
 
+// Whole chunked dispatch of this card in one persistent cooperative launch
+// (xchg.cu).  CTAs are split across roles in proportion to the expected
+// bytes each moves (uniform routing): NVLink legs ~8x slower per byte than
+// local HBM copies.
+moe_status launch_dispatch_xchg(moe_ctx* c, Card& cd, int level, int n, int landing, cudaStream_t s, bool* done) {
+  *done = false;
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  const bool staged = landing == MOE_LAND_STAGED;
+  const int vec = copy_vec(c, dedup);
+  if (vec < 4) return MOE_OK;
+  const int max_ctas = xchg_max_ctas(vec);
+  if (max_ctas < 8) return MOE_OK;
+  XchgArgs x{};
+  x.d2d_in_ag = (staged && dedup && level == MOE_O2) ? 1 : 0;
+  // Role sizes from measured per-CTA rates (calibration, profiles/r01):
+  // an NVLink-store CTA moves ~4 GB/s, an HBM-copy CTA ~20 GB/s.
+  const double row = double(c->row_bytes), rem = (d.e - 1.0) / d.e, loc = 1.0 / d.e;
+  const double kNv = 1.0 / 4.0, kHbm = 1.0 / 20.0;
+  const bool nv_needed = d.e > 1 || dedup;
+  const double w_nv = (d.e > 1 ? rem * (dedup ? row / d.t : row) * kNv : 0.0) +
+                      (dedup ? (d.t - 1.0) * rem * (row / d.t) * kNv : 0.0) +
+                      (x.d2d_in_ag ? row * 2.0 * kHbm : 0.0);
+  const double w_loc = loc * row * 2.0 * kHbm;
+  const double w_d2d = (staged && !x.d2d_in_ag) ? row * 2.0 * kHbm : 0.0;
+  const double wsum = w_nv + w_loc + w_d2d;
+  const int G = max_ctas;
+  auto share = [&](double w, bool needed) {
+    if (!needed) return 0;
+    return std::max(4, int(G * w / wsum + 0.5));
+  };
+  x.r_aa = share(w_nv, nv_needed);
+  x.r_aal = share(w_loc, true);
+  x.r_ag = 0;
+  x.r_d2d = share(w_d2d, staged && !x.d2d_in_ag);
+  while (x.r_aa + x.r_aal + x.r_d2d > max_ctas) {  // trim the largest role
+    int* big = &x.r_aa;
+    for (int* r : {&x.r_aal, &x.r_d2d})
+      if (*r > *big) big = r;
+    if (*big <= 4) return MOE_OK;
+    --*big;
+  }
+  CopyArgs& a = x.cp;
+  a.src = static_cast<const char*>(cd.v.x);
+  a.src_stride = c->row_bytes;
+  a.gather = cd.v.perm_src;
+  a.token_ids = cd.v.token_ids;
+  a.source_card = card_of(c, cd.node, 0);
+  a.synth_tags = 1;
+  a.dst_stride = c->row_bytes;
+  for (int q = 0; q < c->cards; ++q) {
+    if (!c->peer[q].slab) continue;
+    a.dst[q] = staged ? c->peer[q].pre : c->peer[q].recv;
+    a.dst_tags[q] = staged ? c->peer[q].pre_tags : c->peer[q].recv_tags;
+    x.flags[q] = c->peer[q].flags;
+  }
+  a.err = cd.err;
+  x.lists = cd.lists;
+  x.seg_cap = d.num_experts;
+  x.max_chunks = d.max_chunks;
+  x.n = n;
+  x.me = cd.id;
+  x.node = cd.node;
+  x.rho = cd.rho;
+  x.e = d.e;
+  x.t = d.t;
+  x.dedup = dedup ? 1 : 0;
+  x.staged = staged ? 1 : 0;
+  x.cpr_full = items_per_row(vec, c->row_bytes);
+  x.cpr_slice = items_per_row(vec, c->row_bytes / d.t);
+  x.recv_local = static_cast<char*>(cd.v.recv);
+  x.recv_tags_local = cd.v.recv_tags;
+  x.pre_local = static_cast<char*>(cd.v.pre);
+  x.pre_tags_local = cd.v.pre_tags;
+  x.d2d_dst[cd.id] = static_cast<char*>(cd.v.recv);
+  x.d2d_dst_tags[cd.id] = cd.v.recv_tags;
+  for (int r = 0; r < d.t; ++r) {
+    const int q = card_of(c, cd.node, r);
+    if (q == cd.id) continue;
+    x.ag_mask |= 1ull << q;
+    x.ag_dst[q] = staged ? c->peer[q].pre : c->peer[q].recv;
+    x.ag_dst_tags[q] = staged ? c->peer[q].pre_tags : c->peer[q].recv_tags;
+  }
+  x.epoch_ptr = cd.epoch_dev;
+  x.counters = cd.xchg_counters;
+  x.local_flags = cd.xchg_flags;
+  x.err = cd.err;
+  if (c->timing) {
+    x.trace = cd.xtrace;
+    MONTA_CUDA(cudaMemsetAsync(cd.xtrace, 0xff, size_t(4) * d.max_chunks * 2 * 8, s));
+  }
+  size_t sl;
+  span_begin(c, MOE_STAGE_AA, -1, s, &sl);
+  MONTA_CUDA(launch_xchg(x, vec, s));
+  span_end(c, sl, s);
+  ++c->launches;
+  *done = true;
+  return MOE_OK;
+}
+
 moe_status validate_dispatch(moe_ctx* c, int level, int n, int landing) {
   const moe_layer_desc& d = c->d;
   if (level == MOE_BASELINE) {
@@ -881,6 +991,11 @@ moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t
   // AllGather on its own stream, reorder copies on the AllGather stream (O2)
   // or their own (O3).
   Card& cd = c->local[0];
+  if (c->use_xchg) {
+    bool done = false;
+    if (moe_status st = launch_dispatch_xchg(c, cd, level, n, landing, s, &done)) return st;
+    if (done) return MOE_OK;
+  }
   cudaStream_t s_d2d = level == MOE_O3 ? c->s_d2d : c->s_ag;
   MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
   MONTA_CUDA(cudaStreamWaitEvent(c->s_aa, c->ev_fork, 0));
@@ -1003,6 +1118,87 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
   return MOE_OK;
 }
 
+// Whole combine of this card in one persistent cooperative launch: CAA role
+// (reverse AllToAll per chunk) and UNP role (wait, un-permute + output
+// all-gather store per chunk).  *done stays false when no persistent
+// instantiation fits (dtype combination / alignment): per-launch path.
+moe_status launch_combine_persistent(moe_ctx* c, Card& cd, int level, int n, cudaStream_t s, bool* done) {
+  *done = false;
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  const int vec = copy_vec(c, dedup);
+  CombArgs x{};
+  UnpermArgs& u = x.up;
+  u.comb = static_cast<const char*>(cd.v.comb);
+  u.local_y = static_cast<const char*>(cd.v.expert_out);
+  u.local_delta = cd.local_delta;
+  u.local_lo = cd.node * c->L;
+  u.local_hi = (cd.node + 1) * c->L;
+  u.y_stride = c->row_bytes;
+  u.slot_pos = cd.v.slot_pos;
+  u.experts = cd.v.experts;
+  u.probs = cd.v.probs;
+  u.k = d.top_k;
+  u.col_begin = dedup ? int64_t(cd.rho) * (d.hidden / d.t) : 0;
+  u.cols = dedup ? d.hidden / d.t : d.hidden;
+  u.out_stride = d.hidden * int64_t(c->ob);
+  if (dedup) {
+    for (int r = 0; r < d.t; ++r) u.out[u.n_out++] = c->peer[card_of(c, cd.node, r)].out;
+  } else {
+    u.out[u.n_out++] = static_cast<char*>(cd.v.out);
+  }
+  u.err = cd.err;
+  CopyArgs& a = x.cp;
+  a.src = static_cast<const char*>(cd.v.expert_out);
+  a.src_stride = c->row_bytes;
+  a.dst_stride = c->row_bytes;
+  for (int q = 0; q < c->cards; ++q) {
+    if (!c->peer[q].slab) continue;
+    a.dst[q] = c->peer[q].comb;
+    x.flags[q] = c->peer[q].flags;
+  }
+  a.err = cd.err;
+  x.lists = cd.lists;
+  x.seg_cap = d.num_experts;
+  x.max_chunks = d.max_chunks;
+  x.n = n;
+  x.me = cd.id;
+  x.node = cd.node;
+  x.rho = cd.rho;
+  x.e = d.e;
+  x.t = d.t;
+  x.dedup = dedup ? 1 : 0;
+  x.cpr = items_per_row(vec, dedup ? c->row_bytes / d.t : c->row_bytes);
+  x.T = d.tokens;
+  x.epoch_ptr = cd.epoch_dev;
+  x.counters = cd.xchg_counters + 4 * d.max_chunks * 17;
+  x.err = cd.err;
+  if (c->timing) {
+    x.trace = cd.xtrace + size_t(4) * d.max_chunks * 2;
+    MONTA_CUDA(cudaMemsetAsync(x.trace, 0xff, size_t(4) * d.max_chunks * 2 * 8, s));
+  }
+  int max_ctas = 0;
+  if (launch_combine_xchg(x, d.dtype, d.logit_dtype, d.out_dtype, vec, s, &max_ctas) != cudaSuccess) {
+    cudaGetLastError();
+    return MOE_OK;
+  }
+  if (max_ctas < 8) return MOE_OK;
+  x.r_caa = 0;
+  x.r_unp = max_ctas;  // every CTA runs both legs, software-pipelined over chunks
+  size_t sl;
+  span_begin(c, MOE_STAGE_UNPERMUTE, -1, s, &sl);
+  const cudaError_t err = launch_combine_xchg(x, d.dtype, d.logit_dtype, d.out_dtype, vec, s, nullptr);
+  if (err == cudaErrorNotSupported) {
+    cudaGetLastError();
+    return MOE_OK;
+  }
+  MONTA_CUDA(err);
+  span_end(c, sl, s);
+  ++c->launches;
+  *done = true;
+  return MOE_OK;
+}
+
 }  // namespace
 
 namespace {
@@ -1042,6 +1238,11 @@ moe_status combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
     MONTA_CUDA(launch_signal(sg, s));
     MONTA_CUDA(launch_wait(w, cd.err, s));
     c->launches += 2;
+  }
+  if (c->use_xchg) {
+    bool done = false;
+    if (moe_status st = launch_combine_persistent(c, cd, level, n, s, &done)) return st;
+    if (done) return MOE_OK;
   }
   MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
   MONTA_CUDA(cudaStreamWaitEvent(c->s_aa, c->ev_fork, 0));
@@ -1325,4 +1526,25 @@ extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint
       return MOE_OK;
     }
   return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: card %d is not local", card);
+}
+
+extern "C" moe_status moe_ctx_set_persistent(moe_ctx* c, int enable) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "set_persistent: null ctx");
+  c->use_xchg = enable != 0;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_xchg_trace(moe_ctx* c, int card, uint64_t* out, int32_t capacity, int32_t* max_chunks) {
+  if (!c || !out || !max_chunks) return fail(MOE_ERR_INVALID_ARGUMENT, "xchg_trace: null argument");
+  *max_chunks = c->d.max_chunks;
+  const int32_t need = 2 * 4 * c->d.max_chunks * 2;
+  if (capacity < need) return fail(MOE_ERR_INVALID_ARGUMENT, "xchg_trace: need capacity %d", need);
+  MONTA_CUDA(cudaSetDevice(c->device));
+  for (auto& cd : c->local)
+    if (cd.id == card) {
+      MONTA_CUDA(cudaDeviceSynchronize());
+      MONTA_CUDA(cudaMemcpy(out, cd.xtrace, size_t(need) * 8, cudaMemcpyDeviceToHost));
+      return MOE_OK;
+    }
+  return fail(MOE_ERR_INVALID_ARGUMENT, "xchg_trace: card %d is not local", card);
 }

@@ -96,6 +96,59 @@ cudaError_t launch_unpermute(const UnpermArgs& a, int y_dtype, int probs_dtype, 
 cudaError_t launch_wait(const WaitList& w, int32_t* err, cudaStream_t s);
 cudaError_t launch_signal(const SignalList& sg, cudaStream_t s);
 
+// Persistent exchange (xchg.cu): the whole chunked dispatch of one card in
+// one cooperative launch.  CTA roles, in order: AA (cross-node legs), AAL
+// (own-node legs), AG (dedup forward to TP peers; under O2 staged it also
+// runs the reorder), D2D (staged reorder, O3).  Per chunk, each role's last
+// CTA publishes a flag; consumers wait in-kernel (every CTA is co-resident).
+struct XchgArgs {
+  CopyArgs cp;                  // gather/src/dst/tags (src = node batch for AA/AAL)
+  SegList* lists;               // [kNumPhases][max_chunks]
+  int32_t seg_cap, max_chunks, n;
+  int32_t me, node, rho, e, t;
+  int32_t dedup, staged, d2d_in_ag;
+  int32_t r_aa, r_aal, r_ag, r_d2d;  // CTAs per role (AA | AAL | AG | D2D)
+  int32_t cpr_full, cpr_slice;
+  char* recv_local;             // AG source (FINAL) / D2D destination
+  int32_t* recv_tags_local;
+  char* pre_local;              // AG source (STAGED) / D2D source
+  int32_t* pre_tags_local;
+  char* ag_dst[kMaxCards];      // AG destinations (peer recv or pre)
+  int32_t* ag_dst_tags[kMaxCards];
+  char* d2d_dst[kMaxCards];     // reorder destination: [me] = recv_local
+  int32_t* d2d_dst_tags[kMaxCards];
+  uint64_t ag_mask;             // TP peers
+  uint64_t* flags[kMaxCards];   // every card's flag array (peer-mapped)
+  const uint64_t* epoch_ptr;
+  unsigned int* counters;       // [4][max_chunks] per-role chunk completion (local, zero)
+  uint64_t* local_flags;        // [max_chunks] own-node copy of chunk j finished (epoch)
+  unsigned long long* trace;    // optional [4 roles][max_chunks][2] (ns)
+  int32_t* err;
+};
+cudaError_t launch_xchg(const XchgArgs& a, int vec, cudaStream_t s);
+int xchg_max_ctas(int vec);
+
+// Persistent combine (combine.cu): roles CAA (reverse AllToAll of the expert
+// outputs, per chunk) | UNP (wait CAA[j], weighted un-permute of chunk j's
+// tokens, output slice stored to every TP peer = the output AllGather).
+struct CombArgs {
+  UnpermArgs up;
+  CopyArgs cp;
+  SegList* lists;
+  int32_t seg_cap, max_chunks, n;
+  int32_t me, node, rho, e, t, dedup;
+  int32_t r_caa, r_unp, cpr;
+  int64_t T;
+  uint64_t* flags[kMaxCards];
+  const uint64_t* epoch_ptr;
+  unsigned int* counters;  // [2][max_chunks]
+  unsigned long long* trace;  // optional [2 roles][max_chunks][2] (ns)
+  int32_t* err;
+};
+// Returns cudaErrorNotSupported when no persistent instantiation fits.
+cudaError_t launch_combine_xchg(const CombArgs& a, int y_dtype, int probs_dtype, int out_dtype, int vec,
+                                cudaStream_t s, int* max_ctas_out);
+
 // Plan kernel (plan.cu).
 struct PlanArgs {
   const int32_t* count_table;  // [e][max_chunks][E]

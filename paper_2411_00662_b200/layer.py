@@ -182,6 +182,34 @@ class MoeLayer:
         """Replay forward()/forward_host() as captured CUDA graphs."""
         check(self.lib.moe_ctx_enable_graphs(self._ctx, int(on)))
 
+    def set_persistent(self, on: bool = True) -> None:
+        """Multi-GPU: one persistent exchange kernel per phase (default) vs per-chunk launches."""
+        check(self.lib.moe_ctx_set_persistent(self._ctx, int(on)))
+
+    ROLES = (("aa", "aal", "ag", "d2d"), ("caa", "unpermute", "", ""))
+
+    def xchg_trace(self) -> list[tuple[str, int, float, float]]:
+        """Role spans of the last persistent dispatch/combine: (role, chunk, start_us, end_us),
+        relative to the earliest start (timing must be enabled)."""
+        mc = self.max_chunks
+        cap = 2 * 4 * mc * 2
+        arr = (C.c_uint64 * cap)()
+        got = C.c_int32()
+        check(self.lib.moe_ctx_xchg_trace(self._ctx, self.local_cards[0], arr, cap, C.byref(got)))
+        out = []
+        for kern in range(2):
+            for role in range(4):
+                for j in range(mc):
+                    base = ((kern * 4 + role) * mc + j) * 2
+                    a, b = arr[base], arr[base + 1]
+                    if a == 0xFFFFFFFFFFFFFFFF or b == 0xFFFFFFFFFFFFFFFF or not self.ROLES[kern][role]:
+                        continue
+                    out.append((self.ROLES[kern][role], j, a, b))
+        if not out:
+            return []
+        t0 = min(a for _, _, a, _ in out)
+        return [(r, j, (a - t0) / 1e3, (b - t0) / 1e3) for r, j, a, b in out]
+
     def spans(self) -> list[tuple[str, int, float, float]]:
         cap = 4096
         arr = (_lib.Span * cap)()

@@ -82,12 +82,9 @@ def main():
             flush.zero_()
             dist.all_reduce(bar)
             step()
-            sp = layer.spans()
-            aa = [(x, y) for s_, j, x, y in sp if s_ == "aa"]
-            oth = [(x, y) for s_, j, x, y in sp if s_ in ("ag", "d2d")]
-            caa = [(x, y) for s_, j, x, y in sp if s_ == "caa"]
-            unp = [(x, y) for s_, j, x, y in sp if s_ == "unpermute"]
-            exp.append(1e3 * (bench.exposed(aa, oth) + bench.exposed(caa, unp)))
+            busy, ex = bench.role_stats(layer.xchg_trace())
+            exp.append(ex)
+            roles = busy
         layer.enable_timing(False)
         pred = None
         if curves is not None and lv != BASELINE:
@@ -105,6 +102,7 @@ def main():
         if rank == 0:
             print(json.dumps({"topology": f"{e}x{t}", "level": ["Baseline", "O1", "O2", "O3"][lv], "n": n,
                               "us_per_layer": float(v.item()), "exposed_alltoall_us": sum(exp) / len(exp),
+                              "roles_busy_us": {r: round(x, 1) for r, x in roles.items()},
                               "planner_dispatch_pred_us": None if pred is None else pred * 1e6}), flush=True)
     layer.close()
     dist.barrier()

@@ -35,6 +35,7 @@ def main():
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graphs", type=int, default=0)
+    ap.add_argument("--persistent", type=int, default=1)
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -45,6 +46,7 @@ def main():
                      world_size=world)
     layer.connect()
     layer.enable_graphs(bool(a.graphs))
+    layer.set_persistent(bool(a.persistent))
     cd = layer.cards[0]
     node = cd.node
     g = torch.Generator().manual_seed(a.seed * 1000 + node)

@@ -29,14 +29,14 @@ def _port():
     return p
 
 
-def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0):
+def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0, persistent=1):
     world = e * t
     if torch.cuda.device_count() < world:
         pytest.skip(f"needs {world} GPUs, have {torch.cuda.device_count()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--out", str(tmp), "--groups", str(e), "--tp", str(t), "--experts", str(E), "--topk", str(k), "--tokens", str(T),
-           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs)]
+           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs), "--persistent", str(persistent)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
@@ -98,3 +98,15 @@ def test_four_gpus_2x2_cuda_graphs(cuda, tmp_path):
     # the captured step replays in lockstep across ranks (device-resident epoch)
     runs = "0:1:0,3:4:0,2:2:1"
     _check(_launch(tmp_path, 2, 2, runs=runs, T=512, h=512, graphs=1), 2, 2, 8, runs)
+
+
+def test_four_gpus_2x2_per_chunk_launches(cuda, tmp_path):
+    # the per-(leg, chunk) launch path on prioritised streams (persistent kernels off)
+    runs = "0:1:0,1:1:0,2:2:0,3:4:0,2:4:1,3:2:1"
+    _check(_launch(tmp_path, 2, 2, runs=runs, T=512, h=512, persistent=0), 2, 2, 8, runs)
+
+
+def test_four_gpus_2x2_deep_chunking(cuda, tmp_path):
+    # many chunks through the persistent exchange (per-chunk flags in-kernel)
+    runs = "3:16:0,2:8:1,3:16:1"
+    _check(_launch(tmp_path, 2, 2, runs=runs, T=1024, h=256), 2, 2, 8, runs)
