@@ -1286,9 +1286,58 @@ extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* st
 namespace {
 
 // route + dispatch + combine, optionally wrapped in host<->device copies.
+// Single-card end to end with host buffers, pipelined per token chunk: the
+// host->device copy of chunk j+1, the layer of chunk j (its rows never leave
+// the chunk on one card: AA(j) then un-permute(j)) and the device->host copy
+// of chunk j-1 run concurrently (copy engines both ways + SMs).  The result
+// is identical to the unpipelined path; only the schedule differs.
+moe_status forward_host_pipelined(moe_ctx* c, int level, int landing, const void* hx, const void* hl, void* ho,
+                                  cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  Card& cd = c->local[0];
+  int P = std::min(8, d.max_chunks);
+  while (P > 1 && d.tokens % P) --P;
+  const int64_t ct = d.tokens / P;
+  const size_t xrow = size_t(c->row_bytes), orow = size_t(d.hidden) * c->ob;
+  const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;
+  MONTA_CUDA(cudaMemcpyAsync(cd.v.logits, hl, lbytes, cudaMemcpyHostToDevice, s));
+  // x chunks on the copy-in stream
+  MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_aa, c->ev_fork, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_d2d, c->ev_fork, 0));
+  for (int j = 0; j < P; ++j) {
+    MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(cd.v.x) + size_t(j) * ct * xrow,
+                               static_cast<const char*>(hx) + size_t(j) * ct * xrow, size_t(ct) * xrow,
+                               cudaMemcpyHostToDevice, c->s_aa));
+    MONTA_CUDA(cudaEventRecord(c->ev_aa[j], c->s_aa));
+  }
+  c->last_level = level;
+  c->last_n = P;
+  c->last_landing = MOE_LAND_FINAL;
+  if (moe_status st = do_front(c, true, level, P, MOE_LAND_FINAL, s)) return st;
+  for (int j = 0; j < P; ++j) {
+    MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_aa[j], 0));
+    if (moe_status st = launch_aa(c, cd, level, j, MOE_LAND_FINAL, s, false)) return st;
+    if (moe_status st = launch_unperm(c, cd, level, P, j, s, false)) return st;
+    MONTA_CUDA(cudaEventRecord(c->ev_ag[j], s));
+    MONTA_CUDA(cudaStreamWaitEvent(c->s_d2d, c->ev_ag[j], 0));
+    MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(ho) + size_t(j) * ct * orow,
+                               static_cast<const char*>(cd.v.out) + size_t(j) * ct * orow, size_t(ct) * orow,
+                               cudaMemcpyDeviceToHost, c->s_d2d));
+  }
+  MONTA_CUDA(cudaEventRecord(c->ev_join_d2d, c->s_d2d));
+  MONTA_CUDA(cudaEventRecord(c->ev_join_aa, c->s_aa));
+  MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_d2d, 0));
+  MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_aa, 0));
+  c->combine_ready = false;
+  return MOE_OK;
+}
+
 moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
                         cudaStream_t s) {
   const moe_layer_desc& d = c->d;
+  if (hx && is_virtual(c) && c->local.size() == 1 && !c->timing && c->d.tokens > 0)
+    return forward_host_pipelined(c, level, landing, hx, hl, ho, s);
   const size_t xbytes = size_t(d.tokens) * c->row_bytes;
   const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;
   const size_t obytes = size_t(d.tokens) * d.hidden * c->ob;

@@ -240,3 +240,32 @@ def test_front_index_matches_oracle_full_size(cuda, T, E, k, n):
         assert np.array_equal(cd.expert_offsets.cpu().numpy(), np.concatenate([[0], np.cumsum(want.sum(0))]))
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("graphs", [False, True])
+def test_forward_host_pipelined_single_card_bit_exact(cuda, graphs):
+    """Single-card forward_host pipelines host copies against the layer per
+    token chunk; the output must be bit-identical to the device path."""
+    T, h, E, k = 4096, 1024, 8, 2
+    x, logits = _inputs(1, T, h, E, torch.bfloat16, 31)
+    layer = MoeLayer(1, 1, E, k, T, h, dtype=torch.bfloat16, max_chunks=16)
+    try:
+        layer.enable_graphs(graphs)
+        cd = layer.cards[0]
+        cd.x.copy_(x[0])
+        cd.logits.copy_(logits[0])
+        layer.forward(BASELINE, 1)
+        layer.sync()
+        want = cd.out.clone()
+        cd.out.zero_()
+        cd.x.zero_()
+        hx = x[0].contiguous().pin_memory()
+        hl = logits[0].contiguous().pin_memory()
+        ho = torch.zeros(T, h, dtype=torch.bfloat16).pin_memory()
+        for _ in range(3):
+            layer.forward_host(hx, hl, ho, BASELINE, 1)
+        torch.cuda.synchronize()
+        layer.sync()
+        assert torch.equal(ho.view(torch.int16), want.cpu().view(torch.int16))
+    finally:
+        layer.close()
