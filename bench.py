@@ -413,7 +413,9 @@ def main():
     Rdst = layer.recv_rows(cd.card)
     # algorithmic bytes per launch
     if world == 1:
-        aa_bytes = 2 * R * row + 16 * R + 4 * R
+        # token-side AA: each token row read once, written to its k destinations,
+        # + tags (16 B/row) and the index reads (experts, slot_pos: 8 B/pair)
+        aa_bytes = T * row + R * row + 16 * R + 8 * R
     else:
         aa_bytes = None  # NVLink-bound: reported under "nvlink"
     unp_cols = h // t if (level != BASELINE and t > 1) else h
@@ -428,7 +430,7 @@ def main():
     if dom == "aa" and aa_bytes:
         ach = kern["fused_permute_aa"]
         traffic_alg = aa_bytes
-        dom_name = "fused_permute_aa (k_seg_copy<16>)"
+        dom_name = "fused_permute_aa (k_aa_token<16>)"
     else:
         ach = kern.get("unpermute_combine", 0.0)
         traffic_alg = unp_bytes

@@ -75,7 +75,7 @@ __device__ __forceinline__ void unpermute_tokens(const UnpermArgs& a, int64_t to
     __syncwarp();
     // UV column vectors per lane per batch; for every slot the UV loads are
     // independent, and no store intervenes, so k*UV loads are in flight.
-    constexpr int UV = N >= 8 ? 4 : 2;
+    constexpr int UV = N >= 8 ? 8 : 2;
     for (int64_t v0 = lane; v0 < nvec; v0 += 32 * UV) {
       TAcc acc[UV][N];
 #pragma unroll

@@ -46,7 +46,7 @@ struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
   size_t lists, local_delta, recv_rows, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
-      ready, xchg_counters, xchg_flags, xtrace, total;
+      ready, xchg_counters, xchg_flags, xtrace, aa_table, total;
 };
 
 struct Card {
@@ -71,6 +71,7 @@ struct Card {
   unsigned* xchg_counters = nullptr;  // [4][max_chunks] persistent-exchange chunk counters
   uint64_t* xchg_flags = nullptr;     // [max_chunks] own-node chunk completion
   unsigned long long* xtrace = nullptr;  // [2 kernels][4 roles][max_chunks][2] role trace (ns)
+  int32_t* aa_table = nullptr;        // [4 + max_chunks][E] token-side AA destinations
   unsigned* front_done = nullptr;  // CTA election counter of the front kernel
 };
 
@@ -173,6 +174,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.xchg_counters = take(size_t(8) * d.max_chunks * 17 * 4);  // [dispatch 4 + combine 2 legs][chunk][1 + 16 groups]
   s.xchg_flags = take(size_t(d.max_chunks) * 8);
   s.xtrace = take(size_t(2) * 4 * d.max_chunks * 2 * 8);
+  s.aa_table = take(size_t(4 + d.max_chunks) * E * 4);
   s.total = off;
   return s;
 }
@@ -220,6 +222,7 @@ void bind_card(moe_ctx* c, Card& cd) {
   cd.xchg_counters = reinterpret_cast<unsigned*>(b + s.xchg_counters);
   cd.xchg_flags = reinterpret_cast<uint64_t*>(b + s.xchg_flags);
   cd.xtrace = reinterpret_cast<unsigned long long*>(b + s.xtrace);
+  cd.aa_table = reinterpret_cast<int32_t*>(b + s.aa_table);
 }
 
 void set_peer(moe_ctx* c, int card, char* slab) {
@@ -544,6 +547,7 @@ PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
   a.seg_cap = d.num_experts;
   a.lists = cd.lists;
   a.local_delta = cd.local_delta;
+  a.aa_table = cd.aa_table;
   a.recv_rows = cd.recv_rows;
   a.err = cd.err;
   a.wait = no_wait();
@@ -659,6 +663,45 @@ int items_per_row(int vec, int64_t max_width) {
 moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaStream_t s, bool concurrent) {
   const moe_layer_desc& d = c->d;
   const bool dedup = level != MOE_BASELINE && d.t > 1;
+  if (d.top_k <= 16) {  // token-side: each row read once, stored to its k destinations
+    TokArgs t{};
+    t.x = static_cast<const char*>(cd.v.x);
+    t.row_bytes = c->row_bytes;
+    t.experts = cd.v.experts;
+    t.slot_pos = cd.v.slot_pos;
+    t.token_ids = cd.v.token_ids;
+    t.source_card = card_of(c, cd.node, 0);
+    t.table = cd.aa_table;
+    t.E = d.num_experts;
+    t.k = d.top_k;
+    t.n = c->last_n;
+    t.j = j;
+    t.staged = landing == MOE_LAND_STAGED ? 1 : 0;
+    const int64_t ct = d.tokens / std::max(1, c->last_n);
+    t.tok_begin = int64_t(j) * ct;
+    t.tok_end = t.tok_begin + ct;
+    t.dst_stride = c->row_bytes;
+    for (int q = 0; q < c->cards; ++q) {
+      if (!c->peer[q].slab) continue;
+      t.dst[q] = t.staged ? c->peer[q].pre : c->peer[q].recv;
+      t.dst_tags[q] = t.staged ? c->peer[q].pre_tags : c->peer[q].recv_tags;
+    }
+    t.sig = no_signal();
+    t.sig.epoch_ptr = cd.epoch_dev;
+    t.sig.done = cd.done + kPsAA * d.max_chunks + j;
+    if (!is_virtual(c))
+      for (int x = 0; x < d.e; ++x)
+        if (x != cd.node) t.sig.flags[t.sig.n++] = flag_at(c, card_of(c, x, cd.rho), sig_chunk(c, kPsAA, j), cd.id);
+    t.err = cd.err;
+    int grid = int(std::min<int64_t>((ct + 7) / 8, int64_t(c->sms) * (concurrent ? 2 : 8)));
+    grid = std::max(grid, 1);
+    size_t sl;
+    span_begin(c, MOE_STAGE_AA, j, s, &sl);
+    MONTA_CUDA(launch_aa_token(t, copy_vec(c, dedup), grid, s));
+    span_end(c, sl, s);
+    ++c->launches;
+    return MOE_OK;
+  }
   CopyArgs a{};
   const int grid = copy_grid(c, concurrent, true);
   if (d.e > 1) {

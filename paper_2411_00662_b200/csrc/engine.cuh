@@ -96,6 +96,27 @@ cudaError_t launch_unpermute(const UnpermArgs& a, int y_dtype, int probs_dtype, 
 cudaError_t launch_wait(const WaitList& w, int32_t* err, cudaStream_t s);
 cudaError_t launch_signal(const SignalList& sg, cudaStream_t s);
 
+// Token-side fused permute + AllToAll (aa.cu): one warp per token reads the
+// row once and stores it (or this rank's 1/t slice of it) to each of its k
+// destinations; dst row = table base of its expert + its permuted position.
+struct TokArgs {
+  const char* x;
+  int64_t row_bytes;
+  const int32_t* experts;   // [T, k]
+  const int32_t* slot_pos;  // [T, k]
+  const int32_t* token_ids;
+  int32_t source_card;
+  const int32_t* table;     // PlanArgs::aa_table
+  int32_t E, k, n, j, staged;
+  int64_t tok_begin, tok_end;
+  int64_t dst_stride;
+  char* dst[kMaxCards];
+  int32_t* dst_tags[kMaxCards];
+  SignalList sig;
+  int32_t* err;
+};
+cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s);
+
 // Persistent exchange (xchg.cu): the whole chunked dispatch of one card in
 // one cooperative launch.  CTA roles, in order: AA (cross-node legs), AAL
 // (own-node legs), AG (dedup forward to TP peers; under O2 staged it also
@@ -159,6 +180,7 @@ struct PlanArgs {
   int32_t seg_cap;             // capacity of each list
   SegList* lists;              // [kNumPhases][max_chunks] lists, stride seglist_bytes(seg_cap)
   int32_t* local_delta;        // [E]
+  int32_t* aa_table;           // [4][E] {card, base_final, col_off, width} + [n][E] base_staged
   int64_t* recv_rows;          // [1]
   WaitList wait;
   int32_t* err;

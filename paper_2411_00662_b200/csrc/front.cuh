@@ -372,6 +372,24 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
     const int x = a.node * L + l;
     a.local_delta[x] = tb.fin[(a.node * L + l) * e + a.node] - tb.eo[a.node * (E + 1) + x];
   }
+  // 6b. per-expert destination table of this sender for the token-side AA:
+  //     dst row of permuted position p = base[x] + p on card[x], columns
+  //     [off, off + width) (this rank's slice on cross-node legs under dedup)
+  if (a.aa_table) {
+    const bool dd = a.level != MOE_BASELINE && t > 1;
+    const int g = a.node;
+    for (int x = tid; x < E; x += nth) {
+      const int xg = x / L, l = x % L;
+      const int eo = tb.eo[g * (E + 1) + x];
+      const bool slice = dd && xg != g;
+      a.aa_table[x] = xg * t + a.rho;
+      a.aa_table[E + x] = tb.fin[(xg * L + l) * e + g] - eo;
+      a.aa_table[2 * E + x] = slice ? a.rho * int(a.row_bytes / t) : 0;
+      a.aa_table[3 * E + x] = slice ? int(a.row_bytes / t) : int(a.row_bytes);
+      for (int j = 0; j < n; ++j)
+        a.aa_table[(4 + j) * E + x] = tb.pre[(xg * n + j) * E + g * L + l] - eo - CUM(g, j, x);
+    }
+  }
   __syncthreads();
   // 7. segment lists: one warp per (phase, chunk); candidates u in [0, E)
   const bool dedup = a.level != MOE_BASELINE && t > 1;
