@@ -16,7 +16,7 @@ Baseline (naive AllToAll) for t == 1; the naive TP-redundant exchange is
 timed alongside.
 
 Timing: W warm-up steps; K timed steps, each bracketed by CUDA events on the
-launching stream after an L2 flush (256 MiB memset) and a cross-rank barrier
+launching stream after an L2 flush (256 MiB memset + 256 MiB read) and a cross-rank barrier
 (both outside the events); value = sum over steps, max over ranks.  e2e is
 the same step through the C ABI host-buffer call (moe_ctx_forward_host: H2D
 of x/logits from pinned memory, the layer, D2H of the output).
@@ -40,6 +40,7 @@ CONFIG = {"workload": "mixtral-8x7b-moe-layer", "tokens_per_node": 4096, "hidden
           "top_k": 2, "dtype": "bf16", "logits": "f32"}
 TOPOLOGY = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}
 METRIC = "moe_dispatch_combine_us_per_layer"
+SPAN_LEAD_CYCLES = 2_000_000  # ~1 ms spin ahead of each per-kernel span pass
 L2_FLUSH_BYTES = 256 << 20
 
 
@@ -278,6 +279,15 @@ def main():
     cd.x.copy_(x0)
     cd.logits.copy_(l0)
     flush = torch.empty(L2_FLUSH_BYTES, dtype=torch.uint8, device=f"cuda:{local}")
+    flush_rd = torch.ones(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def cold_l2():
+        # write a buffer larger than L2 (evicts everything), then read another
+        # one: the memset's dirty lines are written back here, outside the
+        # events, so the step starts from a cold AND clean L2 (what ncu's
+        # --cache-control all gives each kernel)
+        flush.zero_()
+        flush_rd.amax()
     stream = torch.cuda.current_stream()
     bar = torch.zeros(1, device=f"cuda:{local}")
 
@@ -291,7 +301,7 @@ def main():
         barrier()
         torch.cuda.synchronize()
         for a, b in evs:
-            flush.zero_()
+            cold_l2()
             barrier()
             a.record(stream)
             step_fn()
@@ -322,8 +332,9 @@ def main():
     layer.enable_timing(True)
     span_sets, traces = [], []
     for _ in range(3):
-        flush.zero_()
+        cold_l2()
         barrier()
+        torch.cuda._sleep(SPAN_LEAD_CYCLES)  # the host enqueues the whole step before the GPU reaches it
         step()
         span_sets.append(layer.spans())
         traces.append(layer.xchg_trace() if world > 1 else [])
@@ -367,8 +378,9 @@ def main():
         layer.enable_timing(True)
         nspans, ntr = [], []
         for _ in range(3):
-            flush.zero_()
+            cold_l2()
             barrier()
+            torch.cuda._sleep(SPAN_LEAD_CYCLES)
             step(BASELINE, 1)
             nspans.append(layer.spans())
             ntr.append(layer.xchg_trace() if world > 1 else [])
@@ -463,7 +475,7 @@ def main():
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn x, randn f32 gate logits)",
             "config": dict(CONFIG, topology=f"{e}x{t}", level=_lib.LEVEL_NAMES[level], chunks=n,
                            landing=args.landing, parallelism=f"ep{e}xtp{t}", cuda_graphs=not args.no_graphs,
-                           l2="flushed between steps (256 MiB memset outside the events)",
+                           l2="flushed between steps (256 MiB memset + 256 MiB read outside the events: cold, clean L2)",
                            planner=None if decision is None else
                            {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
                             "t_pred_us": decision.t_pred * 1e6}),

@@ -257,8 +257,8 @@ moe_status moe_ctx_set_aa_ctas(moe_ctx* ctx, int32_t ctas);
 moe_status moe_ctx_xfer(moe_ctx* ctx, const int64_t* rows_per_card, int32_t row_bytes, int32_t grid,
                         void* stream);
 /* Debug: record phase timestamps of the fused front kernel (enable != 0);
- * with out8 != NULL, synchronise and copy card's 8 globaltimer stamps (ns). */
-moe_status moe_ctx_debug_front(moe_ctx* ctx, int enable, int card, uint64_t* out8);
+ * with out16 != NULL, synchronise and copy card's 16 globaltimer stamps (ns). */
+moe_status moe_ctx_debug_front(moe_ctx* ctx, int enable, int card, uint64_t* out16);
 /* Multi-GPU contexts run each phase (dispatch, combine) as ONE persistent,
  * role-specialised cooperative kernel with per-chunk flags (default on);
  * enable = 0 selects one launch per (leg, chunk) on prioritised streams. */

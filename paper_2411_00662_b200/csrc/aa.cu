@@ -2,15 +2,22 @@
 // dispatch_chunked data movement, dataplane.hpp:145-283).
 //
 // The permute-side form gathers each of the R = T*k destination rows from
-// its source row (x is read k times).  Here one warp owns a TOKEN: it reads
-// the token's row once, 4 KiB piece by piece (all loads of a piece in flight
-// before any store), and stores each piece to every destination of the
-// token — the final (or staged) row of each selected expert on its card,
-// full width on own-node legs, this rank's 1/t column slice on cross-node
-// legs under TP dedup (hidden_shard, dataplane.hpp:166-176).  The row index
-// is base[expert] + slot_pos: the plan's per-expert table turns the permuted
-// position into the receiver's offset.  Tags {token_id, source_card,
-// source_position, expert} are written once per destination row.
+// its source row (x is read k times).  Here a warp owns an ITEM = (token,
+// piece of 32*U vectors): it loads the piece of the token's row once (all U
+// loads in flight) and stores it to every destination of the token — the
+// final (or staged) row of each selected expert on its card, full width on
+// own-node legs, this rank's 1/t column slice on cross-node legs under TP
+// dedup (hidden_shard, dataplane.hpp:166-176).  The row index is
+// base[expert] + slot_pos: the plan's per-expert table turns the permuted
+// position into the receiver's offset.  Lanes 0..k-1 resolve one destination
+// each and the store loop takes them by shuffle (no staging).  Tags
+// {token_id, source_card, source_position, expert} are written once per
+// destination row, by the token's first piece.
+//
+// Sub-row items and a small register budget (four CTAs, 32 warps per SM) are
+// what keep enough loads in flight: the gather micro-benchmark
+// (scripts/micro/gather_bench.cu) gains ~10% from 16 to 32 warps per SM at
+// equal bytes in flight.
 #include "copy.cuh"
 
 namespace monta {
@@ -20,22 +27,25 @@ constexpr int kTokThreads = 256;
 constexpr int kTokMaxK = 16;
 
 template <int V>
-__global__ void __launch_bounds__(kTokThreads) k_aa_token(const __grid_constant__ TokArgs a) {
+__global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_constant__ TokArgs a) {
   using Vec = typename VecT<V>::type;
-  constexpr int U = CopyUnroll<V>::value;
-  constexpr int kPiece = 32 * V * U;
-  __shared__ char* s_dst[kTokThreads / 32][kTokMaxK];
-  __shared__ int s_off[kTokThreads / 32][kTokMaxK];
-  __shared__ int s_end[kTokThreads / 32][kTokMaxK];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  constexpr int U = 64 / V > 4 ? 4 : (64 / V < 1 ? 1 : 64 / V);  // 16-byte vectors: 4 per lane (2 KiB pieces)
+  constexpr int kPieceVec = 32 * U;
+  const int lane = threadIdx.x & 31;
   const int E = a.E, k = a.k;
-  for (int64_t i = a.tok_begin + int64_t(blockIdx.x) * (blockDim.x / 32) + w; i < a.tok_end; i += warps) {
+  const int64_t nvec = a.row_bytes / V;
+  const int64_t pieces = (nvec + kPieceVec - 1) / kPieceVec;
+  const int64_t n_items = (a.tok_end - a.tok_begin) * pieces;
+  const int64_t warps = int64_t(gridDim.x) * (kTokThreads / 32);
+  for (int64_t it = int64_t(blockIdx.x) * (kTokThreads / 32) + (threadIdx.x >> 5); it < n_items; it += warps) {
+    const int64_t i = a.tok_begin + it / pieces;
+    const int64_t v0 = (it % pieces) * kPieceVec;
+    // lane s < k: destination of slot s (row pointer, byte window [off, end))
+    char* dp = nullptr;
+    int off = 0, end = 0;
     if (lane < k) {
       const int64_t q = i * k + lane;
       const int x = __ldg(a.experts + q);
-      char* dp = nullptr;
-      int off = 0, end = 0;
       if (x >= 0 && x < E) {
         const int p = __ldg(a.slot_pos + q);
         const int card = __ldg(a.table + x);
@@ -44,39 +54,31 @@ __global__ void __launch_bounds__(kTokThreads) k_aa_token(const __grid_constant_
         off = __ldg(a.table + 2 * E + x);
         end = off + __ldg(a.table + 3 * E + x);
         dp = a.dst[card] + row * a.dst_stride;
-        if (a.dst_tags[card])
-          *reinterpret_cast<int4*>(a.dst_tags[card] + 4 * row) =
-              make_int4(__ldg(a.token_ids + i), a.source_card, int(i), x);
+        if (v0 == 0 && a.dst_tags[card])
+          *reinterpret_cast<int4*>(a.dst_tags[card] + 4 * row) = make_int4(__ldg(a.token_ids + i), a.source_card,
+                                                                             int(i), x);
       }
-      s_dst[w][lane] = dp;
-      s_off[w][lane] = off;
-      s_end[w][lane] = end;
     }
-    __syncwarp();
     const Vec* src = reinterpret_cast<const Vec*>(a.x + i * a.row_bytes);
-    const int64_t nvec = a.row_bytes / V;
-    for (int64_t v0 = 0; v0 < nvec; v0 += 32 * U) {
-      Vec r[U];
+    Vec r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + u * 32 + lane;
+      if (v < nvec) r[u] = ld_stream(src + v);
+    }
+    const int64_t piece_lo = v0 * V, piece_hi = piece_lo + int64_t(kPieceVec) * V;
+    for (int s = 0; s < k; ++s) {
+      char* d = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dp), s));
+      const int o = __shfl_sync(0xffffffffu, off, s), e = __shfl_sync(0xffffffffu, end, s);
+      if (!d || e <= piece_lo || o >= piece_hi) continue;  // warp-uniform
+      Vec* dv = reinterpret_cast<Vec*>(d);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) r[u] = ld_stream(src + v);
-      }
-      const int64_t piece_lo = v0 * V, piece_hi = piece_lo + kPiece;
-      for (int s = 0; s < k; ++s) {
-        char* dp = s_dst[w][s];
-        const int off = s_off[w][s], end = s_end[w][s];
-        if (!dp || end <= piece_lo || off >= piece_hi) continue;  // warp-uniform
-        Vec* dv = reinterpret_cast<Vec*>(dp);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int64_t v = v0 + u * 32 + lane;
-          const int64_t byte = v * V;
-          if (v < nvec && byte >= off && byte < end) st_vec(dv + v, r[u]);
-        }
+        const int64_t byte = v * V;
+        if (v < nvec && byte >= o && byte < e) st_vec(dv + v, r[u]);
       }
     }
-    __syncwarp();
   }
   cta_signal(a.sig);
 }

@@ -95,7 +95,7 @@ extern "C" moe_status moe_unpermute_combine(const void* y, int y_dtype, int64_t 
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int grid = int(std::min<int64_t>((T + 7) / 8, int64_t(sms) * 4));
+  const int grid = sms;  // SM budget: the launcher sizes the grid per kernel
   bool ok = true;
   cudaError_t err = launch_unpermute(a, y_dtype, probs_dtype, out_dtype, grid,
                                      static_cast<cudaStream_t>(stream), &ok);

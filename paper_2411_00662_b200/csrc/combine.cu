@@ -13,6 +13,9 @@
 // One warp per token; each lane owns 16-byte column vectors; fp32
 // accumulation for 16/32-bit inputs, fp64 for f64/i64 (the reference's
 // double arithmetic, without FMA contraction).
+#include <algorithm>
+#include <cstdlib>
+
 #include "copy.cuh"
 
 namespace monta {
@@ -44,82 +47,442 @@ template <> __device__ __forceinline__ __nv_bfloat16 narrow<float, __nv_bfloat16
 }
 template <> __device__ __forceinline__ __half narrow<float, __half>(float v) { return __float2half_rn(v); }
 
-// Tokens [tok_begin, tok_end) by a group of warps: warp (warp0 + w) of
-// `nwarps` takes tokens tok_begin + warp0 + w, strided by nwarps.
-template <class TIn, class TAcc, class TOut, class TProb, int N>
+constexpr int kDeltaSmem = 1024;  // own-node expert deltas staged in shared memory up to this many
+
+// Column vectors per lane per work item.
+template <int N> constexpr int unperm_uv() { return N >= 8 ? 4 : 2; }
+
+// Tokens [tok_begin, tok_end) by a group of warps.  Work item = (token,
+// column batch of 32*UV vectors); warp (warp0 + w) of `nwarps` takes items
+// warp0 + w, strided by nwarps, so the grid balances at sub-token grain.
+// Per-warp pipeline: while item i is computed, the row addresses of item i+1
+// are staged and the index entries (slot, expert, weight) of item i+2 are in
+// flight.  Own-node expert deltas sit in shared memory, so a row address is
+// one dependent load away from its index.
+template <class TIn, class TAcc, class TOut, class TProb, int N, int UV = unperm_uv<N>(), int KC = 0>
 __device__ __forceinline__ void unpermute_tokens(const UnpermArgs& a, int64_t tok_begin, int64_t tok_end,
                                                  int64_t warp0, int64_t nwarps) {
-  // Per-warp staging of the token's k source rows and weights: the column
-  // loop below has a lane-dependent trip count, so no shuffles inside it.
-  __shared__ const char* s_row[kThreads / 32][kMaxK];
-  __shared__ TAcc s_p[kThreads / 32][kMaxK];
+  // Per-warp staging (double-buffered) of an item's k source rows and weights:
+  // the column loop below has a lane-dependent trip count, so no shuffles in it.
+  __shared__ const char* s_row[2][kThreads / 32][kMaxK];
+  __shared__ TAcc s_p[2][kThreads / 32][kMaxK];
+  __shared__ int s_delta[kDeltaSmem];
   const int lane = threadIdx.x & 31;
   const int wib = threadIdx.x >> 5;
-  const int64_t warps = nwarps;
   const TProb* probs = static_cast<const TProb*>(a.probs);
   const int64_t nvec = a.cols / N;
-  for (int64_t i = tok_begin + warp0 + (threadIdx.x >> 5); i < tok_end; i += warps) {
-    if (lane < a.k) {
-      const int64_t q = i * a.k + lane;
-      const int pos = __ldg(a.slot_pos + q);
-      const int x = __ldg(a.experts + q);
-      s_p[wib][lane] = TAcc(__ldg(probs + q));
-      if (pos < 0) {
-        s_row[wib][lane] = nullptr;  // empty slot (negative expert id)
-      } else if (a.local_y && x >= a.local_lo && x < a.local_hi) {
-        s_row[wib][lane] = a.local_y + (int64_t(pos) + __ldg(a.local_delta + x)) * a.y_stride;
-      } else {
-        s_row[wib][lane] = a.comb + int64_t(pos) * a.y_stride;
-      }
+  const int64_t nb = (nvec + 32 * UV - 1) / (32 * UV);
+  const int64_t n_items = (tok_end - tok_begin) * nb;
+  const int nloc = a.local_y ? a.local_hi - a.local_lo : 0;
+  const bool delta_smem = nloc <= kDeltaSmem;
+  if (delta_smem)
+    for (int l = threadIdx.x; l < nloc; l += blockDim.x) s_delta[l] = __ldg(a.local_delta + a.local_lo + l);
+  __syncthreads();
+  int pos = -1, x = -1;
+  TAcc p = TAcc(0);
+  auto load_index = [&](int64_t item) {
+    if (item < n_items && lane < a.k) {
+      const int64_t q = (tok_begin + item / nb) * a.k + lane;
+      pos = __ldg(a.slot_pos + q);
+      x = __ldg(a.experts + q);
+      p = TAcc(__ldg(probs + q));
     }
+  };
+  // rows of `item` from the index registers into staging buffer `buf`
+  auto stage = [&](int buf) {
+    if (lane < a.k) {
+      s_p[buf][wib][lane] = p;
+      const char* row;
+      if (pos < 0) {
+        row = nullptr;  // empty slot (negative expert id)
+      } else if (nloc && x >= a.local_lo && x < a.local_hi) {
+        const int d = delta_smem ? s_delta[x - a.local_lo] : __ldg(a.local_delta + x);
+        row = a.local_y + (int64_t(pos) + d) * a.y_stride;
+      } else {
+        row = a.comb + int64_t(pos) * a.y_stride;
+      }
+      s_row[buf][wib][lane] = row;
+    }
+  };
+  int64_t it = warp0 + wib;
+  int buf = 0;
+  load_index(it);
+  if (it < n_items) stage(0);
+  load_index(it + nwarps);
+  for (; it < n_items; it += nwarps, buf ^= 1) {
     __syncwarp();
-    // UV column vectors per lane per batch; for every slot the UV loads are
-    // independent, and no store intervenes, so k*UV loads are in flight.
-    constexpr int UV = N >= 8 ? 8 : 2;
-    for (int64_t v0 = lane; v0 < nvec; v0 += 32 * UV) {
-      TAcc acc[UV][N];
+    if (it + nwarps < n_items) stage(buf ^ 1);
+    load_index(it + 2 * nwarps);
+    const int64_t i = tok_begin + it / nb;
+    const int64_t v0 = (it % nb) * (32 * UV) + lane;
+    if constexpr (KC > 0) {
+      // k <= KC: every slot's UV loads are issued up front (KC*UV*16 bytes per
+      // lane in flight), then each vector is reduced over the slots and stored
+      // items never straddle the row end here (the launcher checks
+      // nvec % (32*UV) == 0): one base pointer per slot, immediate offsets,
+      // no per-vector predicates
+      const char* rb[KC];
+      TAcc ps[KC];
+      Pack<TIn, N> y[KC][UV];
 #pragma unroll
-      for (int w = 0; w < UV; ++w)
+      for (int g = 0; g < KC; ++g) {
+        const char* r = g < a.k ? s_row[buf][wib][g] : nullptr;
+        ps[g] = g < a.k ? s_p[buf][wib][g] : TAcc(0);
+        rb[g] = r ? r + (a.col_begin + v0 * N) * int64_t(sizeof(TIn)) : nullptr;
+        if (rb[g])
 #pragma unroll
-        for (int u = 0; u < N; ++u) acc[w][u] = TAcc(0);
-      for (int s = 0; s < a.k; ++s) {
-        const TAcc p = s_p[wib][s];
-        const char* row = s_row[wib][s];
-        if (!row) continue;
-        Pack<TIn, N> y[UV];
+          for (int w = 0; w < UV; ++w)
+            y[g][w] = *reinterpret_cast<const Pack<TIn, N>*>(rb[g] + w * 32 * N * int(sizeof(TIn)));
+      }
+      const int64_t obase = i * a.out_stride + (a.col_begin + v0 * N) * int64_t(sizeof(TOut));
+#pragma unroll
+      for (int w = 0; w < UV; ++w) {
+        TAcc acc[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) acc[u] = TAcc(0);
+#pragma unroll
+        for (int g = 0; g < KC; ++g)
+          if (rb[g])
+#pragma unroll
+            for (int u = 0; u < N; ++u) acc[u] = madd<TAcc>(acc[u], ps[g], widen<TIn, TAcc>(y[g][w].v[u]));
+        Pack<TOut, N> o;
+#pragma unroll
+        for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[u]);
+        for (int d = 0; d < a.n_out; ++d)
+          *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + obase + w * 32 * N * int(sizeof(TOut))) = o;
+      }
+    } else {
+    // slots in groups of SG: all SG*UV loads of a group are issued before its
+    // first multiply-add (the slot loop has a runtime trip count, so without
+    // the grouping each slot's loads would wait for the previous slot's math);
+    // accumulation stays in ascending slot order
+    constexpr int SG = 2;
+    TAcc acc[UV][N];
+#pragma unroll
+    for (int w = 0; w < UV; ++w)
+#pragma unroll
+      for (int u = 0; u < N; ++u) acc[w][u] = TAcc(0);
+    for (int s0 = 0; s0 < a.k; s0 += SG) {
+      const char* rows[SG];
+      Pack<TIn, N> y[SG][UV];
+#pragma unroll
+      for (int g = 0; g < SG; ++g) {
+        rows[g] = s0 + g < a.k ? s_row[buf][wib][s0 + g] : nullptr;
 #pragma unroll
         for (int w = 0; w < UV; ++w) {
           const int64_t v = v0 + w * 32;
-          if (v < nvec) y[w] = *reinterpret_cast<const Pack<TIn, N>*>(row + (a.col_begin + v * N) * sizeof(TIn));
+          if (rows[g] && v < nvec)
+            y[g][w] = *reinterpret_cast<const Pack<TIn, N>*>(rows[g] + (a.col_begin + v * N) * sizeof(TIn));
         }
+      }
+#pragma unroll
+      for (int g = 0; g < SG; ++g) {
+        if (!rows[g]) continue;
+        const TAcc ps = s_p[buf][wib][s0 + g];
 #pragma unroll
         for (int w = 0; w < UV; ++w)
 #pragma unroll
-          for (int u = 0; u < N; ++u) acc[w][u] = madd<TAcc>(acc[w][u], p, widen<TIn, TAcc>(y[w].v[u]));
+          for (int u = 0; u < N; ++u) acc[w][u] = madd<TAcc>(acc[w][u], ps, widen<TIn, TAcc>(y[g][w].v[u]));
       }
+    }
 #pragma unroll
-      for (int w = 0; w < UV; ++w) {
-        const int64_t v = v0 + w * 32;
-        if (v >= nvec) continue;
-        const int64_t col = a.col_begin + v * N;
-        Pack<TOut, N> o;
+    for (int w = 0; w < UV; ++w) {
+      const int64_t v = v0 + w * 32;
+      if (v >= nvec) continue;
+      const int64_t col = a.col_begin + v * N;
+      Pack<TOut, N> o;
 #pragma unroll
-        for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[w][u]);
-        for (int d = 0; d < a.n_out; ++d)
-          *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + i * a.out_stride + col * sizeof(TOut)) = o;
-      }
+      for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[w][u]);
+      for (int d = 0; d < a.n_out; ++d)
+        *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + i * a.out_stride + col * sizeof(TOut)) = o;
+    }
     }
     __syncwarp();
   }
 }
 
-template <class TIn, class TAcc, class TOut, class TProb, int N>
-__global__ void __launch_bounds__(kThreads) k_unpermute(const __grid_constant__ UnpermArgs a) {
+// Lean top-1/top-2 un-permute (16-byte vectors, fp32 accumulation): warp per
+// item of (token, 32*UV vectors); both slots' UV loads are in flight at once;
+// row addresses and weights are broadcast by shuffle from lanes 0..k-1 (no
+// staging); 32-bit item arithmetic keeps it within 64 registers, so four
+// CTAs (32 warps) fit per SM — occupancy is what keeps the gather at HBM
+// speed (scripts/micro/gather_bench.cu: 5.7 TB/s at 16 warps/SM, 6.3 TB/s at
+// 32 warps/SM for the same bytes in flight).
+template <class TIn, class TOut, class TProb, int UV, int MinB>
+__global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_constant__ UnpermArgs a) {
+  constexpr int N = 16 / sizeof(TIn);
+  __shared__ int s_delta[kDeltaSmem];
+  if (!cta_wait(a.wait, a.err)) return;
+  const int lane = threadIdx.x & 31;
+  const int nvec = int(a.cols / N);
+  const int nb = nvec / (32 * UV);  // launcher: nvec % (32*UV) == 0
+  const int n_items = int(a.tok_end - a.tok_begin) * nb;
+  const int nloc = a.local_y ? a.local_hi - a.local_lo : 0;
+  const bool delta_smem = nloc <= kDeltaSmem;
+  if (delta_smem)
+    for (int l = threadIdx.x; l < nloc; l += blockDim.x) s_delta[l] = __ldg(a.local_delta + a.local_lo + l);
+  __syncthreads();
+  const TProb* probs = static_cast<const TProb*>(a.probs);
+  const int k = a.k;
+  const int warps = int(gridDim.x) * (kThreads / 32);
+  for (int it = int(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); it < n_items; it += warps) {
+    const int64_t i = a.tok_begin + it / nb;
+    const int cv = (it % nb) * (32 * UV);  // first vector of the item
+    const char* row = nullptr;
+    float p = 0.f;
+    if (lane < k) {
+      const int64_t q = i * k + lane;
+      const int pos = __ldg(a.slot_pos + q);
+      const int x = __ldg(a.experts + q);
+      p = float(__ldg(probs + q));
+      if (pos >= 0) {
+        if (nloc && x >= a.local_lo && x < a.local_hi) {
+          const int d = delta_smem ? s_delta[x - a.local_lo] : __ldg(a.local_delta + x);
+          row = a.local_y + (int64_t(pos) + d) * a.y_stride;
+        } else {
+          row = a.comb + int64_t(pos) * a.y_stride;
+        }
+        row += (a.col_begin + int64_t(cv) * N) * int64_t(sizeof(TIn));  // the item's first vector
+      }
+    }
+    // slot rows (null: empty slot or k == 1) broadcast from lanes 0 and 1
+    const char* r0 = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row), 0));
+    const char* r1 = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row), 1));
+    const float p0 = __shfl_sync(0xffffffffu, p, 0), p1 = __shfl_sync(0xffffffffu, p, 1);
+    if (k < 2) r1 = nullptr;
+    Pack<TIn, N> y0[UV], y1[UV];
+#pragma unroll
+    for (int w = 0; w < UV; ++w) {
+      if (r0) y0[w] = *reinterpret_cast<const Pack<TIn, N>*>(r0 + w * 512 + lane * 16);
+      if (r1) y1[w] = *reinterpret_cast<const Pack<TIn, N>*>(r1 + w * 512 + lane * 16);
+    }
+    const int64_t obase = i * a.out_stride + (a.col_begin + int64_t(cv + lane) * N) * int64_t(sizeof(TOut));
+#pragma unroll
+    for (int w = 0; w < UV; ++w) {
+      float acc[N];
+#pragma unroll
+      for (int u = 0; u < N; ++u) acc[u] = 0.f;
+      if (r0)
+#pragma unroll
+        for (int u = 0; u < N; ++u) acc[u] = madd<float>(acc[u], p0, widen<TIn, float>(y0[w].v[u]));
+      if (r1)
+#pragma unroll
+        for (int u = 0; u < N; ++u) acc[u] = madd<float>(acc[u], p1, widen<TIn, float>(y1[w].v[u]));
+      Pack<TOut, N> o;
+#pragma unroll
+      for (int u = 0; u < N; ++u) o.v[u] = narrow<float, TOut>(acc[u]);
+      for (int d = 0; d < a.n_out; ++d)
+        *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + obase + w * 32 * N * int(sizeof(TOut))) = o;
+    }
+  }
+  cta_signal(a.sig);
+}
+
+// MinB: resident CTAs per SM the register budget must allow (occupancy, not
+// per-warp depth, is what keeps enough gather loads in flight on B200:
+// scripts/micro/gather_bench.cu measured 5.7 TB/s at 16 warps/SM vs 6.3 TB/s
+// at 32 warps/SM for the same bytes in flight).
+template <class TIn, class TAcc, class TOut, class TProb, int N, int UV = unperm_uv<N>(), int KC = 0, int MinB = 2>
+__global__ void __launch_bounds__(kThreads, MinB) k_unpermute(const __grid_constant__ UnpermArgs a) {
   if (!cta_wait(a.wait, a.err)) return;
   const int64_t wpc = blockDim.x / 32;
-  unpermute_tokens<TIn, TAcc, TOut, TProb, N>(a, a.tok_begin, a.tok_end, int64_t(blockIdx.x) * wpc,
-                                              int64_t(gridDim.x) * wpc);
+  unpermute_tokens<TIn, TAcc, TOut, TProb, N, UV, KC>(a, a.tok_begin, a.tok_end, int64_t(blockIdx.x) * wpc,
+                                                      int64_t(gridDim.x) * wpc);
   cta_signal(a.sig);
+}
+
+// ---------------------------------------------------------------------------
+// Bulk-copy un-permute (single-card and per-launch paths): a producer warp
+// streams every item's k source segments into a ring of shared-memory stages
+// with cp.async.bulk (TMA engine, completion counted on an mbarrier); eight
+// consumer warps reduce each stage into the output.  Bytes in flight are
+// bounded by shared memory (S stages x k x seg bytes per CTA), not by
+// registers, which is what kept the register kernel below HBM speed.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+constexpr int kBulkConsumers = 8;                        // consumer warps
+constexpr int kBulkThreads = (kBulkConsumers + 1) * 32;  // + one producer warp
+constexpr int kBulkMaxK = 8;
+constexpr int kBulkStages = 8;
+
+template <class TIn, class TAcc, class TOut, class TProb>
+__global__ void __launch_bounds__(kBulkThreads) k_unpermute_bulk(const __grid_constant__ UnpermArgs a, int seg_bytes,
+                                                                 int stages) {
+  constexpr int N = 16 / sizeof(TIn);  // elements per 16-byte vector
+  extern __shared__ __align__(128) char ring[];  // [stages][k][seg_bytes]
+  __shared__ uint64_t full[kBulkStages], empty[kBulkStages];
+  __shared__ int64_t s_tok[kBulkStages];
+  __shared__ int s_bytes[kBulkStages], s_col[kBulkStages];
+  __shared__ unsigned s_valid[kBulkStages];
+  __shared__ TAcc s_p[kBulkStages][kBulkMaxK];
+  __shared__ int s_delta[kDeltaSmem];
+  if (!cta_wait(a.wait, a.err)) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int k = a.k;
+  const int64_t cols_bytes = a.cols * int64_t(sizeof(TIn));
+  const int nseg = int((cols_bytes + seg_bytes - 1) / seg_bytes);
+  const int64_t n_items = (a.tok_end - a.tok_begin) * nseg;
+  const int nloc = a.local_y ? a.local_hi - a.local_lo : 0;
+  const bool delta_smem = nloc <= kDeltaSmem;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], kBulkConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (delta_smem)
+    for (int l = threadIdx.x; l < nloc; l += blockDim.x) s_delta[l] = __ldg(a.local_delta + a.local_lo + l);
+  __syncthreads();
+  if (warp == kBulkConsumers) {
+    // ---- producer warp: the index entries of B = 32/k items are loaded in
+    // one round trip (lane = item * k + slot), then each item's k bulk copies
+    // are issued as stages free up
+    const TProb* probs = static_cast<const TProb*>(a.probs);
+    const int B = 32 / k;
+    const int mb = lane / k, slot = lane - (lane / k) * k;
+    for (int m0 = 0;; m0 += B) {
+      const int64_t my_it = blockIdx.x + int64_t(m0 + mb) * gridDim.x;
+      const bool live = mb < B && my_it < n_items;
+      if (!__any_sync(0xffffffffu, live)) break;
+      const char* row = nullptr;
+      TAcc pv = TAcc(0);
+      if (live) {
+        const int64_t q = (a.tok_begin + my_it / nseg) * k + slot;
+        const int pos = __ldg(a.slot_pos + q);
+        const int x = __ldg(a.experts + q);
+        pv = TAcc(__ldg(probs + q));
+        if (pos >= 0) {
+          if (nloc && x >= a.local_lo && x < a.local_hi) {
+            const int d = delta_smem ? s_delta[x - a.local_lo] : __ldg(a.local_delta + x);
+            row = a.local_y + (int64_t(pos) + d) * a.y_stride;
+          } else {
+            row = a.comb + int64_t(pos) * a.y_stride;
+          }
+        }
+      }
+      const unsigned valid_all = __ballot_sync(0xffffffffu, row != nullptr);
+      for (int bb = 0; bb < B; ++bb) {
+        const int m = m0 + bb;
+        const int64_t it = blockIdx.x + int64_t(m) * gridDim.x;
+        if (it >= n_items) break;
+        const int st = m % stages;
+        if (m >= stages) mbar_wait(&empty[st], ((m / stages) & 1) ^ 1);
+        const int c = int(it % nseg);
+        const int64_t off = int64_t(c) * seg_bytes;
+        const int bytes = int(cols_bytes - off < seg_bytes ? cols_bytes - off : seg_bytes);
+        const unsigned valid = (valid_all >> (bb * k)) & ((1u << k) - 1u);
+        const bool mine = mb == bb;
+        if (mine) s_p[st][slot] = pv;
+        if (lane == 0) {
+          s_tok[st] = a.tok_begin + it / nseg;
+          s_bytes[st] = bytes;
+          s_col[st] = c;
+          s_valid[st] = valid;
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive_expect_tx(&full[st], unsigned(__popc(valid)) * unsigned(bytes));
+        __syncwarp();
+        if (mine && row)
+          bulk_g2s(ring + (size_t(st) * k + slot) * seg_bytes, row + a.col_begin * int64_t(sizeof(TIn)) + off,
+                   unsigned(bytes), &full[st]);
+      }
+    }
+  } else {
+    // ---- consumer warps: reduce the stage's k segments in slot order
+    int m = 0;
+    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++m) {
+      const int st = m % stages;
+      mbar_wait(&full[st], (m / stages) & 1);
+      const int64_t i = s_tok[st];
+      const int nvec = s_bytes[st] / 16;
+      const unsigned valid = s_valid[st];
+      const int64_t col0 = a.col_begin + int64_t(s_col[st]) * (seg_bytes / int(sizeof(TIn)));
+      for (int v = warp * 32 + lane; v < nvec; v += kBulkConsumers * 32) {
+        TAcc acc[N];
+#pragma unroll
+        for (int u = 0; u < N; ++u) acc[u] = TAcc(0);
+        for (int s = 0; s < k; ++s) {
+          if (!((valid >> s) & 1u)) continue;
+          const TAcc ps = s_p[st][s];
+          const Pack<TIn, N> y =
+              *reinterpret_cast<const Pack<TIn, N>*>(ring + (size_t(st) * k + s) * seg_bytes + size_t(v) * 16);
+#pragma unroll
+          for (int u = 0; u < N; ++u) acc[u] = madd<TAcc>(acc[u], ps, widen<TIn, TAcc>(y.v[u]));
+        }
+        Pack<TOut, N> o;
+#pragma unroll
+        for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[u]);
+        const int64_t col = col0 + int64_t(v) * N;
+        for (int d = 0; d < a.n_out; ++d)
+          *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + i * a.out_stride + col * int64_t(sizeof(TOut))) = o;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[st]);
+    }
+  }
+  cta_signal(a.sig);
+}
+
+// Bulk path eligibility and shape: 16-byte vectors end to end, k <= 8.
+template <class TIn, class TAcc, class TOut, class TProb>
+static bool launch_bulk(const UnpermArgs& a, int grid, cudaStream_t s, cudaError_t* err) {
+  constexpr int N = 16 / sizeof(TIn);
+  if (a.k < 1 || a.k > kBulkMaxK || N * sizeof(TOut) > 16 || 16 % sizeof(TIn) != 0) return false;
+  const int64_t cols_bytes = a.cols * int64_t(sizeof(TIn));
+  uintptr_t in_bits = reinterpret_cast<uintptr_t>(a.comb) | reinterpret_cast<uintptr_t>(a.local_y);
+  uintptr_t out_bits = 0;
+  for (int d = 0; d < a.n_out; ++d) out_bits |= reinterpret_cast<uintptr_t>(a.out[d]);
+  const int64_t ob = int64_t(N) * sizeof(TOut);
+  if (cols_bytes % 16 || (a.col_begin * int64_t(sizeof(TIn))) % 16 || a.y_stride % 16 || in_bits % 16 ||
+      a.out_stride % ob || (a.col_begin * int64_t(sizeof(TOut))) % ob || out_bits % ob)
+    return false;
+  // 4 KiB segments (two per 8 KiB row: finer load balance), as many stages as
+  // fit 64 KiB per CTA (three CTAs per SM)
+  const int seg = int(cols_bytes < 4096 ? cols_bytes : 4096);
+  int stages = int(65536 / (int64_t(a.k) * seg));
+  stages = stages > kBulkStages ? kBulkStages : stages;
+  if (stages < 2) return false;
+  const size_t smem = size_t(stages) * a.k * seg;
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_unpermute_bulk<TIn, TAcc, TOut, TProb>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         96 * 1024);
+    configured = true;
+  }
+  const int64_t items = (a.tok_end - a.tok_begin) * ((cols_bytes + seg - 1) / seg);
+  const int g = int(std::max<int64_t>(1, std::min<int64_t>(grid, items)));
+  k_unpermute_bulk<TIn, TAcc, TOut, TProb><<<g, kBulkThreads, smem, s>>>(a, seg, stages);
+  *err = cudaGetLastError();
+  return true;
 }
 
 __device__ __forceinline__ SegList* comb_list(const CombArgs& a, int j) {
@@ -166,8 +529,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_combine_xchg(const __grid_const
     __syncthreads();
     if (!s_ok) return;
     trace_start(a.trace, 1, a.max_chunks, j);
-    unpermute_tokens<TIn, TAcc, TOut, TProb, N>(a.up, int64_t(j) * ct, int64_t(j + 1) * ct, int64_t(c) * wpc,
-                                                int64_t(ctas) * wpc);
+    // UV 2: the persistent kernel also carries the copy engine within 128 registers
+    unpermute_tokens<TIn, TAcc, TOut, TProb, N, 2>(a.up, int64_t(j) * ct, int64_t(j + 1) * ct, int64_t(c) * wpc,
+                                                   int64_t(ctas) * wpc);
     chunk_done(a.counters + (a.max_chunks + j) * 17, ctas, c, [&] {
       trace_end(a.trace, 1, a.max_chunks, j);
       if (a.dedup)
@@ -238,14 +602,35 @@ static cudaError_t launch_n(const UnpermArgs& a, int grid, cudaStream_t s) {
            (a.col_begin * int64_t(sizeof(TOut))) % ob == 0 && a.y_stride % ib == 0 &&
            a.out_stride % ob == 0 && addr_bits % (ib > ob ? ib : ob) == 0 && ob <= 16;
   };
-  if (N16 >= 8 && fits(8)) {
-    k_unpermute<TIn, TAcc, TOut, TProb, 8><<<grid, kThreads, 0, s>>>(a);
+  if constexpr (sizeof(TIn) <= 4 && sizeof(TAcc) == 4) {
+    cudaError_t err = cudaSuccess;
+    if (a.bulk_grid > 0 && launch_bulk<TIn, TAcc, TOut, TProb>(a, a.bulk_grid * 3, s, &err)) return err;
+  }
+  // grid: at most one item per warp (items = tokens x column batches)
+  // grid: `grid` is the SM budget; resident CTAs per SM of the chosen
+  // kernel, capped at one item per warp (items = tokens x column batches)
+  auto g = [&](int n, int uv, int per_sm = 2) {
+    const int64_t nb = (a.cols / n + 32 * uv - 1) / (32 * uv);
+    const int64_t need = ((a.tok_end - a.tok_begin) * nb + kThreads / 32 - 1) / (kThreads / 32);
+    return int(std::max<int64_t>(1, std::min<int64_t>(int64_t(grid) * per_sm, need)));
+  };
+  if (N16 >= 8 && fits(8) && a.k <= 2 && sizeof(TAcc) == 4 && (a.cols / 8) % (32 * 4) == 0 &&
+      (a.tok_end - a.tok_begin) * (a.cols / 8) < (int64_t(1) << 31)) {
+    // top-1/top-2: lean kernel, both slots' loads in flight
+    static const int variant = [] {
+      const char* v = std::getenv("MONTA_UNPERM_K2");
+      return v ? std::atoi(v) : 0;
+    }();
+    if (variant == 1) k_unpermute_k2<TIn, TOut, TProb, 2, 4><<<g(8, 2, 4), kThreads, 0, s>>>(a);
+    else k_unpermute_k2<TIn, TOut, TProb, 4, 3><<<g(8, 4, 3), kThreads, 0, s>>>(a);
+  } else if (N16 >= 8 && fits(8)) {
+    k_unpermute<TIn, TAcc, TOut, TProb, 8><<<g(8, unperm_uv<8>()), kThreads, 0, s>>>(a);
   } else if (N16 >= 4 && fits(4)) {
-    k_unpermute<TIn, TAcc, TOut, TProb, 4><<<grid, kThreads, 0, s>>>(a);
+    k_unpermute<TIn, TAcc, TOut, TProb, 4><<<g(4, unperm_uv<4>()), kThreads, 0, s>>>(a);
   } else if (N16 >= 2 && fits(2)) {
-    k_unpermute<TIn, TAcc, TOut, TProb, 2><<<grid, kThreads, 0, s>>>(a);
+    k_unpermute<TIn, TAcc, TOut, TProb, 2><<<g(2, unperm_uv<2>()), kThreads, 0, s>>>(a);
   } else {
-    k_unpermute<TIn, TAcc, TOut, TProb, 1><<<grid, kThreads, 0, s>>>(a);
+    k_unpermute<TIn, TAcc, TOut, TProb, 1><<<g(1, unperm_uv<1>()), kThreads, 0, s>>>(a);
   }
   return cudaGetLastError();
 }

@@ -14,6 +14,8 @@
 // phases run in lockstep on the caller's stream — no card ever waits on
 // another card's kernel, so nothing spins.
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -107,6 +109,8 @@ struct moe_ctx {
     void* ho;
     cudaGraphExec_t exec;
     int64_t kernels;  // this context's kernels inside the graph
+    bool timed;       // captured with timing events (spans of the replay)
+    std::vector<std::pair<int, int>> span_labels;  // (stage, chunk) of c->spans[0..)
   };
   std::vector<GraphEntry> graphs;
   bool connected = false;
@@ -164,7 +168,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
   s.epoch = take(8);
   s.front_done = take(16);
-  s.dbg = take(64);
+  s.dbg = take(256);
   const int64_t tiles = (T + front_router_tokens(int(E)) - 1) / front_router_tokens(int(E));
   s.tile_hist = take(size_t(tiles) * E * 4);
   s.tile_base = take(size_t(tiles) * E * 4);
@@ -254,6 +258,14 @@ SegList* list_of(const moe_ctx* c, const Card& cd, int phase, int j) {
 }
 
 // ---- timing -------------------------------------------------------------
+// Timing events are recorded as external event nodes when the stream is being
+// captured, so a replayed graph reports the same per-kernel spans.
+void record_timing(cudaEvent_t ev, cudaStream_t s) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  if (cs == cudaStreamCaptureStatusActive) cudaEventRecordWithFlags(ev, s, cudaEventRecordExternal);
+  else cudaEventRecord(ev, s);
+}
 void span_begin(moe_ctx* c, int stage, int chunk, cudaStream_t s, size_t* slot) {
   *slot = SIZE_MAX;
   if (!c->timing) return;
@@ -266,12 +278,12 @@ void span_begin(moe_ctx* c, int stage, int chunk, cudaStream_t s, size_t* slot) 
   Span& sp = c->spans[c->span_used];
   sp.stage = stage;
   sp.chunk = chunk;
-  cudaEventRecord(sp.a, s);
+  record_timing(sp.a, s);
   *slot = c->span_used++;
 }
 void span_end(moe_ctx* c, size_t slot, cudaStream_t s) {
   if (slot == SIZE_MAX) return;
-  cudaEventRecord(c->spans[slot].b, s);
+  record_timing(c->spans[slot].b, s);
 }
 
 int copy_grid(const moe_ctx* c, bool concurrent, bool aa) {
@@ -602,11 +614,14 @@ moe_status do_front(moe_ctx* c, bool route, int level, int n, int landing, cudaS
       f.dst_tables[f.n_dst++] = c->peer[dst].count_table;
       if (!is_virtual(c) && dst != cd.id) f.sig_flags[f.n_sig++] = flag_at(c, dst, kSigCounts, cd.id);
     }
-    f.do_plan = fused_plan ? 1 : 0;
+    // a lone card with final landing needs no plan: its final layout is the permuted order
+    const bool identity = d.e == 1 && d.t == 1 && landing == MOE_LAND_FINAL && d.top_k <= 16;
+    f.do_plan = fused_plan ? (identity ? 2 : 1) : 0;
     f.plan = make_plan_args(c, cd, level, n, landing);
     f.plan_scratch = cd.scratch;
     f.plan_in_smem = plan_fits_smem(d.e, d.num_experts, n) ? 1 : 0;
     f.dbg = c->debug ? cd.dbg : nullptr;
+    f.plan.dbg = f.dbg;
     size_t sl;
     span_begin(c, route ? MOE_STAGE_ROUTE : MOE_STAGE_INDEX, 0, s, &sl);
     if (moe_status st = launch_front(f, d.logit_dtype, s)) return st;
@@ -693,7 +708,9 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
       for (int x = 0; x < d.e; ++x)
         if (x != cd.node) t.sig.flags[t.sig.n++] = flag_at(c, card_of(c, x, cd.rho), sig_chunk(c, kPsAA, j), cd.id);
     t.err = cd.err;
-    int grid = int(std::min<int64_t>((ct + 7) / 8, int64_t(c->sms) * (concurrent ? 2 : 8)));
+    // four resident CTAs (32 warps) per SM, at most one item (token x 2 KiB piece) per warp
+    const int64_t items = ct * ((c->row_bytes + 2047) / 2048);
+    int grid = int(std::min<int64_t>((items + 7) / 8, int64_t(c->sms) * (concurrent ? 2 : 4)));
     grid = std::max(grid, 1);
     size_t sl;
     span_begin(c, MOE_STAGE_AA, j, s, &sl);
@@ -1013,7 +1030,7 @@ moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t
   c->combine_ready = true;
   if (c->timing && !c->in_forward) {
     c->span_used = 0;
-    cudaEventRecord(c->ev_base, s);
+    record_timing(c->ev_base, s);
   }
   if (moe_status st = do_front(c, route, level, n, landing, s)) return st;
 
@@ -1146,9 +1163,14 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
         if (r != cd.rho) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, cd.node, r), sig_chunk(c, kPsCAG, j), cd.id);
   }
   a.err = cd.err;
-  int grid = c->sms * (concurrent ? 2 : 4);
-  const int64_t need = (ct + 7) / 8;
-  if (need < grid) grid = int(std::max<int64_t>(need, 1));
+  // resident CTAs (2 per SM at 256 threads); the launcher clamps to the item count
+  const int grid = concurrent ? c->sms / 2 : c->sms;  // SM budget (the launcher sizes per kernel)
+  // bulk-copy kernel (64 KiB of stages per CTA, three per SM): opt-in, MONTA_UNPERM=bulk
+  static const bool bulk = [] {
+    const char* v = std::getenv("MONTA_UNPERM");
+    return v && std::string(v) == "bulk";
+  }();
+  a.bulk_grid = bulk ? grid : 0;
   if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;
   size_t sl;
   span_begin(c, MOE_STAGE_UNPERMUTE, j, s, &sl);
@@ -1393,7 +1415,7 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
     }
   if (c->timing) {
     c->span_used = 0;
-    cudaEventRecord(c->ev_base, s);
+    record_timing(c->ev_base, s);
   }
   c->in_forward = true;
   moe_status st = dispatch_impl(c, level, n, landing, s, true);
@@ -1413,8 +1435,16 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
 moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
                          cudaStream_t s) {
   for (auto& g : c->graphs)
-    if (g.level == level && g.n == n && g.landing == landing && g.hx == hx && g.hl == hl && g.ho == ho) {
+    if (g.level == level && g.n == n && g.landing == landing && g.hx == hx && g.hl == hl && g.ho == ho &&
+        g.timed == c->timing) {
       if (!g.exec) return forward_impl(c, level, n, landing, hx, hl, ho, s);
+      if (g.timed) {  // the replay re-records the captured events: restore their labels
+        c->span_used = g.span_labels.size();
+        for (size_t i = 0; i < g.span_labels.size(); ++i) {
+          c->spans[i].stage = g.span_labels[i].first;
+          c->spans[i].chunk = g.span_labels[i].second;
+        }
+      }
       c->last_level = level;
       c->last_n = n;
       c->last_landing = level == MOE_BASELINE ? MOE_LAND_FINAL : landing;
@@ -1424,7 +1454,7 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
       return MOE_OK;
     }
   // capture on the context's own stream (the legacy stream cannot be captured)
-  moe_ctx::GraphEntry e{level, n, landing, hx, hl, ho, nullptr, 0};
+  moe_ctx::GraphEntry e{level, n, landing, hx, hl, ho, nullptr, 0, c->timing, {}};
   const int64_t before = c->launches;
   MONTA_CUDA(cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal));
   moe_status st = forward_impl(c, level, n, landing, hx, hl, ho, c->s_cap);
@@ -1432,6 +1462,8 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
   cudaError_t err = cudaStreamEndCapture(c->s_cap, &graph);
   e.kernels = c->launches - before;
   c->launches = before;
+  if (e.timed)
+    for (size_t i = 0; i < c->span_used; ++i) e.span_labels.emplace_back(c->spans[i].stage, c->spans[i].chunk);
   if (st != MOE_OK) {
     if (graph) cudaGraphDestroy(graph);
     return st;
@@ -1455,7 +1487,7 @@ extern "C" moe_status moe_ctx_forward(moe_ctx* c, int level, int32_t n, int land
   if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
   MONTA_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c->use_graphs && !c->timing) return forward_graph(c, level, n, landing, nullptr, nullptr, nullptr, s);
+  if (c->use_graphs) return forward_graph(c, level, n, landing, nullptr, nullptr, nullptr, s);
   return forward_impl(c, level, n, landing, nullptr, nullptr, nullptr, s);
 }
 
@@ -1466,7 +1498,7 @@ extern "C" moe_status moe_ctx_forward_host(moe_ctx* c, int level, int32_t n, int
   if (moe_status st = validate_dispatch(c, level, n, landing)) return st;
   MONTA_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (c->use_graphs && !c->timing) return forward_graph(c, level, n, landing, host_x, host_logits, host_out, s);
+  if (c->use_graphs) return forward_graph(c, level, n, landing, host_x, host_logits, host_out, s);
   return forward_impl(c, level, n, landing, host_x, host_logits, host_out, s);
 }
 
@@ -1606,15 +1638,15 @@ extern "C" moe_status moe_ctx_xfer(moe_ctx* c, const int64_t* rows_per_card, int
 
 extern "C" int64_t moe_ctx_launch_count(const moe_ctx* c) { return c ? c->launches : 0; }
 
-extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint64_t* out8) {
+extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint64_t* out16) {
   if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: null ctx");
   c->debug = enable != 0;
-  if (!out8) return MOE_OK;
+  if (!out16) return MOE_OK;
   MONTA_CUDA(cudaSetDevice(c->device));
   for (auto& cd : c->local)
     if (cd.id == card) {
       MONTA_CUDA(cudaDeviceSynchronize());
-      MONTA_CUDA(cudaMemcpy(out8, cd.dbg, 64, cudaMemcpyDeviceToHost));
+      MONTA_CUDA(cudaMemcpy(out16, cd.dbg, 128, cudaMemcpyDeviceToHost));
       return MOE_OK;
     }
   return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: card %d is not local", card);

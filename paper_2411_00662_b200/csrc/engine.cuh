@@ -83,6 +83,7 @@ struct UnpermArgs {
   WaitList wait;
   SignalList sig;
   int32_t* err;
+  int32_t bulk_grid;         // > 0: bulk-copy kernel with this many CTAs where eligible
 };
 
 // Launchers (return cudaGetLastError()).
@@ -184,6 +185,7 @@ struct PlanArgs {
   int64_t* recv_rows;          // [1]
   WaitList wait;
   int32_t* err;
+  unsigned long long* dbg;     // optional step timestamps (front kernel debug)
 };
 size_t plan_scratch_ints(int e, int E, int max_chunks);
 bool plan_fits_smem(int e, int E, int n);
@@ -225,7 +227,7 @@ struct FrontArgs {
   int32_t* dst_tables[kMaxCards];
   int32_t n_sig;
   uint64_t* sig_flags[kMaxCards];
-  int32_t do_plan;
+  int32_t do_plan;      // 0: none (separate plan launch), 1: plan_block, 2: identity plan (lone card, final landing)
   PlanArgs plan;        // its wait list is satisfied at the bumped epoch
   int32_t* plan_scratch;
   int32_t plan_in_smem; // plan tables in (reused) dynamic shared memory

@@ -1,21 +1,24 @@
 // Fused dispatch front end: route -> index -> epoch bump -> count exchange
-// -> plan, in ONE cooperative launch (grid = token tiles, co-resident).
+// -> plan, in ONE cooperative launch (co-resident grid: token-tile CTAs plus
+// one control CTA, the last block).
 //
-//   phase 1 (every CTA, per tile): gate the tile's tokens (dataplane::route_topk,
-//            dataplane.hpp:72-106) and histogram its (token, slot) pairs by
-//            expert (order-free shared-memory counts);
-//   barrier  the last CTA to arrive is elected: it scans the tile histograms
-//            into per-tile bases and expert offsets, derives the per-chunk
-//            counts (dataplane.hpp:224-240), bumps the device epoch, stores
-//            this node's counts into every expert-parallel peer's count table
-//            over NVLink, and releases the grid;
-//   phase 2 (every CTA, per tile): stable ranks of the tile's pairs — warps own
-//            32-pair groups, __match_any_sync ranks lanes with equal experts,
-//            a scan over groups orders them — written as the index
-//            (dataplane::permute, dataplane.hpp:118-140).  The order depends
-//            only on (token, slot), never on atomics or scheduling;
-//   plan     the elected CTA waits for its peers' counts and plans
-//            (plan_block, front.cuh).
+//   phase 1 (tile CTAs): gate the tile's tokens (dataplane::route_topk,
+//            dataplane.hpp:72-106) — experts also mirrored in shared memory —
+//            and histogram its (token, slot) pairs by expert;
+//   barrier  every CTA arrives; the last to arrive bumps the device epoch and
+//            releases the grid at once (no scan on the release path);
+//   phase 2 (tile CTAs): each CTA sums the tile histograms itself (L2 reads,
+//            shared-memory atomics) into expert totals and its own tile's
+//            prefix, scans the totals into expert offsets, and ranks its pairs
+//            stably — warps own 32-pair groups, __match_any_sync ranks lanes
+//            with equal experts, a scan over groups orders them — written as
+//            the index (dataplane::permute, dataplane.hpp:118-140).  The order
+//            depends only on (token, slot), never on atomics or scheduling;
+//   control  (last CTA, concurrently): the same sums give expert offsets and
+//            per-chunk counts (dataplane.hpp:224-240); it stores this node's
+//            counts into every expert-parallel peer's count table over NVLink,
+//            raises their flags, waits for theirs and plans (plan_block) from
+//            a shared-memory copy of its arguments prefetched while phase 1 ran.
 #include <algorithm>
 #include <vector>
 
@@ -25,7 +28,6 @@ namespace monta {
 namespace {
 
 constexpr int kFrontSmemMax = 200 * 1024;
-constexpr int kScanSmemInts = 48 * 1024;  // tile histograms scanned in shared memory up to 192 KiB
 
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
   unsigned long long v;
@@ -36,232 +38,342 @@ __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned l
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-template <class T, int G, int PER>
-__global__ void __launch_bounds__(kFrontThreads) k_front(const FrontArgs a) {
-  extern __shared__ int smem[];
-  __shared__ int s_last;
-  __shared__ unsigned long long s_epoch;
-  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
-  const int E = a.E, k = a.k;
-  const int64_t ct = a.T / a.n;
+// Exclusive scan of v[0..n) in shared memory by the whole CTA; v[n] = total.
+// Chunks of 32 per warp, then one warp scans the chunk totals (chunk_tot holds
+// (n + 31) / 32 <= 33 entries: n <= 1056).
+__device__ __forceinline__ void block_exscan(int* v, int n, int* chunk_tot) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nch = (n + 31) / 32;
+  #pragma unroll 1
+  for (int c = wid; c < nch; c += nw) {
+    const int x = c * 32 + lane;
+    int tsum;
+    const int ex = warp_exscan(x < n ? v[x] : 0, lane, &tsum);
+    if (x < n) v[x] = ex;
+    if (lane == 0) chunk_tot[c] = tsum;
+  }
+  __syncthreads();
+  if (wid == 0) {
+    int carry = 0;
+    #pragma unroll 1
+    for (int c0 = 0; c0 < nch; c0 += 32) {
+      const int c = c0 + lane;
+      int tsum;
+      const int ex = warp_exscan(c < nch ? chunk_tot[c] : 0, lane, &tsum);
+      if (c < nch) chunk_tot[c] = carry + ex;
+      carry += tsum;
+    }
+    if (lane == 0) v[n] = carry;
+  }
+  __syncthreads();
+  #pragma unroll 1
+  for (int x = threadIdx.x; x < n; x += blockDim.x) v[x] += chunk_tot[x / 32];
+  __syncthreads();
+}
+
+// Sums of the tile histograms [rows][E] (L2-coherent loads, kB in flight per
+// thread): tot[x] over all rows, pre[x] over rows < b_pre, cnt[j][x] over the
+// rows of chunk j = row / tpc (j < n).  Null targets are skipped; with tot
+// null only rows < b_pre are read.  (row, x) advance incrementally — no
+// integer division in the loop (it dominated the instruction count).
+__device__ __forceinline__ void sum_hists(const int32_t* hist, int rows, int E, int* tot, int* pre, int b_pre,
+                                          int* cnt, int tpc, int n) {
+  constexpr int kB = 8;
+  const int bd = blockDim.x, dq = bd / E, dr = bd - (bd / E) * E;
+  const int N = (tot ? rows : b_pre) * E;
+  const double inv_tpc = 1.0 / double(tpc);
+  int row = threadIdx.x / E, x = threadIdx.x - (threadIdx.x / E) * E;
+  for (int base = threadIdx.x; base < N; base += kB * bd) {
+    int v[kB];
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      const int i = base + u * bd;
+      v[u] = i < N ? __ldcg(hist + i) : 0;
+    }
+#pragma unroll
+    for (int u = 0; u < kB; ++u) {
+      if (v[u]) {
+        if (tot) atomicAdd(tot + x, v[u]);
+        if (pre && row < b_pre) atomicAdd(pre + x, v[u]);
+        if (cnt) {
+          const int j = n == 1 ? (row < tpc ? 0 : 1) : int((double(row) + 0.5) * inv_tpc);
+          if (j < n) atomicAdd(cnt + j * E + x, v[u]);
+        }
+      }
+      row += dq;
+      x += dr;
+      if (x >= E) {
+        x -= E;
+        ++row;
+      }
+    }
+  }
+}
+
+// Shared-memory layout (ints) of one front CTA.
+struct FrontSmem {
+  int exp_ints;   // tile experts mirror [tile_tokens * k] (one tile per CTA), else 0
+  int work_ints;  // phase-dependent work area
+};
+__host__ __device__ inline FrontSmem front_smem_layout(int tile_tokens, int k, int E, int n, bool single,
+                                                       size_t plan_ints) {
+  FrontSmem l;
+  l.exp_ints = single ? tile_tokens * k : 0;
+  const int groups = (tile_tokens * k + 31) / 32;
+  size_t w = size_t(3) * E;                                            // phase 1: h[E] | hc[2][E]
+  const size_t p2 = size_t(2 * E + 1 + 33) + size_t(groups) * E;  // phase 2: offs | pre | ctot | hg
+  const size_t cc = size_t(E + 1 + 33) + size_t(n) * E;              // control: offs | ctot | cnt
+  w = w > p2 ? w : p2;
+  w = w > cc ? w : cc;
+  w = w > plan_ints ? w : plan_ints;
+  l.work_ints = int(w);
+  return l;
+}
+
+// Control CTA after the barrier: expert offsets, chunk counts, count push,
+// plan.
+__device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs& p, int* W,
+                                             unsigned long long epoch) {
+  __shared__ int s_ok;
+  const int tid = threadIdx.x;
+  const int E = a.E, nt = a.n_tiles, n = a.n;
+  const int64_t ct = a.T / n;
+  int* offs = W;            // [E+1]
+  int* ctot = W + E + 1;    // [33]
+  int* cnt = ctot + 33;     // [n][E]
+  #pragma unroll 1
+  for (int i = tid; i < E + 1 + 33 + n * E; i += blockDim.x) W[i] = 0;
+  __syncthreads();
+  const int tpc = ct > 0 ? int(ct / a.tile_tokens) : 0;  // tiles per chunk (aligned)
+  sum_hists(a.tile_hist, nt, E, offs, nullptr, 0, a.aligned && tpc > 0 ? cnt : nullptr, tpc > 0 ? tpc : 1, n);
+  if (!a.aligned)
+    #pragma unroll 1
+    for (int q = tid; q < n * E; q += blockDim.x) {
+      cnt[q] = __ldcg(a.counts_acc + q);
+      a.counts_acc[q] = 0;
+    }
+  __syncthreads();
+  block_exscan(offs, E, ctot);
+  #pragma unroll 1
+  for (int x = tid; x <= E; x += blockDim.x)
+    a.expert_offsets[x] = offs[x];
+  #pragma unroll 1
+  for (int q = tid; q < n * E; q += blockDim.x)
+    a.counts[q] = cnt[q];
+  // count exchange: this node's [n][E] block of every EP peer's table
+  #pragma unroll 1
+  for (int d = 0; d < a.n_dst; ++d) {
+    int32_t* dst = a.dst_tables[d] + int64_t(a.node) * a.max_chunks * E;
+    #pragma unroll 1
+    for (int q = tid; q < n * E; q += blockDim.x)
+      dst[q] = cnt[q];
+  }
+  __syncthreads();
   if (tid == 0) {
-    s_epoch = *a.epoch_dev + 1;  // read before any CTA can arrive: the bump happens after the barrier
+    if (a.n_sig > 0) {
+      __threadfence_system();
+      #pragma unroll 1
+      for (int i = 0; i < a.n_sig; ++i) st_release_sys(a.sig_flags[i], epoch);
+    } else {
+      __threadfence();
+    }
+    if (a.dbg) a.dbg[2] = globaltimer();
+  }
+  if (!a.do_plan) return;
+  if (a.do_plan == 2) {
+    // one card holding every expert, final landing: the final layout IS the
+    // permuted order (every base 0, full rows, nothing crosses a node)
+    for (int x = tid; x < E; x += blockDim.x) {
+      p.local_delta[x] = 0;
+      p.aa_table[x] = 0;
+      p.aa_table[E + x] = 0;
+      p.aa_table[2 * E + x] = 0;
+      p.aa_table[3 * E + x] = int(p.row_bytes);
+    }
+    if (tid == 0) {
+      *p.recv_rows = offs[E];
+      if (a.dbg) a.dbg[3] = a.dbg[6] = globaltimer();
+    }
+    return;
+  }
+  if (tid == 0) {
+    s_ok = 1;
+    const unsigned long long t0 = globaltimer();
+    #pragma unroll 1
+    for (int i = 0; i < p.wait.n && s_ok; ++i)
+      while (ld_acquire_sys(p.wait.flags[i]) < epoch) {
+        if (globaltimer() - t0 > kWaitTimeoutNs) {
+          atomicExch(a.err, (int)MOE_ERR_TIMEOUT);
+          s_ok = 0;
+          break;
+        }
+        __nanosleep(32);
+      }
+    if (a.dbg) a.dbg[3] = globaltimer();
+  }
+  __syncthreads();
+  if (s_ok) plan_block(p, plan_tables(a.plan_in_smem ? W : a.plan_scratch, p.e, p.E, p.n));
+  __syncthreads();
+  if (a.dbg && tid == 0) a.dbg[6] = globaltimer();
+}
+
+template <class T, int G, int PER>
+__global__ void __launch_bounds__(kFrontThreads) k_front(const __grid_constant__ FrontArgs a) {
+  extern __shared__ int smem[];
+  __shared__ unsigned long long s_epoch;
+  __shared__ PlanArgs s_plan;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x >> 5;
+  const int E = a.E, k = a.k, nt = a.n_tiles, n = a.n;
+  const int64_t ct = a.T / n;
+  const int tile_ctas = gridDim.x - 1;
+  const bool control = blockIdx.x == tile_ctas;
+  const bool single = nt <= tile_ctas;  // at most one tile per CTA: experts stay in shared memory
+  const FrontSmem L = front_smem_layout(a.tile_tokens, k, E, n, single, 0);
+  int* s_exp = smem;
+  int* W = smem + L.exp_ints;
+  if (tid == 0) {
+    s_epoch = *a.epoch_dev + 1;  // read before this CTA arrives: the bump happens after every arrival
     if (a.dbg && blockIdx.x == 0) a.dbg[0] = globaltimer();
   }
-  // ---------------- phase 1: route + tile histograms
-  for (int b = blockIdx.x; b < a.n_tiles; b += gridDim.x) {
-    const int64_t i0 = int64_t(b) * a.tile_tokens;
-    const int64_t i1 = i0 + a.tile_tokens < a.T ? i0 + a.tile_tokens : a.T;
-    if (a.route)
-      for (int64_t r0 = i0; r0 < i1; r0 += kFrontThreads / G)
-        route_tokens<T, G, PER>(static_cast<const T*>(a.logits), i1, E, k, a.experts, static_cast<T*>(a.probs),
-                                r0 + tid / G);
-    int* h = smem;                 // [E]
-    int* hc = smem + E;            // [2][E] chunk parts (unaligned only)
-    for (int i = tid; i < 3 * E; i += blockDim.x) smem[i] = 0;
-    __syncthreads();  // routing of this tile visible; histogram zeroed
-    const int64_t np = (i1 - i0) * k;
-    const int64_t j0 = i0 / ct;
-    for (int64_t q = tid; q < np; q += blockDim.x) {
-      const int x = a.experts[i0 * k + q];
-      if (x < 0) continue;  // empty slot
-      if (x >= E) {
-        atomicExch(a.err, (int)MOE_ERR_INVALID_ARGUMENT);
-        continue;
+  // ---------------- phase 1: route + tile histograms (tile CTAs)
+  if (!control) {
+    for (int b = blockIdx.x; b < nt; b += tile_ctas) {
+      const int64_t i0 = int64_t(b) * a.tile_tokens;
+      const int64_t i1 = i0 + a.tile_tokens < a.T ? i0 + a.tile_tokens : a.T;
+      const int np = int((i1 - i0) * k);
+      int* h = W;       // [E]
+      int* hc = W + E;  // [2][E] chunk parts (unaligned only)
+      for (int i = tid; i < 3 * E; i += blockDim.x) W[i] = 0;
+      if (a.route) {
+        for (int64_t r0 = i0; r0 < i1; r0 += kFrontThreads / G)
+          route_tokens<T, G, PER>(static_cast<const T*>(a.logits), i1, E, k, a.experts, static_cast<T*>(a.probs),
+                                  r0 + tid / G, single ? s_exp : nullptr, i0);
+      } else if (single) {
+        for (int q = tid; q < np; q += blockDim.x) s_exp[q] = a.experts[i0 * k + q];
       }
-      atomicAdd(h + x, 1);
-      if (!a.aligned) {
-        const int64_t j = (i0 + q / k) / ct;
-        if (j - j0 < 2) atomicAdd(hc + (j - j0) * E + x, 1);
-        else atomicAdd(a.counts_acc + j * E + x, 1);
+      __syncthreads();  // the tile's experts visible; histogram zeroed
+      const int64_t j0 = i0 / ct;
+      for (int q = tid; q < np; q += blockDim.x) {
+        const int x = single ? s_exp[q] : a.experts[i0 * k + q];
+        if (x < 0) continue;  // empty slot
+        if (x >= E) {
+          atomicExch(a.err, (int)MOE_ERR_INVALID_ARGUMENT);
+          continue;
+        }
+        atomicAdd(h + x, 1);
+        if (!a.aligned) {
+          const int64_t j = (i0 + q / k) / ct;
+          if (j - j0 < 2) atomicAdd(hc + (j - j0) * E + x, 1);
+          else atomicAdd(a.counts_acc + j * E + x, 1);
+        }
       }
+      __syncthreads();
+      for (int x = tid; x < E; x += blockDim.x) {
+        a.tile_hist[int64_t(b) * E + x] = h[x];
+        if (!a.aligned) {
+          if (hc[x]) atomicAdd(a.counts_acc + j0 * E + x, hc[x]);
+          if (hc[E + x]) atomicAdd(a.counts_acc + (j0 + 1) * E + x, hc[E + x]);
+        }
+      }
+      __syncthreads();
     }
-    __syncthreads();
-    for (int x = tid; x < E; x += blockDim.x) {
-      a.tile_hist[int64_t(b) * E + x] = h[x];
-      if (!a.aligned) {
-        if (hc[x]) atomicAdd(a.counts_acc + j0 * E + x, hc[x]);
-        if (hc[E + x]) atomicAdd(a.counts_acc + (j0 + 1) * E + x, hc[E + x]);
-      }
-    }
-    __syncthreads();
+  } else {
+    // control: prefetch the plan arguments (kernel-parameter space) into shared memory
+    const int* src = reinterpret_cast<const int*>(&a.plan);
+    int* dst = reinterpret_cast<int*>(&s_plan);
+    for (int i = tid; i < int(sizeof(PlanArgs) / 4); i += blockDim.x) dst[i] = src[i];
   }
-  // ---------------- grid barrier: the last CTA to arrive is elected
+  // ---------------- grid barrier: every CTA arrives; the last one releases
+  __shared__ int s_last;
   if (tid == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(a.arrive, 1u);
     s_last = prev == gridDim.x - 1;
-  }
-  __syncthreads();
-  if (s_last) {
-    if (tid == 0) {
+    if (s_last) {
       *a.arrive = 0u;
       *a.epoch_dev = s_epoch;
+      __threadfence();
+      st_release_gpu(a.ready, s_epoch);
       if (a.dbg) a.dbg[1] = globaltimer();
-      __threadfence();
     }
-    const int nt = a.n_tiles;
-    const int ld = nt + 1;  // padded row: conflict-free column walks
-    const bool in_smem = int64_t(E) * ld + E + 1 <= int64_t(kScanSmemInts);
-    int* tot = smem;                  // [E+1]
-    int* tbs = smem + E + 1;          // [E][ld] tile-local exclusive prefix (x-major)
-    auto TB = [&](int b, int x) -> int& { return in_smem ? tbs[x * ld + b] : a.tile_base[int64_t(b) * E + x]; };
-    if (in_smem)
-      for (int64_t i = tid; i < int64_t(nt) * E; i += blockDim.x) tbs[(i % E) * ld + i / E] = __ldcg(a.tile_hist + i);
-    __syncthreads();
-    // exclusive scan over tiles, one warp per expert
-    for (int x = wid; x < E; x += nw) {
-      int carry = 0;
-      for (int b0 = 0; b0 < nt; b0 += 32) {
-        const int b = b0 + lane;
-        int tsum;
-        const int v = b < nt ? (in_smem ? TB(b, x) : __ldcg(a.tile_hist + int64_t(b) * E + x)) : 0;
-        const int ex = warp_exscan(v, lane, &tsum);
-        if (b < nt) TB(b, x) = carry + ex;
-        carry += tsum;
-      }
-      if (lane == 0) tot[x] = carry;
-    }
-    __syncthreads();
-    // per-chunk counts: differences of the tile prefixes at chunk starts
-    const int n = a.n;
-    if (a.aligned) {
-      const int tpc = ct > 0 ? int(ct / a.tile_tokens) : 0;  // tiles per chunk
-      for (int q = tid; q < n * E; q += blockDim.x) {
-        const int j = q / E, x = q % E;
-        const int b_lo = j * tpc, b_hi = (j + 1) * tpc;
-        const int lo = b_lo < nt ? TB(b_lo, x) : tot[x];
-        const int hi = b_hi < nt ? TB(b_hi, x) : tot[x];
-        a.counts[q] = hi - lo;
-      }
-    } else {
-      for (int q = tid; q < n * E; q += blockDim.x) {
-        a.counts[q] = __ldcg(a.counts_acc + q);
-        a.counts_acc[q] = 0;
-      }
-    }
-    __syncthreads();
-    if (wid == 0) {  // expert offsets
-      int carry = 0;
-      for (int x0 = 0; x0 < E; x0 += 32) {
-        const int x = x0 + lane;
-        int tsum;
-        const int ex = warp_exscan(x < E ? tot[x] : 0, lane, &tsum);
-        __syncwarp();
-        if (x < E) tot[x] = carry + ex;
-        carry += tsum;
-      }
-      if (lane == 0) tot[E] = carry;
-    }
-    __syncthreads();
-    for (int x = tid; x <= E; x += blockDim.x) a.expert_offsets[x] = tot[x];
-    for (int64_t i = tid; i < int64_t(nt) * E; i += blockDim.x) a.tile_base[i] = TB(int(i / E), int(i % E)) + tot[i % E];
-    __syncthreads();
-    if (tid == 0) {
-      __threadfence();
-      st_release_gpu(a.ready, s_epoch);  // release the grid: tile bases are final
-    }
-    __syncthreads();
-    // count exchange: this node's [n][E] block of every EP peer's table
-    for (int d = 0; d < a.n_dst; ++d) {
-      int32_t* dst = a.dst_tables[d] + int64_t(a.node) * a.max_chunks * E;
-      for (int i = tid; i < n * E; i += blockDim.x) dst[i] = a.counts[i];
-    }
-    __syncthreads();
-    if (tid == 0) {
-      if (a.n_sig > 0) {
-        __threadfence_system();
-        for (int i = 0; i < a.n_sig; ++i) st_release_sys(a.sig_flags[i], s_epoch);
-      }
-      if (a.dbg) a.dbg[2] = globaltimer();
-    }
-  } else if (tid == 0) {
+  }
+  if (tid == 0 && !s_last) {
     const unsigned long long t0 = globaltimer();
     while (ld_acquire_gpu(a.ready) < s_epoch) {
       if (globaltimer() - t0 > kWaitTimeoutNs) {
         atomicExch(a.err, (int)MOE_ERR_TIMEOUT);
         break;
       }
-      __nanosleep(32);
+      __nanosleep(20);
     }
   }
   __syncthreads();
-  // ---------------- plan (elected CTA), overlapping the other CTAs' ranking
-  __shared__ int s_ok;
-  if (s_last && a.do_plan) {
-    if (tid == 0) {
-      s_ok = 1;
-      if (a.dbg) a.dbg[3] = globaltimer();
-      const unsigned long long t0 = globaltimer();
-      for (int i = 0; i < a.plan.wait.n && s_ok; ++i)
-        while (ld_acquire_sys(a.plan.wait.flags[i]) < s_epoch) {
-          if (globaltimer() - t0 > kWaitTimeoutNs) {
-            atomicExch(a.err, (int)MOE_ERR_TIMEOUT);
-            s_ok = 0;
-            break;
+  if (!control) {
+    // ---------------- phase 2: expert totals + own tile prefix, then stable ranks
+    int* offs = W;               // [E+1] totals -> exclusive offsets
+    int* pre = W + E + 1;        // [E] this tile's prefix over earlier tiles
+    int* ctot = pre + E;         // [32+1] scan chunk totals
+    int* hg = ctot + 33;         // [groups][E]
+    bool have_tot = false;
+    for (int b = blockIdx.x; b < nt; b += tile_ctas) {
+      for (int i = tid; i < (have_tot ? E : 2 * E + 1); i += blockDim.x) (have_tot ? pre : W)[i] = 0;
+      __syncthreads();
+      sum_hists(a.tile_hist, nt, E, have_tot ? nullptr : offs, pre, b, nullptr, 1, 0);
+      __syncthreads();
+      if (!have_tot) block_exscan(offs, E, ctot);
+      have_tot = true;
+      const int64_t i0 = int64_t(b) * a.tile_tokens;
+      const int64_t i1 = i0 + a.tile_tokens < a.T ? i0 + a.tile_tokens : a.T;
+      const int np = int((i1 - i0) * k);
+      const int groups = (np + 31) / 32;
+      for (int i = tid; i < groups * E; i += blockDim.x) hg[i] = 0;
+      __syncthreads();
+      for (int g = wid; g < groups; g += nw) {
+        const int q = g * 32 + lane;
+        int x = q < np ? (single ? s_exp[q] : a.experts[i0 * k + q]) : -1;
+        if (x >= E || x < 0) x = -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, x);
+        if (x >= 0 && lane == __ffs(peers) - 1) hg[g * E + x] = __popc(peers);
+      }
+      __syncthreads();
+      for (int x = tid; x < E; x += blockDim.x) {
+        int run = offs[x] + pre[x];
+        for (int g = 0; g < groups; ++g) {
+          const int c = hg[g * E + x];
+          hg[g * E + x] = run;
+          run += c;
+        }
+      }
+      __syncthreads();
+      for (int g = wid; g < groups; g += nw) {
+        const int q = g * 32 + lane;
+        int x = q < np ? (single ? s_exp[q] : a.experts[i0 * k + q]) : -1;
+        if (x >= E || x < 0) x = -1;
+        const unsigned peers = __match_any_sync(0xffffffffu, x);
+        if (q < np) {
+          if (x >= 0) {
+            const int pos = hg[g * E + x] + __popc(peers & lanemask_lt());
+            a.expert_of[pos] = x;
+            a.perm_src[pos] = int32_t(i0 + q / k);
+            a.slot_pos[i0 * k + q] = pos;
+          } else {
+            a.slot_pos[i0 * k + q] = -1;
           }
-          __nanosleep(32);
-        }
-      if (a.dbg) a.dbg[4] = globaltimer();
-    }
-    __syncthreads();
-    if (s_ok) plan_block(a.plan, plan_tables(a.plan_in_smem ? smem : a.plan_scratch, a.plan.e, a.plan.E, a.plan.n));
-    __syncthreads();
-    if (a.dbg && tid == 0) a.dbg[5] = globaltimer();
-  }
-  // ---------------- phase 2: stable ranks of every tile's pairs
-  for (int b = blockIdx.x; b < a.n_tiles; b += gridDim.x) {
-    const int64_t i0 = int64_t(b) * a.tile_tokens;
-    const int64_t i1 = i0 + a.tile_tokens < a.T ? i0 + a.tile_tokens : a.T;
-    const int np = int((i1 - i0) * k);
-    const int groups = (np + 31) / 32;
-    int* hg = smem;  // [groups][E]
-    for (int i = tid; i < groups * E; i += blockDim.x) hg[i] = 0;
-    __syncthreads();
-    for (int g = wid; g < groups; g += nw) {
-      const int q = g * 32 + lane;
-      int x = q < np ? a.experts[i0 * k + q] : -1;
-      if (x >= E || x < 0) x = -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, x);
-      if (x >= 0 && lane == __ffs(peers) - 1) hg[g * E + x] = __popc(peers);
-    }
-    __syncthreads();
-    for (int x = tid; x < E; x += blockDim.x) {
-      int run = __ldcg(a.tile_base + int64_t(b) * E + x);
-      for (int g = 0; g < groups; ++g) {
-        const int c = hg[g * E + x];
-        hg[g * E + x] = run;
-        run += c;
-      }
-    }
-    __syncthreads();
-    for (int g = wid; g < groups; g += nw) {
-      const int q = g * 32 + lane;
-      int x = q < np ? a.experts[i0 * k + q] : -1;
-      if (x >= E || x < 0) x = -1;
-      const unsigned peers = __match_any_sync(0xffffffffu, x);
-      if (q < np) {
-        if (x >= 0) {
-          const int pos = hg[g * E + x] + __popc(peers & lanemask_lt());
-          a.expert_of[pos] = x;
-          a.perm_src[pos] = int32_t(i0 + q / k);
-          a.slot_pos[i0 * k + q] = pos;
-        } else {
-          a.slot_pos[i0 * k + q] = -1;
         }
       }
+      __syncthreads();
     }
-    __syncthreads();
+    if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[7] = globaltimer();
+    return;
   }
+  control_tail(a, s_plan, W, s_epoch);
 }
 
-size_t front_smem_bytes(const FrontArgs* a) {
-  const int groups = (a->tile_tokens * a->k + 31) / 32;
-  size_t ints = std::max<size_t>(size_t(3) * a->E, size_t(groups) * a->E);
-  const size_t scan = size_t(a->E) * (a->n_tiles + 1) + size_t(a->E) + 1;
-  ints = std::max<size_t>(ints, scan <= size_t(kScanSmemInts) ? scan : size_t(a->E) + 1);
-  if (a->do_plan && a->plan_in_smem) ints = std::max(ints, plan_smem_ints(a->plan.e, a->plan.E, a->plan.n));
-  return ints * 4;
+size_t front_smem_bytes(const FrontArgs* a, int tile_ctas) {
+  const bool single = a->n_tiles <= tile_ctas;
+  const size_t plan = a->do_plan && a->plan_in_smem ? plan_smem_ints(a->plan.e, a->plan.E, a->plan.n) : 0;
+  const FrontSmem l = front_smem_layout(a->tile_tokens, a->k, a->E, a->n, single, plan);
+  return (size_t(l.exp_ints) + size_t(l.work_ints)) * 4;
 }
 
 struct CoopInfo {
@@ -277,23 +389,26 @@ moe_status launch_t(const FrontArgs* a, cudaStream_t s, bool configure) {
     MONTA_CUDA(cudaFuncSetAttribute(k_front<T, G, PER>, cudaFuncAttributeMaxDynamicSharedMemorySize, kFrontSmemMax));
     return MOE_OK;
   }
-  const size_t smem = front_smem_bytes(a);
-  if (smem > size_t(kFrontSmemMax)) return fail(MOE_ERR_UNSUPPORTED, "front: too many experts (%d)", a->E);
-  // co-resident grid for the barrier: tiles, capped at the occupancy limit
+  // co-resident grid for the barrier: tile CTAs (capped at the occupancy
+  // limit) plus the control CTA; occupancy is taken at the largest layout
   static std::vector<CoopInfo> cache;
   int dev = 0;
   cudaGetDevice(&dev);
+  const size_t smem_max = front_smem_bytes(a, a->n_tiles);  // the one-tile-per-CTA layout is the larger
+  if (smem_max > size_t(kFrontSmemMax)) return fail(MOE_ERR_UNSUPPORTED, "front: too many experts (%d)", a->E);
   int max_blocks = -1;
   for (const auto& ci : cache)
-    if (ci.fn == (const void*)k_front<T, G, PER> && ci.device == dev && ci.smem == smem) max_blocks = ci.blocks;
+    if (ci.fn == (const void*)k_front<T, G, PER> && ci.device == dev && ci.smem == smem_max) max_blocks = ci.blocks;
   if (max_blocks < 0) {
     int per_sm = 0, sms = 0;
-    MONTA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_front<T, G, PER>, kFrontThreads, smem));
+    MONTA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_front<T, G, PER>, kFrontThreads, smem_max));
     MONTA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-    max_blocks = std::max(1, per_sm * sms);
-    cache.push_back(CoopInfo{(const void*)k_front<T, G, PER>, dev, smem, max_blocks});
+    max_blocks = std::max(2, per_sm * sms);
+    cache.push_back(CoopInfo{(const void*)k_front<T, G, PER>, dev, smem_max, max_blocks});
   }
-  const int grid = std::max(1, std::min(a->n_tiles, max_blocks));
+  const int tile_ctas = std::max(1, std::min(a->n_tiles, max_blocks - 1));
+  const int grid = tile_ctas + 1;
+  const size_t smem = std::min(smem_max, front_smem_bytes(a, tile_ctas));
   void* args[] = {const_cast<FrontArgs*>(a)};
   MONTA_CUDA(cudaLaunchCooperativeKernel((const void*)k_front<T, G, PER>, dim3(grid), dim3(kFrontThreads), args, smem,
                                          s));
@@ -337,8 +452,10 @@ moe_status launch_front(const FrontArgs& a, int logit_dtype, cudaStream_t s) {
   if (a.route)
     if (moe_status st = check_route_args(a.T, a.E, a.k)) return st;
   if (a.tile_tokens % front_router_tokens(a.E) != 0) return fail(MOE_ERR_INVALID_ARGUMENT, "front: bad tile size");
-  if (logit_dtype == MOE_F64) return launch_e<double>(&a, a.E, s, false);
-  return launch_e<float>(&a, a.E, s, false);
+  FrontArgs f = a;
+  if (f.plan_in_smem && front_smem_bytes(&f, f.n_tiles) > size_t(kFrontSmemMax)) f.plan_in_smem = 0;
+  if (logit_dtype == MOE_F64) return launch_e<double>(&f, f.E, s, false);
+  return launch_e<float>(&f, f.E, s, false);
 }
 
 moe_status configure_front(int E, int logit_dtype) {

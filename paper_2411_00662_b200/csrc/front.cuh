@@ -29,7 +29,7 @@ template <> __device__ __forceinline__ double neg_inf<double>() { return -(doubl
 template <class T, int G, int PER>
 __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64_t T_tokens, int E, int k,
                                              int32_t* __restrict__ experts, T* __restrict__ probs,
-                                             int64_t token) {
+                                             int64_t token, int* s_exp = nullptr, int64_t s_base = 0) {
   const int lane = threadIdx.x & (kWarp - 1);
   const int sub = lane % G;
   const bool active = token < T_tokens;
@@ -63,37 +63,83 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
   unsigned taken = 0;
   int my_sel = -1;
   T my_soft = T(0);
-  for (int s = 0; s < k; ++s) {
-    T bv = neg_inf<T>();
-    int bi = int(kNone);
-    T bs = T(0);
+  if constexpr (sizeof(T) == 4) {
+    // fp32 scores: a lane's best candidate is an order-preserving 32-bit key;
+    // the group argmax is one max-reduction (redux.sync for whole warps, a
+    // packed 64-bit {key, ~index} shuffle tree for sub-warp groups) — ties go
+    // to the lower expert index in both
+    for (int s = 0; s < k; ++s) {
+      unsigned key = 0u;  // 0: no candidate (every real score maps above it)
+      unsigned bi = 0xffffffffu;
 #pragma unroll
-    for (int m = 0; m < PER; ++m) {
-      const int x = sub + m * G;
-      if (x < E && !((taken >> m) & 1u)) {
-        if (bi == int(kNone) || v[m] > bv || (v[m] == bv && x < bi)) {
-          bv = v[m];
-          bi = x;
-          bs = ex[m];
+      for (int m = 0; m < PER; ++m) {
+        const int x = sub + m * G;
+        if (x < E && !((taken >> m) & 1u)) {
+          const unsigned b = __float_as_uint(float(v[m]));
+          const unsigned u = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+          if (u > key) {  // x ascends within the lane: strict > keeps the lower index on ties
+            key = u;
+            bi = unsigned(x);
+          }
         }
       }
-    }
+      unsigned wi;
+      if constexpr (G == 32) {
+        const unsigned mk = __reduce_max_sync(0xffffffffu, key);
+        wi = __reduce_min_sync(0xffffffffu, key == mk ? bi : 0xffffffffu);
+      } else {
+        unsigned long long pk = (static_cast<unsigned long long>(key) << 32) | (0xffffffffu - bi);
 #pragma unroll
-    for (int off = G / 2; off > 0; off >>= 1) {
-      const T ov = __shfl_xor_sync(gmask, bv, off, G);
-      const int oi = __shfl_xor_sync(gmask, bi, off, G);
-      const T os = __shfl_xor_sync(gmask, bs, off, G);
-      const bool take = (oi != int(kNone)) && (bi == int(kNone) || ov > bv || (ov == bv && oi < bi));
-      if (take) {
-        bv = ov;
-        bi = oi;
-        bs = os;
+        for (int off = G / 2; off > 0; off >>= 1) {
+          const unsigned long long o = __shfl_xor_sync(gmask, pk, off, G);
+          pk = o > pk ? o : pk;
+        }
+        wi = 0xffffffffu - unsigned(pk & 0xffffffffull);
+      }
+      T mine = T(0);
+#pragma unroll
+      for (int m = 0; m < PER; ++m)
+        if (unsigned(sub + m * G) == wi) mine = ex[m];
+      const T bs = __shfl_sync(gmask, mine, (lane / G) * G + int(wi % G), kWarp);
+      if (int(wi % G) == sub) taken |= 1u << (wi / G);
+      if (sub == s) {
+        my_sel = int(wi);
+        my_soft = bs / sum;
       }
     }
-    if (bi != int(kNone) && (bi % G) == sub) taken |= 1u << (bi / G);
-    if (sub == s) {
-      my_sel = bi;
-      my_soft = bs / sum;
+  } else {
+    for (int s = 0; s < k; ++s) {
+      T bv = neg_inf<T>();
+      int bi = int(kNone);
+      T bs = T(0);
+#pragma unroll
+      for (int m = 0; m < PER; ++m) {
+        const int x = sub + m * G;
+        if (x < E && !((taken >> m) & 1u)) {
+          if (bi == int(kNone) || v[m] > bv || (v[m] == bv && x < bi)) {
+            bv = v[m];
+            bi = x;
+            bs = ex[m];
+          }
+        }
+      }
+#pragma unroll
+      for (int off = G / 2; off > 0; off >>= 1) {
+        const T ov = __shfl_xor_sync(gmask, bv, off, G);
+        const int oi = __shfl_xor_sync(gmask, bi, off, G);
+        const T os = __shfl_xor_sync(gmask, bs, off, G);
+        const bool take = (oi != int(kNone)) && (bi == int(kNone) || ov > bv || (ov == bv && oi < bi));
+        if (take) {
+          bv = ov;
+          bi = oi;
+          bs = os;
+        }
+      }
+      if (bi != int(kNone) && (bi % G) == sub) taken |= 1u << (bi / G);
+      if (sub == s) {
+        my_sel = bi;
+        my_soft = bs / sum;
+      }
     }
   }
   int rank = 0;
@@ -104,6 +150,7 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
   if (active && sub < k) {
     experts[token * k + rank] = my_sel;
     probs[token * k + rank] = my_soft;
+    if (s_exp) s_exp[(token - s_base) * k + rank] = my_sel;  // the tile's mirror in shared memory
   }
 }
 
@@ -298,17 +345,21 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
   const int tid = threadIdx.x, nth = blockDim.x;
   const int lane = tid & 31, wid = tid >> 5, nw = nth >> 5;
   // 1. counts (peers wrote them over NVLink: L2-coherent loads)
+  #pragma unroll 1
   for (int i = tid; i < e * n * E; i += nth) {
     const int g = i / (n * E), r = i % (n * E);
     tb.ct[i] = __ldcg(a.count_table + int64_t(g) * a.max_chunks * E + r);
   }
   __syncthreads();
+  if (a.dbg && tid == 0) a.dbg[8] = globaltimer();
   auto CT = [&](int g, int j, int x) { return tb.ct[(g * n + j) * E + x]; };
   auto CUM = [&](int g, int j, int x) -> int& { return tb.cum[(g * (n + 1) + j) * E + x]; };
   // 2. per-(g, x) chunk prefixes
+  #pragma unroll 1
   for (int q = tid; q < e * E; q += nth) {
     const int g = q / E, x = q % E;
     int run = 0;
+    #pragma unroll 1
     for (int j = 0; j < n; ++j) {
       CUM(g, j, x) = run;
       run += CT(g, j, x);
@@ -316,11 +367,14 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
     CUM(g, n, x) = run;
   }
   __syncthreads();
+  if (a.dbg && tid == 0) a.dbg[9] = globaltimer();
   // 3. eo[g][x]: scan over x of totals; 4. fin[xg][l][g]: scan over (l, g)
+  #pragma unroll 1
   for (int task = wid; task < 2 * e; task += nw) {
     const int g = task % e;
     int carry = 0;
     if (task < e) {
+      #pragma unroll 1
       for (int x0 = 0; x0 < E; x0 += 32) {
         const int x = x0 + lane;
         int tot;
@@ -331,6 +385,7 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
       if (lane == 0) tb.eo[g * (E + 1) + E] = carry;
     } else {
       const int xg = g;
+      #pragma unroll 1
       for (int u0 = 0; u0 < E; u0 += 32) {  // u = l*e + src, L*e == E
         const int u = u0 + lane;
         const int l = u / e, src = u % e;
@@ -343,9 +398,11 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
     }
   }
   // 5. staged bases: within-chunk scan over (g, l) per (xg, j)
+  #pragma unroll 1
   for (int task = wid; task < e * n; task += nw) {
     const int xg = task / n, j = task % n;
     int carry = 0;
+    #pragma unroll 1
     for (int u0 = 0; u0 < E; u0 += 32) {  // u = src*L + l, e*L == E
       const int u = u0 + lane;
       int tot;
@@ -356,8 +413,11 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
     if (lane == 0) tb.cb[xg * (n + 1) + j] = carry;
   }
   __syncthreads();
+  if (a.dbg && tid == 0) a.dbg[10] = globaltimer();
+  #pragma unroll 1
   for (int xg = tid; xg < e; xg += nth) {
     int run = 0;
+    #pragma unroll 1
     for (int j = 0; j < n; ++j) {
       const int c = tb.cb[xg * (n + 1) + j];
       tb.cb[xg * (n + 1) + j] = run;
@@ -366,8 +426,11 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
     tb.cb[xg * (n + 1) + n] = run;
   }
   __syncthreads();
+  if (a.dbg && tid == 0) a.dbg[11] = globaltimer();
+  #pragma unroll 1
   for (int i = tid; i < e * n * E; i += nth) tb.pre[i] += tb.cb[(i / (n * E)) * (n + 1) + (i / E) % n];
   // 6. local permuted->final delta of this node's experts
+  #pragma unroll 1
   for (int l = tid; l < L; l += nth) {
     const int x = a.node * L + l;
     a.local_delta[x] = tb.fin[(a.node * L + l) * e + a.node] - tb.eo[a.node * (E + 1) + x];
@@ -378,6 +441,7 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
   if (a.aa_table) {
     const bool dd = a.level != MOE_BASELINE && t > 1;
     const int g = a.node;
+    #pragma unroll 1
     for (int x = tid; x < E; x += nth) {
       const int xg = x / L, l = x % L;
       const int eo = tb.eo[g * (E + 1) + x];
@@ -386,11 +450,13 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
       a.aa_table[E + x] = tb.fin[(xg * L + l) * e + g] - eo;
       a.aa_table[2 * E + x] = slice ? a.rho * int(a.row_bytes / t) : 0;
       a.aa_table[3 * E + x] = slice ? int(a.row_bytes / t) : int(a.row_bytes);
+      #pragma unroll 1
       for (int j = 0; j < n; ++j)
         a.aa_table[(4 + j) * E + x] = tb.pre[(xg * n + j) * E + g * L + l] - eo - CUM(g, j, x);
     }
   }
   __syncthreads();
+  if (a.dbg && tid == 0) a.dbg[12] = globaltimer();
   // 7. segment lists: one warp per (phase, chunk); candidates u in [0, E)
   const bool dedup = a.level != MOE_BASELINE && t > 1;
   const bool staged = a.landing == MOE_LAND_STAGED;
@@ -399,11 +465,13 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
   const int slice_off = a.rho * slice;
   const int g0 = a.node;
   const int me = g0 * t + a.rho;
+  #pragma unroll 1
   for (int task = wid; task < kNumPhases * n; task += nw) {
     const int phase = task / n, j = task % n;
     SegList* lst = plan_list_at(a, phase, j);
     int pos = 0;
     int64_t rowsum = 0;
+    #pragma unroll 1
     for (int u0 = 0; u0 < E; u0 += 32) {
       const int u = u0 + lane;
       Seg sg;

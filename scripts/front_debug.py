@@ -13,9 +13,10 @@ for (e, t, E, k, T) in [(1, 1, 8, 2, 4096), (1, 1, 160, 6, 8192), (1, 1, 2, 1, 8
     layer.lib.moe_ctx_debug_front(layer._ctx, 1, 0, None)
     for rep in range(3):
         layer.forward(BASELINE, 1)
-        out = (C.c_uint64 * 8)()
+        out = (C.c_uint64 * 16)()
         layer.lib.moe_ctx_debug_front(layer._ctx, 1, 0, out)
-        v = [out[i] for i in range(6)]
-        print(f"{e}x{t} E={E} k={k} T={T}: route+hist {(v[1]-v[0])/1e3:.1f}us  scan+push {(v[2]-v[1])/1e3:.1f}us  "
-              f"wait {(v[4]-v[3])/1e3:.1f}  plan {(v[5]-v[4])/1e3:.1f}us  to-plan-end {(v[5]-v[0])/1e3:.1f}us")
+        v = [out[i] for i in range(16)]
+        r = lambda i: (v[i] - v[0]) / 1e3
+        print(f"{e}x{t} E={E} k={k} T={T}: release {r(1):.1f}  counts+push {r(2):.1f}  plan-wait {r(3):.1f}  "
+              f"plan " + " ".join(f"{r(i):.1f}" for i in range(8, 13)) + f"  plan-end {r(6):.1f}  cta0-rank-end {r(7):.1f} us")
     layer.close()
