@@ -220,6 +220,8 @@ def main():
     ap.add_argument("--landing", default="final", choices=["final", "staged"])
     ap.add_argument("--quick", action="store_true", help="skip naive/e2e/cpu extras (profiling runs)")
     ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--no-persistent", action="store_true",
+                    help="multi-GPU: one launch per (leg, chunk) instead of the persistent exchange kernels")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -272,6 +274,8 @@ def main():
                      device=local, rank=rank if world > 1 else 0, world_size=world)
     layer.connect()
     layer.enable_graphs(not args.no_graphs)
+    if args.no_persistent:
+        layer.set_persistent(False)
     cd = layer.cards[0]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + node)
     x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(torch.bfloat16)

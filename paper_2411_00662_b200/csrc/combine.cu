@@ -512,7 +512,7 @@ __global__ void __launch_bounds__(kThreads, 2) k_combine_xchg(const __grid_const
   for (int s = 0; s <= n; ++s) {
     if (s < n && a.e > 1) {
       trace_start(a.trace, 0, a.max_chunks, s);
-      copy_items<V>(view_of(a.cp), comb_list(a, s), a.cpr, c, ctas);
+      copy_items<V, false, false>(view_of(a.cp), comb_list(a, s), a.cpr, c, ctas);
       chunk_done(a.counters + s * 17, ctas, c, [&] {
         trace_end(a.trace, 0, a.max_chunks, s);
         for (int x = 0; x < a.e; ++x)

@@ -70,18 +70,25 @@ __device__ __forceinline__ CopyView view_of(const CopyArgs& a) {
                   a.dst_stride, a.dst_mask, a.dst, a.dst_tags};
 }
 
-template <int V, bool kCG = false>
+// kStage: stage the segment starts in shared memory (one CTA barrier).  The
+// persistent exchange kernels pass false: a barrier at the start of each
+// chunk would make every warp wait for warp 0's system-scope fence of the
+// previous chunk (chunk_done), which under a saturated NVLink lasts as long
+// as the link queue takes to drain.
+template <int V, bool kCG = false, bool kStage = true>
 __device__ __forceinline__ void copy_items(const CopyView& a, const SegList* L, int64_t cpr, int64_t cta,
                                            int64_t ctas) {
   constexpr int kItemBytes = 32 * V * CopyUnroll<V>::value;
-  __shared__ int64_t sbeg[kSegSmem];
+  __shared__ int64_t sbeg[kStage ? kSegSmem : 1];
   const int nseg = L->nseg;
   cpr = cpr > 0 ? cpr : 1;
   const int64_t total = L->total_rows * cpr;
-  const bool cached = nseg <= kSegSmem;
-  if (cached)
-    for (int i = threadIdx.x; i < nseg; i += blockDim.x) sbeg[i] = L->segs[i].row_begin;
-  __syncthreads();
+  const bool cached = kStage && nseg <= kSegSmem;
+  if (kStage) {
+    if (cached)
+      for (int i = threadIdx.x; i < nseg; i += blockDim.x) sbeg[i] = L->segs[i].row_begin;
+    __syncthreads();
+  }
   const int lane = threadIdx.x & 31;
   const int64_t wpc = blockDim.x / 32;
   for (int64_t item = cta * wpc + (threadIdx.x >> 5); item < total; item += ctas * wpc) {
@@ -166,19 +173,30 @@ __device__ __forceinline__ void trace_end(unsigned long long* tr, int role, int 
   if (tr) tr[(size_t(role) * max_chunks + j) * 2 + 1] = globaltimer();
 }
 
-// The role's CTAs count chunk j done; the last one runs `publish`.  Two
-// levels (kGroups sub-counters, then the root) so ~300 CTAs do not
-// serialise on one L2 atomic: counter[0] = root, counter[1 + g] = group g.
-// Counters are left at zero for the next launch.
+// The role's warps count chunk j done; the last one runs `publish`.
+// Warp-granular, with no CTA barrier: a warp never waits for another warp's
+// stores or fence.  A gpu-scope fence per warp orders its (possibly remote)
+// stores before its count; the last arriver's system-scope fence then covers
+// every counted warp's stores (fence-fence synchronisation at gpu scope plus
+// cumulativity, PTX memory model) before `publish` raises the peers' flags.
+// A system-scope fence per CTA and chunk costs a full NVLink queue drain each
+// (scripts/micro/nvlink_bench.cu, 16 MiB in 16 chunks by 148 CTAs: 131 us
+// with per-CTA system fences, 65 us with gpu-scope ones, 36 us unfenced).
+// Two counter levels (kDoneGroups sub-counters, then the root) so ~1000
+// warps do not serialise on one L2 atomic: counter[0] = root, counter[1 + g]
+// = group g.  Counters are left at zero for the next launch.
 constexpr int kDoneGroups = 16;
 template <class F>
 __device__ __forceinline__ void chunk_done(unsigned int* counter, int role_ctas, int cta, F publish) {
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    __threadfence_system();  // this CTA's (possibly remote) stores before the count
-    const int groups = role_ctas < kDoneGroups ? role_ctas : kDoneGroups;
-    const int g = cta % groups;
-    const unsigned members = unsigned(role_ctas / groups + (g < role_ctas % groups ? 1 : 0));
+  __syncwarp();
+  if ((threadIdx.x & 31) == 0) {
+    const int wpc = int(blockDim.x >> 5);
+    const int warps = role_ctas * wpc;
+    const int w = cta * wpc + int(threadIdx.x >> 5);
+    const int groups = warps < kDoneGroups ? warps : kDoneGroups;
+    const int g = w % groups;
+    const unsigned members = unsigned(warps / groups + (g < warps % groups ? 1 : 0));
+    __threadfence();  // this warp's stores (lanes ordered by __syncwarp) before its count
     const unsigned prev = atomicAdd(counter + 1 + g, 1u);
     if (prev == members - 1) {
       counter[1 + g] = 0u;
@@ -191,6 +209,7 @@ __device__ __forceinline__ void chunk_done(unsigned int* counter, int role_ctas,
       }
     }
   }
+  __syncwarp();
 }
 
 }  // namespace monta

@@ -893,24 +893,27 @@ moe_status launch_dispatch_xchg(moe_ctx* c, Card& cd, int level, int n, int land
   const double row = double(c->row_bytes), rem = (d.e - 1.0) / d.e, loc = 1.0 / d.e;
   const double kNv = 1.0 / 4.0, kHbm = 1.0 / 20.0;
   const bool nv_needed = d.e > 1 || dedup;
-  const double w_nv = (d.e > 1 ? rem * (dedup ? row / d.t : row) * kNv : 0.0) +
-                      (dedup ? (d.t - 1.0) * rem * (row / d.t) * kNv : 0.0) +
-                      (x.d2d_in_ag ? row * 2.0 * kHbm : 0.0);
+  const double w_aa = d.e > 1 ? rem * (dedup ? row / d.t : row) * kNv : 0.0;
+  const double w_ag = (dedup ? (d.t - 1.0) * rem * (row / d.t) * kNv : 0.0) + (x.d2d_in_ag ? row * 2.0 * kHbm : 0.0);
+  // chunked + dedup: the AllGather gets its own CTAs so it overlaps the next
+  // chunks' AllToAll; unchunked, the AA CTAs run both legs back to back
+  const bool split_ag = dedup && n > 1 && d.e > 1;
+  const double w_nv = split_ag ? w_aa : w_aa + w_ag;
   const double w_loc = loc * row * 2.0 * kHbm;
   const double w_d2d = (staged && !x.d2d_in_ag) ? row * 2.0 * kHbm : 0.0;
-  const double wsum = w_nv + w_loc + w_d2d;
+  const double wsum = w_nv + (split_ag ? w_ag : 0.0) + w_loc + w_d2d;
   const int G = max_ctas;
   auto share = [&](double w, bool needed) {
     if (!needed) return 0;
     return std::max(4, int(G * w / wsum + 0.5));
   };
   x.r_aa = share(w_nv, nv_needed);
+  x.r_ag = share(w_ag, split_ag);
   x.r_aal = share(w_loc, true);
-  x.r_ag = 0;
   x.r_d2d = share(w_d2d, staged && !x.d2d_in_ag);
-  while (x.r_aa + x.r_aal + x.r_d2d > max_ctas) {  // trim the largest role
+  while (x.r_aa + x.r_ag + x.r_aal + x.r_d2d > max_ctas) {  // trim the largest role
     int* big = &x.r_aa;
-    for (int* r : {&x.r_aal, &x.r_d2d})
+    for (int* r : {&x.r_ag, &x.r_aal, &x.r_d2d})
       if (*r > *big) big = r;
     if (*big <= 4) return MOE_OK;
     --*big;

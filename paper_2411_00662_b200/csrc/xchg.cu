@@ -3,17 +3,21 @@
 // launch per card.
 //
 // CTA roles (disjoint CTA ranges, all co-resident):
-//   NV   software-pipelined over chunks: step s runs the fused permute +
-//        cross-node AllToAll of chunk s (this rank's 1/t slice under dedup,
-//        straight into the peer's final/staged rows; the last CTA releases
-//        AA[s] at every EP peer), then waits for every remote AA[s-1] and
-//        forwards this rank's slice of those rows to the t-1 TP peers
-//        (AllGather; releases AG[s-1]).  Every NVLink leg gets all NVLink
-//        CTAs.  Under O2 with staged landing the reorder of chunk s-1 follows
-//        (the reference simulator queues the D2D on the AllGather stream,
-//        pipesim.hpp:77-79).
+//   AA   the fused permute + cross-node AllToAll (this rank's 1/t slice under
+//        dedup, straight into the peer's final/staged rows), chunk after
+//        chunk without waiting for anything; the last CTA of chunk s releases
+//        AA[s] at every EP peer;
+//   AG   (chunked runs, r_ag > 0) for each chunk j: wait for every remote
+//        AA[j], forward this rank's slice of those rows to the t-1 TP peers
+//        (AllGather; releases AG[j]); under O2 with staged landing the
+//        reorder of chunk j follows (the reference simulator queues the D2D
+//        on the AllGather stream, pipesim.hpp:77-79).  The AllGather of chunk
+//        j overlaps the AllToAll of chunks > j, which is MoNTA's pipeline.
+//        With one chunk (r_ag == 0) there is nothing to overlap and the AA
+//        CTAs run the AllGather themselves after the AllToAll, so every leg
+//        gets every NVLink CTA;
 //   LOC  own-node rows, full width, local HBM copy; releases a local chunk
-//        flag (read by the reorder).
+//        flag (read by the reorder);
 //   D2D  (O3, staged) for j: wait AA[j] remote, AG[j] from TP peers and the
 //        local chunk flag, then reorder chunk j staged -> final.
 // A chunk therefore costs a flag round trip (~µs), not kernel launches.
@@ -59,62 +63,70 @@ __global__ void __launch_bounds__(kXchgThreads, 2) k_xchg(const __grid_constant_
   const uint64_t epoch = s_epoch;
   const int b = blockIdx.x;
   const int n = a.n;
-  // roles: NV = [0, r_aa) runs AA(j) then AG(j-1); LOC = [r_aa, r_aa + r_aal); D2D after
-  const int loc0 = a.r_aa, d2d0 = a.r_aa + a.r_aal;
+  // roles: AA = [0, r_aa); AG = [r_aa, r_aa + r_ag); LOC; D2D after
+  const int ag0 = a.r_aa, loc0 = a.r_aa + a.r_ag, d2d0 = loc0 + a.r_aal;
+  CopyView g = view_of(a.cp);  // AllGather view: this card's landed rows -> TP peers
+  g.gather = nullptr;
+  g.synth_tags = 0;
+  g.src = a.staged ? a.pre_local : a.recv_local;
+  g.src_tags = a.staged ? a.pre_tags_local : a.recv_tags_local;
+  g.dst_mask = a.ag_mask;
+  g.dst = a.ag_dst;
+  g.dst_tags = a.ag_dst_tags;
+  // AllGather of chunk j by `ctas` CTAs (c = this CTA's index among them)
+  auto gather = [&](int j, int c, int ctas) -> bool {
+    if (threadIdx.x == 0) {
+      s_ok = 1;
+      for (int x = 0; x < a.e && s_ok; ++x)
+        if (x != a.node) s_ok = wait_flag(flag(a, a.me, sig_of(a, kPsAA, j), x * a.t + a.rho), epoch, a.err);
+    }
+    __syncthreads();
+    if (!s_ok) return false;
+    trace_start(a.trace, 2, a.max_chunks, j);
+    copy_items<V, true, false>(g, list_at(a, kPhaseAG, j), a.cpr_slice, c, ctas);
+    chunk_done(a.counters + (2 * a.max_chunks + j) * 17, ctas, c, [&] {
+      trace_end(a.trace, 2, a.max_chunks, j);
+      for (int r = 0; r < a.t; ++r)
+        if (r != a.rho) st_release_sys(flag(a, a.node * a.t + r, sig_of(a, kPsAG, j), a.me), epoch);
+    });
+    if (a.d2d_in_ag) {  // O2 staged: the reorder queued behind the gather
+      if (threadIdx.x == 0) {
+        s_ok = wait_flag(a.local_flags + j, epoch, a.err);
+        for (int r = 0; r < a.t && s_ok; ++r)
+          if (r != a.rho) s_ok = wait_flag(flag(a, a.me, sig_of(a, kPsAG, j), a.node * a.t + r), epoch, a.err);
+      }
+      __syncthreads();
+      if (!s_ok) return false;
+      copy_items<V, true, false>(d2d_view(a), list_at(a, kPhaseD2D, j), a.cpr_full, c, ctas);
+    }
+    return true;
+  };
 
-  if (b < loc0) {  // ---------------- NV: AllToAll of chunk s, then AllGather of chunk s-1
-    const int c = b;
+  if (b < loc0) {  // ---------------- AA and AG roles (one loop, one gather site)
+    const bool is_aa = b < ag0;
+    const int c = is_aa ? b : b - ag0;
+    const int ctas = is_aa ? a.r_aa : a.r_ag;
+    // the AA CTAs gather too when there is no AG role (chunk s-1 after AA(s))
+    const bool do_gather = a.dedup && (is_aa ? a.r_ag == 0 : true);
     const CopyView aa = view_of(a.cp);
-    CopyView g = aa;
-    g.gather = nullptr;
-    g.synth_tags = 0;
-    g.src = a.staged ? a.pre_local : a.recv_local;
-    g.src_tags = a.staged ? a.pre_tags_local : a.recv_tags_local;
-    g.dst_mask = a.ag_mask;
-    g.dst = a.ag_dst;
-    g.dst_tags = a.ag_dst_tags;
     for (int s = 0; s <= n; ++s) {
-      if (s < n && a.e > 1) {
+      if (is_aa && s < n && a.e > 1) {
         trace_start(a.trace, 0, a.max_chunks, s);
-        copy_items<V>(aa, list_at(a, kPhaseAA, s), a.cpr_full, c, a.r_aa);
+        copy_items<V, false, false>(aa, list_at(a, kPhaseAA, s), a.cpr_full, c, a.r_aa);
         chunk_done(a.counters + (0 * a.max_chunks + s) * 17, a.r_aa, c, [&] {
           trace_end(a.trace, 0, a.max_chunks, s);
           for (int x = 0; x < a.e; ++x)
             if (x != a.node) st_release_sys(flag(a, x * a.t + a.rho, sig_of(a, kPsAA, s), a.me), epoch);
         });
       }
-      const int j = s - 1;
-      if (j < 0 || !a.dedup) continue;
-      if (threadIdx.x == 0) {
-        s_ok = 1;
-        for (int x = 0; x < a.e && s_ok; ++x)
-          if (x != a.node) s_ok = wait_flag(flag(a, a.me, sig_of(a, kPsAA, j), x * a.t + a.rho), epoch, a.err);
-      }
-      __syncthreads();
-      if (!s_ok) return;
-      trace_start(a.trace, 2, a.max_chunks, j);
-      copy_items<V, true>(g, list_at(a, kPhaseAG, j), a.cpr_slice, c, a.r_aa);
-      chunk_done(a.counters + (2 * a.max_chunks + j) * 17, a.r_aa, c, [&] {
-        trace_end(a.trace, 2, a.max_chunks, j);
-        for (int r = 0; r < a.t; ++r)
-          if (r != a.rho) st_release_sys(flag(a, a.node * a.t + r, sig_of(a, kPsAG, j), a.me), epoch);
-      });
-      if (a.d2d_in_ag) {  // O2 staged: the reorder queued behind the gather
-        if (threadIdx.x == 0) {
-          s_ok = wait_flag(a.local_flags + j, epoch, a.err);
-          for (int r = 0; r < a.t && s_ok; ++r)
-            if (r != a.rho) s_ok = wait_flag(flag(a, a.me, sig_of(a, kPsAG, j), a.node * a.t + r), epoch, a.err);
-        }
-        __syncthreads();
-        if (!s_ok) return;
-        copy_items<V, true>(d2d_view(a), list_at(a, kPhaseD2D, j), a.cpr_full, c, a.r_aa);
-      }
+      const int j = is_aa ? s - 1 : s;
+      if (do_gather && j >= 0 && j < n && !gather(j, c, ctas)) return;
     }
   } else if (b < d2d0) {  // ---------------- LOC: own-node legs
     const int c = b - loc0;
     for (int j = 0; j < n; ++j) {
       trace_start(a.trace, 1, a.max_chunks, j);
-      copy_items<V>(view_of(a.cp), list_at(a, kPhaseAAL, j), a.cpr_full, c, a.r_aal);
+      copy_items<V, false, false>(view_of(a.cp), list_at(a, kPhaseAAL, j), a.cpr_full, c, a.r_aal);
       chunk_done(a.counters + (1 * a.max_chunks + j) * 17, a.r_aal, c, [&] {
         trace_end(a.trace, 1, a.max_chunks, j);
         st_release_sys(a.local_flags + j, epoch);
@@ -135,7 +147,7 @@ __global__ void __launch_bounds__(kXchgThreads, 2) k_xchg(const __grid_constant_
       __syncthreads();
       if (!s_ok) return;
       trace_start(a.trace, 3, a.max_chunks, j);
-      copy_items<V, true>(d, list_at(a, kPhaseD2D, j), a.cpr_full, c, a.r_d2d);
+      copy_items<V, true, false>(d, list_at(a, kPhaseD2D, j), a.cpr_full, c, a.r_d2d);
       chunk_done(a.counters + (3 * a.max_chunks + j) * 17, a.r_d2d, c, [&] { trace_end(a.trace, 3, a.max_chunks, j); });
     }
   }
@@ -170,7 +182,7 @@ int xchg_max_ctas(int vec) {
 }
 
 cudaError_t launch_xchg(const XchgArgs& a, int vec, cudaStream_t s) {
-  const int grid = a.r_aa + a.r_aal + a.r_d2d;
+  const int grid = a.r_aa + a.r_ag + a.r_aal + a.r_d2d;
   void* args[] = {const_cast<XchgArgs*>(&a)};
   switch (vec) {
     case 16: return cudaLaunchCooperativeKernel((const void*)k_xchg<16>, dim3(grid), dim3(kXchgThreads), args, 0, s);
