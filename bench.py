@@ -450,7 +450,7 @@ def main():
     else:
         ach = kern.get("unpermute_combine", 0.0)
         traffic_alg = unp_bytes
-        dom_name = "unpermute_combine (k_unpermute<bf16,f32,bf16,f32,8>)"
+        dom_name = "unpermute_combine (k_unpermute_k2<bf16,bf16,f32>)"
     ncu_traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:

@@ -59,7 +59,7 @@ template <int N> constexpr int unperm_uv() { return N >= 8 ? 4 : 2; }
 // are staged and the index entries (slot, expert, weight) of item i+2 are in
 // flight.  Own-node expert deltas sit in shared memory, so a row address is
 // one dependent load away from its index.
-template <class TIn, class TAcc, class TOut, class TProb, int N, int UV = unperm_uv<N>(), int KC = 0>
+template <class TIn, class TAcc, class TOut, class TProb, int N, int UV = unperm_uv<N>()>
 __device__ __forceinline__ void unpermute_tokens(const UnpermArgs& a, int64_t tok_begin, int64_t tok_end,
                                                  int64_t warp0, int64_t nwarps) {
   // Per-warp staging (double-buffered) of an item's k source rows and weights:
@@ -115,43 +115,6 @@ __device__ __forceinline__ void unpermute_tokens(const UnpermArgs& a, int64_t to
     load_index(it + 2 * nwarps);
     const int64_t i = tok_begin + it / nb;
     const int64_t v0 = (it % nb) * (32 * UV) + lane;
-    if constexpr (KC > 0) {
-      // k <= KC: every slot's UV loads are issued up front (KC*UV*16 bytes per
-      // lane in flight), then each vector is reduced over the slots and stored
-      // items never straddle the row end here (the launcher checks
-      // nvec % (32*UV) == 0): one base pointer per slot, immediate offsets,
-      // no per-vector predicates
-      const char* rb[KC];
-      TAcc ps[KC];
-      Pack<TIn, N> y[KC][UV];
-#pragma unroll
-      for (int g = 0; g < KC; ++g) {
-        const char* r = g < a.k ? s_row[buf][wib][g] : nullptr;
-        ps[g] = g < a.k ? s_p[buf][wib][g] : TAcc(0);
-        rb[g] = r ? r + (a.col_begin + v0 * N) * int64_t(sizeof(TIn)) : nullptr;
-        if (rb[g])
-#pragma unroll
-          for (int w = 0; w < UV; ++w)
-            y[g][w] = *reinterpret_cast<const Pack<TIn, N>*>(rb[g] + w * 32 * N * int(sizeof(TIn)));
-      }
-      const int64_t obase = i * a.out_stride + (a.col_begin + v0 * N) * int64_t(sizeof(TOut));
-#pragma unroll
-      for (int w = 0; w < UV; ++w) {
-        TAcc acc[N];
-#pragma unroll
-        for (int u = 0; u < N; ++u) acc[u] = TAcc(0);
-#pragma unroll
-        for (int g = 0; g < KC; ++g)
-          if (rb[g])
-#pragma unroll
-            for (int u = 0; u < N; ++u) acc[u] = madd<TAcc>(acc[u], ps[g], widen<TIn, TAcc>(y[g][w].v[u]));
-        Pack<TOut, N> o;
-#pragma unroll
-        for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[u]);
-        for (int d = 0; d < a.n_out; ++d)
-          *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + obase + w * 32 * N * int(sizeof(TOut))) = o;
-      }
-    } else {
     // slots in groups of SG: all SG*UV loads of a group are issued before its
     // first multiply-add (the slot loop has a runtime trip count, so without
     // the grouping each slot's loads would wait for the previous slot's math);
@@ -195,7 +158,6 @@ __device__ __forceinline__ void unpermute_tokens(const UnpermArgs& a, int64_t to
       for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[w][u]);
       for (int d = 0; d < a.n_out; ++d)
         *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + i * a.out_stride + col * sizeof(TOut)) = o;
-    }
     }
     __syncwarp();
   }
@@ -282,207 +244,13 @@ __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_co
 // per-warp depth, is what keeps enough gather loads in flight on B200:
 // scripts/micro/gather_bench.cu measured 5.7 TB/s at 16 warps/SM vs 6.3 TB/s
 // at 32 warps/SM for the same bytes in flight).
-template <class TIn, class TAcc, class TOut, class TProb, int N, int UV = unperm_uv<N>(), int KC = 0, int MinB = 2>
+template <class TIn, class TAcc, class TOut, class TProb, int N, int UV = unperm_uv<N>(), int MinB = 2>
 __global__ void __launch_bounds__(kThreads, MinB) k_unpermute(const __grid_constant__ UnpermArgs a) {
   if (!cta_wait(a.wait, a.err)) return;
   const int64_t wpc = blockDim.x / 32;
-  unpermute_tokens<TIn, TAcc, TOut, TProb, N, UV, KC>(a, a.tok_begin, a.tok_end, int64_t(blockIdx.x) * wpc,
+  unpermute_tokens<TIn, TAcc, TOut, TProb, N, UV>(a, a.tok_begin, a.tok_end, int64_t(blockIdx.x) * wpc,
                                                       int64_t(gridDim.x) * wpc);
   cta_signal(a.sig);
-}
-
-// ---------------------------------------------------------------------------
-// Bulk-copy un-permute (single-card and per-launch paths): a producer warp
-// streams every item's k source segments into a ring of shared-memory stages
-// with cp.async.bulk (TMA engine, completion counted on an mbarrier); eight
-// consumer warps reduce each stage into the output.  Bytes in flight are
-// bounded by shared memory (S stages x k x seg bytes per CTA), not by
-// registers, which is what kept the register kernel below HBM speed.
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred p;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-constexpr int kBulkConsumers = 8;                        // consumer warps
-constexpr int kBulkThreads = (kBulkConsumers + 1) * 32;  // + one producer warp
-constexpr int kBulkMaxK = 8;
-constexpr int kBulkStages = 8;
-
-template <class TIn, class TAcc, class TOut, class TProb>
-__global__ void __launch_bounds__(kBulkThreads) k_unpermute_bulk(const __grid_constant__ UnpermArgs a, int seg_bytes,
-                                                                 int stages) {
-  constexpr int N = 16 / sizeof(TIn);  // elements per 16-byte vector
-  extern __shared__ __align__(128) char ring[];  // [stages][k][seg_bytes]
-  __shared__ uint64_t full[kBulkStages], empty[kBulkStages];
-  __shared__ int64_t s_tok[kBulkStages];
-  __shared__ int s_bytes[kBulkStages], s_col[kBulkStages];
-  __shared__ unsigned s_valid[kBulkStages];
-  __shared__ TAcc s_p[kBulkStages][kBulkMaxK];
-  __shared__ int s_delta[kDeltaSmem];
-  if (!cta_wait(a.wait, a.err)) return;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int k = a.k;
-  const int64_t cols_bytes = a.cols * int64_t(sizeof(TIn));
-  const int nseg = int((cols_bytes + seg_bytes - 1) / seg_bytes);
-  const int64_t n_items = (a.tok_end - a.tok_begin) * nseg;
-  const int nloc = a.local_y ? a.local_hi - a.local_lo : 0;
-  const bool delta_smem = nloc <= kDeltaSmem;
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < stages; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kBulkConsumers);
-    }
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (delta_smem)
-    for (int l = threadIdx.x; l < nloc; l += blockDim.x) s_delta[l] = __ldg(a.local_delta + a.local_lo + l);
-  __syncthreads();
-  if (warp == kBulkConsumers) {
-    // ---- producer warp: the index entries of B = 32/k items are loaded in
-    // one round trip (lane = item * k + slot), then each item's k bulk copies
-    // are issued as stages free up
-    const TProb* probs = static_cast<const TProb*>(a.probs);
-    const int B = 32 / k;
-    const int mb = lane / k, slot = lane - (lane / k) * k;
-    for (int m0 = 0;; m0 += B) {
-      const int64_t my_it = blockIdx.x + int64_t(m0 + mb) * gridDim.x;
-      const bool live = mb < B && my_it < n_items;
-      if (!__any_sync(0xffffffffu, live)) break;
-      const char* row = nullptr;
-      TAcc pv = TAcc(0);
-      if (live) {
-        const int64_t q = (a.tok_begin + my_it / nseg) * k + slot;
-        const int pos = __ldg(a.slot_pos + q);
-        const int x = __ldg(a.experts + q);
-        pv = TAcc(__ldg(probs + q));
-        if (pos >= 0) {
-          if (nloc && x >= a.local_lo && x < a.local_hi) {
-            const int d = delta_smem ? s_delta[x - a.local_lo] : __ldg(a.local_delta + x);
-            row = a.local_y + (int64_t(pos) + d) * a.y_stride;
-          } else {
-            row = a.comb + int64_t(pos) * a.y_stride;
-          }
-        }
-      }
-      const unsigned valid_all = __ballot_sync(0xffffffffu, row != nullptr);
-      for (int bb = 0; bb < B; ++bb) {
-        const int m = m0 + bb;
-        const int64_t it = blockIdx.x + int64_t(m) * gridDim.x;
-        if (it >= n_items) break;
-        const int st = m % stages;
-        if (m >= stages) mbar_wait(&empty[st], ((m / stages) & 1) ^ 1);
-        const int c = int(it % nseg);
-        const int64_t off = int64_t(c) * seg_bytes;
-        const int bytes = int(cols_bytes - off < seg_bytes ? cols_bytes - off : seg_bytes);
-        const unsigned valid = (valid_all >> (bb * k)) & ((1u << k) - 1u);
-        const bool mine = mb == bb;
-        if (mine) s_p[st][slot] = pv;
-        if (lane == 0) {
-          s_tok[st] = a.tok_begin + it / nseg;
-          s_bytes[st] = bytes;
-          s_col[st] = c;
-          s_valid[st] = valid;
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive_expect_tx(&full[st], unsigned(__popc(valid)) * unsigned(bytes));
-        __syncwarp();
-        if (mine && row)
-          bulk_g2s(ring + (size_t(st) * k + slot) * seg_bytes, row + a.col_begin * int64_t(sizeof(TIn)) + off,
-                   unsigned(bytes), &full[st]);
-      }
-    }
-  } else {
-    // ---- consumer warps: reduce the stage's k segments in slot order
-    int m = 0;
-    for (int64_t it = blockIdx.x; it < n_items; it += gridDim.x, ++m) {
-      const int st = m % stages;
-      mbar_wait(&full[st], (m / stages) & 1);
-      const int64_t i = s_tok[st];
-      const int nvec = s_bytes[st] / 16;
-      const unsigned valid = s_valid[st];
-      const int64_t col0 = a.col_begin + int64_t(s_col[st]) * (seg_bytes / int(sizeof(TIn)));
-      for (int v = warp * 32 + lane; v < nvec; v += kBulkConsumers * 32) {
-        TAcc acc[N];
-#pragma unroll
-        for (int u = 0; u < N; ++u) acc[u] = TAcc(0);
-        for (int s = 0; s < k; ++s) {
-          if (!((valid >> s) & 1u)) continue;
-          const TAcc ps = s_p[st][s];
-          const Pack<TIn, N> y =
-              *reinterpret_cast<const Pack<TIn, N>*>(ring + (size_t(st) * k + s) * seg_bytes + size_t(v) * 16);
-#pragma unroll
-          for (int u = 0; u < N; ++u) acc[u] = madd<TAcc>(acc[u], ps, widen<TIn, TAcc>(y.v[u]));
-        }
-        Pack<TOut, N> o;
-#pragma unroll
-        for (int u = 0; u < N; ++u) o.v[u] = narrow<TAcc, TOut>(acc[u]);
-        const int64_t col = col0 + int64_t(v) * N;
-        for (int d = 0; d < a.n_out; ++d)
-          *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + i * a.out_stride + col * int64_t(sizeof(TOut))) = o;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);
-    }
-  }
-  cta_signal(a.sig);
-}
-
-// Bulk path eligibility and shape: 16-byte vectors end to end, k <= 8.
-template <class TIn, class TAcc, class TOut, class TProb>
-static bool launch_bulk(const UnpermArgs& a, int grid, cudaStream_t s, cudaError_t* err) {
-  constexpr int N = 16 / sizeof(TIn);
-  if (a.k < 1 || a.k > kBulkMaxK || N * sizeof(TOut) > 16 || 16 % sizeof(TIn) != 0) return false;
-  const int64_t cols_bytes = a.cols * int64_t(sizeof(TIn));
-  uintptr_t in_bits = reinterpret_cast<uintptr_t>(a.comb) | reinterpret_cast<uintptr_t>(a.local_y);
-  uintptr_t out_bits = 0;
-  for (int d = 0; d < a.n_out; ++d) out_bits |= reinterpret_cast<uintptr_t>(a.out[d]);
-  const int64_t ob = int64_t(N) * sizeof(TOut);
-  if (cols_bytes % 16 || (a.col_begin * int64_t(sizeof(TIn))) % 16 || a.y_stride % 16 || in_bits % 16 ||
-      a.out_stride % ob || (a.col_begin * int64_t(sizeof(TOut))) % ob || out_bits % ob)
-    return false;
-  // 4 KiB segments (two per 8 KiB row: finer load balance), as many stages as
-  // fit 64 KiB per CTA (three CTAs per SM)
-  const int seg = int(cols_bytes < 4096 ? cols_bytes : 4096);
-  int stages = int(65536 / (int64_t(a.k) * seg));
-  stages = stages > kBulkStages ? kBulkStages : stages;
-  if (stages < 2) return false;
-  const size_t smem = size_t(stages) * a.k * seg;
-  static bool configured = false;
-  if (!configured) {
-    cudaFuncSetAttribute(k_unpermute_bulk<TIn, TAcc, TOut, TProb>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         96 * 1024);
-    configured = true;
-  }
-  const int64_t items = (a.tok_end - a.tok_begin) * ((cols_bytes + seg - 1) / seg);
-  const int g = int(std::max<int64_t>(1, std::min<int64_t>(grid, items)));
-  k_unpermute_bulk<TIn, TAcc, TOut, TProb><<<g, kBulkThreads, smem, s>>>(a, seg, stages);
-  *err = cudaGetLastError();
-  return true;
 }
 
 __device__ __forceinline__ SegList* comb_list(const CombArgs& a, int j) {
@@ -602,10 +370,6 @@ static cudaError_t launch_n(const UnpermArgs& a, int grid, cudaStream_t s) {
            (a.col_begin * int64_t(sizeof(TOut))) % ob == 0 && a.y_stride % ib == 0 &&
            a.out_stride % ob == 0 && addr_bits % (ib > ob ? ib : ob) == 0 && ob <= 16;
   };
-  if constexpr (sizeof(TIn) <= 4 && sizeof(TAcc) == 4) {
-    cudaError_t err = cudaSuccess;
-    if (a.bulk_grid > 0 && launch_bulk<TIn, TAcc, TOut, TProb>(a, a.bulk_grid * 3, s, &err)) return err;
-  }
   // grid: at most one item per warp (items = tokens x column batches)
   // grid: `grid` is the SM budget; resident CTAs per SM of the chosen
   // kernel, capped at one item per warp (items = tokens x column batches)
@@ -616,13 +380,9 @@ static cudaError_t launch_n(const UnpermArgs& a, int grid, cudaStream_t s) {
   };
   if (N16 >= 8 && fits(8) && a.k <= 2 && sizeof(TAcc) == 4 && (a.cols / 8) % (32 * 4) == 0 &&
       (a.tok_end - a.tok_begin) * (a.cols / 8) < (int64_t(1) << 31)) {
-    // top-1/top-2: lean kernel, both slots' loads in flight
-    static const int variant = [] {
-      const char* v = std::getenv("MONTA_UNPERM_K2");
-      return v ? std::atoi(v) : 0;
-    }();
-    if (variant == 1) k_unpermute_k2<TIn, TOut, TProb, 2, 4><<<g(8, 2, 4), kThreads, 0, s>>>(a);
-    else k_unpermute_k2<TIn, TOut, TProb, 4, 3><<<g(8, 4, 3), kThreads, 0, s>>>(a);
+    // top-1/top-2: lean kernel, both slots' loads in flight (2 KiB items, 3 CTAs/SM;
+    // 1 KiB items at 4 CTAs/SM measured slower)
+    k_unpermute_k2<TIn, TOut, TProb, 4, 3><<<g(8, 4, 3), kThreads, 0, s>>>(a);
   } else if (N16 >= 8 && fits(8)) {
     k_unpermute<TIn, TAcc, TOut, TProb, 8><<<g(8, unperm_uv<8>()), kThreads, 0, s>>>(a);
   } else if (N16 >= 4 && fits(4)) {

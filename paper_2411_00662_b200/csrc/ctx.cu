@@ -1168,12 +1168,6 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
   a.err = cd.err;
   // resident CTAs (2 per SM at 256 threads); the launcher clamps to the item count
   const int grid = concurrent ? c->sms / 2 : c->sms;  // SM budget (the launcher sizes per kernel)
-  // bulk-copy kernel (64 KiB of stages per CTA, three per SM): opt-in, MONTA_UNPERM=bulk
-  static const bool bulk = [] {
-    const char* v = std::getenv("MONTA_UNPERM");
-    return v && std::string(v) == "bulk";
-  }();
-  a.bulk_grid = bulk ? grid : 0;
   if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;
   size_t sl;
   span_begin(c, MOE_STAGE_UNPERMUTE, j, s, &sl);

@@ -83,7 +83,6 @@ struct UnpermArgs {
   WaitList wait;
   SignalList sig;
   int32_t* err;
-  int32_t bulk_grid;         // > 0: bulk-copy kernel with this many CTAs where eligible
 };
 
 // Launchers (return cudaGetLastError()).
