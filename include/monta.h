@@ -76,6 +76,12 @@ const char* moe_last_error(void);
 int moe_abi_version(void);
 size_t moe_dtype_size(int dtype);
 
+/* Page-locked host buffers for moe_ctx_forward_host (cudaHostAlloc, portable
+ * across contexts), for hosts without another pinned allocator.
+ * Errors: null out pointer -> MOE_ERR_INVALID_ARGUMENT. */
+moe_status moe_host_alloc(size_t bytes, void** ptr);
+moe_status moe_host_free(void* ptr);
+
 /* ------------------------------------------------------------------------
  * 1. Stateless device ops
  * ------------------------------------------------------------------------ */
@@ -256,9 +262,11 @@ moe_status moe_ctx_set_aa_ctas(moe_ctx* ctx, int32_t ctas);
  * copy).  Only local + peer-mapped cards may be named. */
 moe_status moe_ctx_xfer(moe_ctx* ctx, const int64_t* rows_per_card, int32_t row_bytes, int32_t grid,
                         void* stream);
-/* Debug: record phase timestamps of the fused front kernel (enable != 0);
- * with out16 != NULL, synchronise and copy card's 16 globaltimer stamps (ns). */
-moe_status moe_ctx_debug_front(moe_ctx* ctx, int enable, int card, uint64_t* out16);
+/* Debug: record phase timestamps of the fused front kernel and the start /
+ * end of the persistent exchange kernels (enable != 0); with out20 != NULL,
+ * synchronise and copy the card's 20 globaltimer stamps (ns): [0..15] front,
+ * [16..17] dispatch kernel start/end, [18..19] combine kernel start/end. */
+moe_status moe_ctx_debug_front(moe_ctx* ctx, int enable, int card, uint64_t* out20);
 /* Multi-GPU contexts run each phase (dispatch, combine) as ONE persistent,
  * role-specialised cooperative kernel with per-chunk flags (default on);
  * enable = 0 selects one launch per (leg, chunk) on prioritised streams. */

@@ -159,6 +159,8 @@ SIGNATURES = {
     "moe_last_error": (C.c_char_p, []),
     "moe_abi_version": (C.c_int, []),
     "moe_dtype_size": (C.c_size_t, [C.c_int]),
+    "moe_host_alloc": (C.c_int, [C.c_size_t, C.POINTER(C.c_void_p)]),
+    "moe_host_free": (C.c_int, [_P]),
     "moe_route_topk": (C.c_int, [_P, C.c_int, _I64, _I32, _I32, _P, _P, _P]),
     "moe_build_index": (C.c_int, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "moe_permute_rows": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P]),

@@ -31,6 +31,22 @@ extern "C" const char* moe_last_error(void) { return g_last_error.c_str(); }
 extern "C" int moe_abi_version(void) { return MONTA_ABI_VERSION; }
 extern "C" size_t moe_dtype_size(int dtype) { return dtype_size(dtype); }
 
+extern "C" moe_status moe_host_alloc(size_t bytes, void** ptr) {
+  if (!ptr) return fail(MOE_ERR_INVALID_ARGUMENT, "host_alloc: null out pointer");
+  *ptr = nullptr;
+  if (bytes == 0) return MOE_OK;
+  const cudaError_t e = cudaHostAlloc(ptr, bytes, cudaHostAllocPortable);
+  if (e != cudaSuccess) return cuda_fail(e, "host_alloc");
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_host_free(void* ptr) {
+  if (!ptr) return MOE_OK;
+  const cudaError_t e = cudaFreeHost(ptr);
+  if (e != cudaSuccess) return cuda_fail(e, "host_free");
+  return MOE_OK;
+}
+
 extern "C" moe_status moe_route_topk(const void* logits, int logit_dtype, int64_t T, int32_t E, int32_t k,
                                      int32_t* experts, void* probs, void* stream) {
   return route_topk(logits, logit_dtype, T, E, k, experts, probs, static_cast<cudaStream_t>(stream));

@@ -269,7 +269,10 @@ template <class TIn, class TAcc, class TOut, class TProb, int N, int V>
 __global__ void __launch_bounds__(kThreads, 2) k_combine_xchg(const __grid_constant__ CombArgs a) {
   __shared__ int s_ok;
   __shared__ unsigned long long s_epoch;
-  if (threadIdx.x == 0) s_epoch = *a.epoch_ptr;
+  if (threadIdx.x == 0) {
+    s_epoch = *a.epoch_ptr;
+    if (a.dbg && blockIdx.x == 0) a.dbg[0] = globaltimer();
+  }
   __syncthreads();
   const uint64_t epoch = s_epoch;
   const int c = blockIdx.x;
@@ -307,11 +310,14 @@ __global__ void __launch_bounds__(kThreads, 2) k_combine_xchg(const __grid_const
           if (r != a.rho) st_release_sys(comb_flag(a, a.node * a.t + r, kPsCAG, j, a.me), epoch);
     });
   }
-  if (c == 0 && threadIdx.x == 0 && a.dedup) {  // tail: every TP peer's output slice landed here
-    bool ok = true;
-    for (int j = 0; j < n && ok; ++j)
-      for (int r = 0; r < a.t && ok; ++r)
-        if (r != a.rho) ok = wait_flag(comb_flag(a, a.me, kPsCAG, j, a.node * a.t + r), epoch, a.err);
+  if (c == 0 && threadIdx.x == 0) {
+    if (a.dedup) {  // tail: every TP peer's output slice landed here
+      bool ok = true;
+      for (int j = 0; j < n && ok; ++j)
+        for (int r = 0; r < a.t && ok; ++r)
+          if (r != a.rho) ok = wait_flag(comb_flag(a, a.me, kPsCAG, j, a.node * a.t + r), epoch, a.err);
+    }
+    if (a.dbg) a.dbg[1] = globaltimer();
   }
 }
 

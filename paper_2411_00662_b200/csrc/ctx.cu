@@ -963,6 +963,7 @@ moe_status launch_dispatch_xchg(moe_ctx* c, Card& cd, int level, int n, int land
   x.counters = cd.xchg_counters;
   x.local_flags = cd.xchg_flags;
   x.err = cd.err;
+  x.dbg = c->debug ? cd.dbg + 16 : nullptr;
   if (c->timing) {
     x.trace = cd.xtrace;
     MONTA_CUDA(cudaMemsetAsync(cd.xtrace, 0xff, size_t(4) * d.max_chunks * 2 * 8, s));
@@ -1235,6 +1236,7 @@ moe_status launch_combine_persistent(moe_ctx* c, Card& cd, int level, int n, cud
   x.epoch_ptr = cd.epoch_dev;
   x.counters = cd.xchg_counters + 4 * d.max_chunks * 17;
   x.err = cd.err;
+  x.dbg = c->debug ? cd.dbg + 18 : nullptr;
   if (c->timing) {
     x.trace = cd.xtrace + size_t(4) * d.max_chunks * 2;
     MONTA_CUDA(cudaMemsetAsync(x.trace, 0xff, size_t(4) * d.max_chunks * 2 * 8, s));
@@ -1635,15 +1637,15 @@ extern "C" moe_status moe_ctx_xfer(moe_ctx* c, const int64_t* rows_per_card, int
 
 extern "C" int64_t moe_ctx_launch_count(const moe_ctx* c) { return c ? c->launches : 0; }
 
-extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint64_t* out16) {
+extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint64_t* out20) {
   if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: null ctx");
   c->debug = enable != 0;
-  if (!out16) return MOE_OK;
+  if (!out20) return MOE_OK;
   MONTA_CUDA(cudaSetDevice(c->device));
   for (auto& cd : c->local)
     if (cd.id == card) {
       MONTA_CUDA(cudaDeviceSynchronize());
-      MONTA_CUDA(cudaMemcpy(out16, cd.dbg, 128, cudaMemcpyDeviceToHost));
+      MONTA_CUDA(cudaMemcpy(out20, cd.dbg, 160, cudaMemcpyDeviceToHost));
       return MOE_OK;
     }
   return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: card %d is not local", card);

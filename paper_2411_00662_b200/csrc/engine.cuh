@@ -144,6 +144,7 @@ struct XchgArgs {
   unsigned int* counters;       // [4][max_chunks] per-role chunk completion (local, zero)
   uint64_t* local_flags;        // [max_chunks] own-node copy of chunk j finished (epoch)
   unsigned long long* trace;    // optional [4 roles][max_chunks][2] (ns)
+  unsigned long long* dbg;      // optional {kernel start, kernel end} stamps (ns, debug)
   int32_t* err;
 };
 cudaError_t launch_xchg(const XchgArgs& a, int vec, cudaStream_t s);
@@ -164,6 +165,7 @@ struct CombArgs {
   const uint64_t* epoch_ptr;
   unsigned int* counters;  // [2][max_chunks]
   unsigned long long* trace;  // optional [2 roles][max_chunks][2] (ns)
+  unsigned long long* dbg;    // optional {kernel start, kernel end} stamps (ns, debug)
   int32_t* err;
 };
 // Returns cudaErrorNotSupported when no persistent instantiation fits.

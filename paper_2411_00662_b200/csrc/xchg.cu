@@ -58,7 +58,10 @@ template <int V>
 __global__ void __launch_bounds__(kXchgThreads, 2) k_xchg(const __grid_constant__ XchgArgs a) {
   __shared__ int s_ok;
   __shared__ unsigned long long s_epoch;
-  if (threadIdx.x == 0) s_epoch = *a.epoch_ptr;
+  if (threadIdx.x == 0) {
+    s_epoch = *a.epoch_ptr;
+    if (a.dbg && blockIdx.x == 0) a.dbg[0] = globaltimer();
+  }
   __syncthreads();
   const uint64_t epoch = s_epoch;
   const int b = blockIdx.x;
@@ -163,6 +166,7 @@ __global__ void __launch_bounds__(kXchgThreads, 2) k_xchg(const __grid_constant_
           if (x != a.node) ok = wait_flag(flag(a, a.me, sig_of(a, kPsAA, j), x * a.t + a.rho), epoch, a.err);
       }
     }
+    if (a.dbg) a.dbg[1] = globaltimer();
   }
 }
 

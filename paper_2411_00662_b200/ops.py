@@ -4,12 +4,16 @@
     build_index       dataplane::permute, index form (dataplane.hpp:118-140)
     permute_rows      gather-permute of rows (or a hidden_shard column slice)
     unpermute_combine weighted un-permute (dataplane.hpp:325-342)
+    host_empty        page-locked host tensor (moe_host_alloc) for forward_host
 
 All run on the current CUDA stream; nothing here synchronises unless
 `check=True` asks for the device-side validation result.
 """
 from __future__ import annotations
 
+import ctypes as C
+import math
+import weakref
 from dataclasses import dataclass
 
 import torch
@@ -20,6 +24,21 @@ from ._lib import check
 
 def _stream() -> int:
     return torch.cuda.current_stream().cuda_stream
+
+
+def host_empty(shape, dtype: torch.dtype) -> torch.Tensor:
+    """Page-locked host tensor allocated by moe_host_alloc (cudaHostAlloc,
+    portable), for forward_host buffers.  Freed when the last view dies."""
+    lib = _lib.load()
+    shape = tuple(shape) if not isinstance(shape, int) else (shape,)
+    nbytes = math.prod(shape) * torch.empty((), dtype=dtype).element_size()
+    if nbytes == 0:
+        return torch.empty(shape, dtype=dtype)
+    ptr = C.c_void_p()
+    check(lib.moe_host_alloc(nbytes, C.byref(ptr)))
+    buf = (C.c_uint8 * nbytes).from_address(ptr.value)
+    weakref.finalize(buf, lib.moe_host_free, ptr)  # torch.frombuffer keeps `buf` alive with the storage
+    return torch.frombuffer(buf, dtype=torch.uint8).view(dtype).view(shape)
 
 
 def route_topk(logits: torch.Tensor, k: int):

@@ -13,7 +13,7 @@ for (e, t, E, k, T) in [(1, 1, 8, 2, 4096), (1, 1, 160, 6, 8192), (1, 1, 2, 1, 8
     layer.lib.moe_ctx_debug_front(layer._ctx, 1, 0, None)
     for rep in range(3):
         layer.forward(BASELINE, 1)
-        out = (C.c_uint64 * 16)()
+        out = (C.c_uint64 * 20)()
         layer.lib.moe_ctx_debug_front(layer._ctx, 1, 0, out)
         v = [out[i] for i in range(16)]
         r = lambda i: (v[i] - v[0]) / 1e3

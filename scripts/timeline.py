@@ -34,6 +34,7 @@ def main():
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--topk", type=int, default=2)
     ap.add_argument("--no-persistent", action="store_true")
+    ap.add_argument("--timing", action="store_true", help="also record role traces and event spans (adds overhead)")
     a = ap.parse_args()
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -54,21 +55,22 @@ def main():
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     bar = torch.zeros(1, device=f"cuda:{local}")
     layer.lib.moe_ctx_debug_front(layer._ctx, 1, 0, None)
-    layer.enable_timing(True)
+    layer.enable_timing(a.timing)
     for rep in range(4):
         flush.zero_()
         dist.all_reduce(bar)
         torch.cuda.synchronize()
         layer.forward(lv, a.chunks, 0, torch.cuda.current_stream())
         torch.cuda.synchronize()
-    out = (C.c_uint64 * 16)()
+    out = (C.c_uint64 * 20)()
     layer.lib.moe_ctx_debug_front(layer._ctx, 1, layer.local_cards[0], out)
-    front = [out[i] for i in range(16)]
+    front = [out[i] for i in range(20)]
     mc = layer.max_chunks
     cap = 2 * 4 * mc * 2
     arr = (C.c_uint64 * cap)()
     got = C.c_int32()
-    layer.lib.moe_ctx_xchg_trace(layer._ctx, layer.local_cards[0], arr, cap, C.byref(got))
+    if a.timing:
+        layer.lib.moe_ctx_xchg_trace(layer._ctx, layer.local_cards[0], arr, cap, C.byref(got))
     roles = []
     for kern in range(2):
         for role in range(4):
@@ -78,7 +80,7 @@ def main():
                 if x0 == 0xFFFFFFFFFFFFFFFF or x1 == 0xFFFFFFFFFFFFFFFF or not layer.ROLES[kern][role]:
                     continue
                 roles.append((layer.ROLES[kern][role], j, x0, x1))
-    spans = layer.spans()
+    spans = layer.spans() if a.timing else []
     allg = [None] * world
     dist.all_gather_object(allg, (rank, front, roles, spans))
     if rank == 0:
@@ -86,7 +88,9 @@ def main():
             t0 = f[0]
             us = lambda v: (v - t0) / 1e3 if v else float("nan")
             print(f"rank {r}: front start {us(f[0]):7.1f}  release {us(f[1]):7.1f}  counts-pushed {us(f[2]):7.1f}  "
-                  f"peers-counts {us(f[3]):7.1f}  plan-end {us(f[6]):7.1f}  tile-rank-end {us(f[7]):7.1f}")
+                  f"peers-counts {us(f[3]):7.1f}  plan-steps " + " ".join(f"{us(f[i]):.1f}" for i in range(8, 13)) +
+                  f"  plan-end {us(f[6]):7.1f}  tile-rank-end {us(f[7]):7.1f}")
+            print(f"    dispatch kernel {us(f[16]):7.1f} -> {us(f[17]):7.1f}   combine kernel {us(f[18]):7.1f} -> {us(f[19]):7.1f}")
             for name, j, x0, x1 in sorted((z for z in rl if z[2] and z[3]), key=lambda z: z[2]):
                 print(f"    {name:10s} chunk {j:2d}  {us(x0):7.1f} -> {us(x1):7.1f}  ({(x1 - x0) / 1e3:6.1f} us)")
             print("    spans (event clock, from the step's first event):",

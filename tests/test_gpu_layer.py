@@ -14,6 +14,7 @@ import pytest
 import torch
 
 import oracle
+from paper_2411_00662_b200.ops import host_empty
 from paper_2411_00662_b200 import _lib
 from paper_2411_00662_b200.layer import MoeLayer, BASELINE, O1, O2, O3, LAND_FINAL, LAND_STAGED
 
@@ -209,11 +210,14 @@ def test_combine_requires_a_pending_dispatch(cuda):
 
 
 @pytest.mark.parametrize("T,E,k,n", [(8192, 160, 6, 8), (8190, 160, 6, 5), (4096, 8, 2, 1), (8192, 2, 1, 64),
-                                     (3, 4, 2, 3), (0, 8, 2, 1)])
+                                     (3, 4, 2, 3), (0, 8, 2, 1),
+                                     # more tiles than co-resident tile CTAs: CTAs own several tiles
+                                     (19264, 160, 6, 1), (19264, 160, 6, 4), (147904, 8, 2, 1)])
 def test_front_index_matches_oracle_full_size(cuda, T, E, k, n):
-    """The fused front kernel's index (cooperative grid: tile histograms,
-    elected scan, per-tile ranks) equals the oracle's permute at full size,
-    including chunk lengths that do not align with the tiles."""
+    """The fused front kernel's index (cooperative grid: tile histograms, a
+    grid barrier, per-tile prefixes and ranks) equals the oracle's permute at
+    full size, including chunk lengths that do not align with the tiles and
+    grids where a CTA owns several tiles."""
     layer = MoeLayer(1, 1, E, k, T, 64, dtype=torch.bfloat16, max_chunks=max(n, 1))
     try:
         cd = layer.cards[0]
@@ -259,9 +263,12 @@ def test_forward_host_pipelined_single_card_bit_exact(cuda, graphs):
         want = cd.out.clone()
         cd.out.zero_()
         cd.x.zero_()
-        hx = x[0].contiguous().pin_memory()
-        hl = logits[0].contiguous().pin_memory()
-        ho = torch.zeros(T, h, dtype=torch.bfloat16).pin_memory()
+        hx = host_empty((T, h), torch.bfloat16)  # moe_host_alloc buffers (what bench.py uses)
+        hx.copy_(x[0].cpu())
+        hl = host_empty((T, E), torch.float32)
+        hl.copy_(logits[0].cpu())
+        ho = host_empty((T, h), torch.bfloat16)
+        ho.zero_()
         for _ in range(3):
             layer.forward_host(hx, hl, ho, BASELINE, 1)
         torch.cuda.synchronize()
@@ -269,3 +276,20 @@ def test_forward_host_pipelined_single_card_bit_exact(cuda, graphs):
         assert torch.equal(ho.view(torch.int16), want.cpu().view(torch.int16))
     finally:
         layer.close()
+
+
+def test_host_empty_buffers(cuda):
+    """moe_host_alloc tensors: page-locked, writable, freed with their last view."""
+    import gc
+    t = host_empty((1000, 3), torch.float32)
+    assert t.shape == (1000, 3) and t.dtype == torch.float32 and t.is_pinned()
+    t.fill_(2.5)
+    d = t.cuda(non_blocking=True)
+    torch.cuda.synchronize()
+    assert float(d.sum()) == 7500.0
+    v = t[10:20]
+    del t
+    gc.collect()
+    v.fill_(1.0)  # storage still alive through the view
+    assert float(v.sum()) == 30.0
+    assert host_empty((0, 4), torch.bfloat16).numel() == 0
