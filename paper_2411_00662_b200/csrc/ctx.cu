@@ -1303,7 +1303,11 @@ moe_status combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
     MONTA_CUDA(launch_wait(w, cd.err, s));
     c->launches += 2;
   }
-  if (c->use_xchg) {
+  // Unchunked without TP dedup, nothing overlaps the reverse AllToAll and the
+  // un-permute writes only local HBM: a separate launch of the top-k item
+  // kernel (3-4 CTAs per SM) beats the persistent kernel's register-capped
+  // un-permute, so only chunked or deduplicated combines go persistent.
+  if (c->use_xchg && (n > 1 || dedup)) {
     bool done = false;
     if (moe_status st = launch_combine_persistent(c, cd, level, n, s, &done)) return st;
     if (done) return MOE_OK;
