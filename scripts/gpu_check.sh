@@ -12,6 +12,8 @@ case $what in
   ncu1) timeout 300 python bench.py --steps 2 --warmup 3 --quick > gpurun_out/ncu_plain.log 2>&1 && \
         timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu_launches.csv python bench.py --steps 2 --warmup 3 --quick > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?"
         timeout 900 ncu --set full --clock-control none --import-source on -k regex:"k_unpermute|k_aa_token|k_front" -s 3 -c 3 -o gpurun_out/prof_n1 python bench.py --steps 2 --warmup 3 --quick > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?";;
+  ncul) timeout 300 python bench.py --steps 2 --warmup 3 --quick > gpurun_out/ncu_plain.log 2>&1 && \
+        timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/ncu_launches.csv python bench.py --steps 2 --warmup 3 --quick > gpurun_out/ncu_launch.log 2>&1; echo "ncu launches rc=$?";;
   calib4) timeout 400 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29533 -m paper_2411_00662_b200.calibrate --out gpurun_out/calib > gpurun_out/calib4.log 2>&1; echo "calib4 rc=$?";;
   calib8) timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 8 --master-addr 127.0.0.1 --master-port 29534 -m paper_2411_00662_b200.calibrate --out gpurun_out/calib > gpurun_out/calib8.log 2>&1; echo "calib8 rc=$?";;
 esac
