@@ -225,7 +225,7 @@ def load(path: str | os.PathLike | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    p = pathlib.Path(path) if path else LIB_PATH
+    p = pathlib.Path(path or os.environ.get("MONTA_LIB") or LIB_PATH)  # MONTA_LIB: A/B a second build
     if not p.exists():
         try:
             from . import build as _build
