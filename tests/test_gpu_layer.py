@@ -293,3 +293,52 @@ def test_host_empty_buffers(cuda):
     v.fill_(1.0)  # storage still alive through the view
     assert float(v.sum()) == 30.0
     assert host_empty((0, 4), torch.bfloat16).numel() == 0
+
+
+@pytest.mark.parametrize("cfg", [
+    # (e, t, E, k, T, h, level, n, landing) — BASELINE.json configs at full size, emulated cards on one GPU
+    (2, 2, 8, 2, 2048, 1024, O2, 4, LAND_STAGED),    # configs[0] toy layer (run here in bf16)
+    (2, 4, 8, 2, 4096, 4096, O1, 1, LAND_FINAL),     # configs[1] Mixtral layer, 2x4
+    (2, 4, 2, 1, 8192, 8192, O3, 4, LAND_STAGED),    # configs[2] 2x70B-style, E = e
+    (4, 2, 160, 6, 8192, 5120, O2, 2, LAND_FINAL),   # configs[3] DeepSeek-V2-style, 4x2
+])
+def test_full_size_configs_round_trip(cuda, cfg):
+    """Size-independent properties at BASELINE.json's full sizes: every landed row
+    is bit-identical to the source row its tag names, each (source, position,
+    expert) lands exactly once on the node owning the expert, row counts match
+    the routing, and combine(dispatch(x)) with identity experts is x * sum(p)."""
+    e, t, E, k, T, h, level, n, landing = cfg
+    L = E // e
+    layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, max_chunks=max(n, 1))
+    try:
+        g = torch.Generator(device="cuda").manual_seed(E * 7 + h)
+        xs = [torch.randn(T, h, generator=g, device="cuda").to(torch.bfloat16) for _ in range(e)]
+        ls = [torch.randn(T, E, generator=g, device="cuda") for _ in range(e)]
+        for cd in layer.cards:
+            cd.x.copy_(xs[cd.node])
+            cd.logits.copy_(ls[cd.node])
+        layer.forward(level, n, landing)
+        layer.sync()
+        experts = [layer.card(x * t).experts.long() for x in range(e)]
+        probs = [layer.card(x * t).probs.double() for x in range(e)]
+        for cd in layer.cards:
+            rows = layer.recv_rows(cd.card)
+            want_rows = sum(int(((ex // L) == cd.node).sum()) for ex in experts)
+            assert rows == want_rows, (cd.card, rows, want_rows)
+            tags = cd.recv_tags[:rows].long()
+            src_node = tags[:, 1] // t
+            pos, xpt = tags[:, 2], tags[:, 3]
+            assert bool(((xpt // L) == cd.node).all()), "a row landed on a node that does not own its expert"
+            key = (src_node * T + pos) * E + xpt
+            assert key.unique().numel() == rows, "a (source, position, expert) landed twice"
+            for x in range(e):
+                sel = src_node == x
+                if not bool(sel.any()):
+                    continue
+                assert torch.equal(cd.recv[:rows][sel].view(torch.int16), xs[x][pos[sel]].view(torch.int16))
+                assert bool((experts[x][pos[sel]] == xpt[sel][:, None]).any(1).all()), "tag expert not routed"
+            want = xs[cd.node].double() * probs[cd.node].sum(1, keepdim=True)
+            err = ((cd.out.double() - want).abs().max() / want.abs().max()).item()
+            assert err <= 1e-2, (cd.card, err)
+    finally:
+        layer.close()
