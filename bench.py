@@ -396,6 +396,23 @@ def main():
             rs = [role_stats(tr)[0] for tr in ntr]
             naive["roles_busy_us"] = {r: statistics.mean(x.get(r, 0.0) for x in rs) for r in set().union(*rs)}
 
+    # ---- robustness: Zipf-skewed routing, same shapes
+    skewed = None
+    if not args.quick:
+        zipf = torch.log(1.0 / torch.arange(1, E + 1, device=f"cuda:{local}", dtype=torch.float32) ** 1.2)
+        cd.logits.copy_(l0 + 2.0 * zipf[None, :])
+        for _ in range(3):
+            step()
+        layer.sync()
+        stot, _ = timed(step, args.steps)
+        loads = torch.bincount(cd.experts.flatten().long(), minlength=E).float()
+        skewed = {"us_per_layer": stot * 1e3 / args.steps, "routing": "logits + 2*log(rank^-1.2) (Zipf s=1.2)",
+                  "max_over_mean_expert_load": float(loads.max() / loads.mean())}
+        cd.logits.copy_(l0)
+        for _ in range(2):
+            step()
+        layer.sync()
+
     # ---- e2e through the C ABI with host buffers
     e2e = None
     if not args.quick:
@@ -486,6 +503,7 @@ def main():
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "stages": stages, "roles_busy_us": roles, "exposed_alltoall_us": exp_aa,
             "naive": naive,
+            "skewed": skewed,
             "nvlink": nvlink, "check_max_rel_err": err}
     if rank == 0:
         print(json.dumps(line), flush=True)
