@@ -38,7 +38,7 @@ struct PeerPtrs {
   int32_t* pre_tags = nullptr;
   char* comb = nullptr;
   char* out = nullptr;
-  int32_t* count_table = nullptr;
+  uint64_t* count_table = nullptr;  // [e][max_chunks][E] of {count | epoch << 32}
   uint64_t* flags = nullptr;
 };
 
@@ -55,7 +55,7 @@ struct Card {
   int id = 0, node = 0, rho = 0;
   char* slab = nullptr;
   moe_card_view v{};
-  int32_t* count_table = nullptr;
+  uint64_t* count_table = nullptr;
   uint64_t* flags = nullptr;
   int32_t* err = nullptr;
   unsigned* done = nullptr;
@@ -158,7 +158,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.pre_tags = take(size_t(c->recv_cap) * 16);
   s.comb = take(size_t(c->R) * c->row_bytes);
   s.out = take(size_t(T) * h * c->ob);
-  s.count_table = take(size_t(d.e) * d.max_chunks * E * 4);
+  s.count_table = take(size_t(d.e) * d.max_chunks * E * 8);
   s.flags = take(size_t(c->n_flag_sigs) * kMaxCards * 8);
   s.err = take(16);
   s.done = take(size_t(kNumPhaseSignals * d.max_chunks + 8) * 4);
@@ -207,7 +207,7 @@ void bind_card(moe_ctx* c, Card& cd) {
   v.out = b + s.out;
   v.rows_permuted = c->R;
   v.recv_cap = c->recv_cap;
-  cd.count_table = reinterpret_cast<int32_t*>(b + s.count_table);
+  cd.count_table = reinterpret_cast<uint64_t*>(b + s.count_table);
   cd.flags = reinterpret_cast<uint64_t*>(b + s.flags);
   cd.err = reinterpret_cast<int32_t*>(b + s.err);
   cd.done = reinterpret_cast<unsigned*>(b + s.done);
@@ -239,7 +239,7 @@ void set_peer(moe_ctx* c, int card, char* slab) {
   p.pre_tags = reinterpret_cast<int32_t*>(slab + s.pre_tags);
   p.comb = slab + s.comb;
   p.out = slab + s.out;
-  p.count_table = reinterpret_cast<int32_t*>(slab + s.count_table);
+  p.count_table = reinterpret_cast<uint64_t*>(slab + s.count_table);
   p.flags = reinterpret_cast<uint64_t*>(slab + s.flags);
 }
 
@@ -564,11 +564,9 @@ PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
   a.err = cd.err;
   a.wait = no_wait();
   a.wait.epoch_ptr = cd.epoch_dev;
-  if (!is_virtual(c))
-    for (int x = 0; x < d.e; ++x) {
-      const int src = card_of(c, x, cd.rho);
-      if (src != cd.id) a.wait.flags[a.wait.n++] = flag_at(c, cd.id, kSigCounts, src);
-    }
+  // multi-GPU: the peers' count blocks are self-validating {count | epoch}
+  // words, polled by the plan — no flag and no system fence on that path
+  a.poll_peers = !is_virtual(c) && d.e > 1 ? 1 : 0;
   return a;
 }
 
@@ -612,7 +610,6 @@ moe_status do_front(moe_ctx* c, bool route, int level, int n, int landing, cudaS
     for (int x = 0; x < d.e; ++x) {
       const int dst = card_of(c, x, cd.rho);
       f.dst_tables[f.n_dst++] = c->peer[dst].count_table;
-      if (!is_virtual(c) && dst != cd.id) f.sig_flags[f.n_sig++] = flag_at(c, dst, kSigCounts, cd.id);
     }
     // a lone card with final landing needs no plan: its final layout is the permuted order
     const bool identity = d.e == 1 && d.t == 1 && landing == MOE_LAND_FINAL && d.top_k <= 16;

@@ -174,7 +174,7 @@ cudaError_t launch_combine_xchg(const CombArgs& a, int y_dtype, int probs_dtype,
 
 // Plan kernel (plan.cu).
 struct PlanArgs {
-  const int32_t* count_table;  // [e][max_chunks][E]
+  const uint64_t* count_table;  // [e][max_chunks][E] words {count (low 32) | epoch (high 32)}
   int32_t e, t, E, L, n, max_chunks;
   int32_t node, rho;
   int32_t level, landing;
@@ -185,6 +185,7 @@ struct PlanArgs {
   int32_t* aa_table;           // [4][E] {card, base_final, col_off, width} + [n][E] base_staged
   int64_t* recv_rows;          // [1]
   WaitList wait;
+  int32_t poll_peers;          // wait until every peer node's count words carry this epoch
   int32_t* err;
   unsigned long long* dbg;     // optional step timestamps (front kernel debug)
 };
@@ -225,7 +226,7 @@ struct FrontArgs {
   uint64_t* epoch_dev;  // bumped once per dispatch
   int32_t node, max_chunks;
   int32_t n_dst;
-  int32_t* dst_tables[kMaxCards];
+  uint64_t* dst_tables[kMaxCards];  // count words stored into every EP peer's table
   int32_t n_sig;
   uint64_t* sig_flags[kMaxCards];
   int32_t do_plan;      // 0: none (separate plan launch), 1: plan_block, 2: identity plan (lone card, final landing)

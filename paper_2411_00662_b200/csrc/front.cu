@@ -29,6 +29,17 @@ namespace {
 
 constexpr int kFrontSmemMax = 200 * 1024;
 
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ bool wait_flag_ok(const uint64_t* f, unsigned long long epoch) {
+  const unsigned long long t0 = globaltimer();
+  while (ld_acquire_sys(f) < epoch) {
+    if (globaltimer() - t0 > kWaitTimeoutNs) return false;
+    __nanosleep(32);
+  }
+  return true;
+}
 __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long long* p) {
   unsigned long long v;
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
@@ -160,25 +171,24 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
   #pragma unroll 1
   for (int q = tid; q < n * E; q += blockDim.x)
     a.counts[q] = cnt[q];
-  // count exchange: this node's [n][E] block of every EP peer's table
+  // count exchange: this node's [n][E] block of every EP peer's table, as
+  // 8-byte {count | epoch << 32} words — each word is single-copy atomic, so a
+  // reader that sees this epoch sees the count, with no flag round trip and
+  // no fence waiting for the words' own acknowledgement.  Each storing thread
+  // fences first (fence + relaxed store = release; cheap here, nothing of
+  // ours is in flight to a peer): with the reader's acquire this orders this
+  // card's earlier reads of the buffers the peer is about to overwrite.
+  const unsigned long long tag = (unsigned long long)(uint32_t(epoch)) << 32;
+  if (tid < n * E) __threadfence_system();
   #pragma unroll 1
   for (int d = 0; d < a.n_dst; ++d) {
-    int32_t* dst = a.dst_tables[d] + int64_t(a.node) * a.max_chunks * E;
+    unsigned long long* dst =
+        reinterpret_cast<unsigned long long*>(a.dst_tables[d]) + int64_t(a.node) * a.max_chunks * E;
     #pragma unroll 1
-    for (int q = tid; q < n * E; q += blockDim.x)
-      dst[q] = cnt[q];
+    for (int q = tid; q < n * E; q += blockDim.x) st_relaxed_sys(dst + q, tag | uint32_t(cnt[q]));
   }
   __syncthreads();
-  if (tid == 0) {
-    if (a.n_sig > 0) {
-      __threadfence_system();
-      #pragma unroll 1
-      for (int i = 0; i < a.n_sig; ++i) st_release_sys(a.sig_flags[i], epoch);
-    } else {
-      __threadfence();
-    }
-    if (a.dbg) a.dbg[2] = globaltimer();
-  }
+  if (tid == 0 && a.dbg) a.dbg[2] = globaltimer();
   if (!a.do_plan) return;
   if (a.do_plan == 2) {
     // one card holding every expert, final landing: the final layout IS the
@@ -196,18 +206,37 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
     }
     return;
   }
-  if (tid == 0) {
-    s_ok = 1;
+  if (tid == 0) s_ok = 1;
+  if (p.poll_peers) {  // every peer node's block carries this epoch once it has landed
+    const unsigned long long* tbl = reinterpret_cast<const unsigned long long*>(p.count_table);
     const unsigned long long t0 = globaltimer();
     #pragma unroll 1
-    for (int i = 0; i < p.wait.n && s_ok; ++i)
-      while (ld_acquire_sys(p.wait.flags[i]) < epoch) {
-        if (globaltimer() - t0 > kWaitTimeoutNs) {
+    for (;;) {
+      int missing = 0;
+      #pragma unroll 1
+      for (int i = tid; i < p.e * n * E; i += blockDim.x) {
+        const int g = i / (n * E);
+        if (g == p.node) continue;
+        const uint64_t v = ld_acquire_sys(reinterpret_cast<const uint64_t*>(tbl) + int64_t(g) * p.max_chunks * E + (i - g * n * E));
+        missing |= uint32_t(v >> 32) != uint32_t(epoch);
+      }
+      if (!__syncthreads_or(missing)) break;
+      if (globaltimer() - t0 > kWaitTimeoutNs) {
+        if (tid == 0) {
           atomicExch(a.err, (int)MOE_ERR_TIMEOUT);
           s_ok = 0;
-          break;
         }
-        __nanosleep(32);
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  if (tid == 0) {
+    #pragma unroll 1
+    for (int i = 0; i < p.wait.n && s_ok; ++i)
+      if (!wait_flag_ok(p.wait.flags[i], epoch)) {
+        atomicExch(a.err, (int)MOE_ERR_TIMEOUT);
+        s_ok = 0;
       }
     if (a.dbg) a.dbg[3] = globaltimer();
   }

@@ -348,7 +348,8 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
   #pragma unroll 1
   for (int i = tid; i < e * n * E; i += nth) {
     const int g = i / (n * E), r = i % (n * E);
-    tb.ct[i] = __ldcg(a.count_table + int64_t(g) * a.max_chunks * E + r);
+    tb.ct[i] = int(uint32_t(__ldcg(reinterpret_cast<const unsigned long long*>(a.count_table) +
+                                   int64_t(g) * a.max_chunks * E + r)));
   }
   __syncthreads();
   if (a.dbg && tid == 0) a.dbg[8] = globaltimer();
