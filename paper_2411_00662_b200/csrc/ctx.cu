@@ -541,6 +541,8 @@ moe_status do_route(moe_ctx* c, cudaStream_t s) {
   return MOE_OK;
 }
 
+bool xchg_eligible(moe_ctx* c, int level);
+
 PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
   const moe_layer_desc& d = c->d;
   PlanArgs a{};
@@ -559,7 +561,9 @@ PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
   a.seg_cap = d.num_experts;
   a.lists = cd.lists;
   a.local_delta = cd.local_delta;
-  a.aa_table = cd.aa_table;
+  // the per-expert destination table feeds only the token-side AA kernel;
+  // the persistent exchange reads the segment lists instead
+  a.aa_table = xchg_eligible(c, level) ? nullptr : cd.aa_table;
   a.recv_rows = cd.recv_rows;
   a.err = cd.err;
   a.wait = no_wait();
@@ -874,15 +878,23 @@ moe_status dispatch_tail_wait(moe_ctx* c, Card& cd, int level, int n, int landin
 // (xchg.cu).  CTAs are split across roles in proportion to the expected
 // bytes each moves (uniform routing): NVLink legs ~8x slower per byte than
 // local HBM copies.
+// The persistent dispatch runs (and declines nothing later) when the rows
+// take 4+-byte vectors and 16+ CTAs are co-resident (four roles of >= 4).
+bool xchg_eligible(moe_ctx* c, int level) {
+  if (!c->use_xchg || is_virtual(c)) return false;
+  const bool dedup = level != MOE_BASELINE && c->d.t > 1;
+  const int vec = copy_vec(c, dedup);
+  return vec >= 4 && xchg_max_ctas(vec) >= 16;
+}
+
 moe_status launch_dispatch_xchg(moe_ctx* c, Card& cd, int level, int n, int landing, cudaStream_t s, bool* done) {
   *done = false;
   const moe_layer_desc& d = c->d;
   const bool dedup = level != MOE_BASELINE && d.t > 1;
   const bool staged = landing == MOE_LAND_STAGED;
   const int vec = copy_vec(c, dedup);
-  if (vec < 4) return MOE_OK;
+  if (!xchg_eligible(c, level)) return MOE_OK;
   const int max_ctas = xchg_max_ctas(vec);
-  if (max_ctas < 8) return MOE_OK;
   XchgArgs x{};
   x.d2d_in_ag = (staged && dedup && level == MOE_O2) ? 1 : 0;
   // Role sizes from measured per-CTA rates (calibration, profiles/r01):
