@@ -610,7 +610,6 @@ moe_status do_front(moe_ctx* c, bool route, int level, int n, int landing, cudaS
     f.node = cd.node;
     f.max_chunks = d.max_chunks;
     f.n_dst = 0;
-    f.n_sig = 0;
     for (int x = 0; x < d.e; ++x) {
       const int dst = card_of(c, x, cd.rho);
       f.dst_tables[f.n_dst++] = c->peer[dst].count_table;

@@ -38,7 +38,7 @@ enum SegPhase { kPhaseAA = 0, kPhaseAG = 1, kPhaseD2D = 2, kPhaseCAA = 3, kPhase
 
 // Signals carried in each card's flag array: flags[(sig) * kMaxCards + sender].
 enum Signal {
-  kSigCounts = 0,
+  kSigCounts = 0,     // unused since the count words carry their epoch (slot kept: flag layout)
   kSigBarrier = 1,
   kSigChunkBase = 2,  // + phase_signal * max_chunks + j
 };
@@ -227,8 +227,6 @@ struct FrontArgs {
   int32_t node, max_chunks;
   int32_t n_dst;
   uint64_t* dst_tables[kMaxCards];  // count words stored into every EP peer's table
-  int32_t n_sig;
-  uint64_t* sig_flags[kMaxCards];
   int32_t do_plan;      // 0: none (separate plan launch), 1: plan_block, 2: identity plan (lone card, final landing)
   PlanArgs plan;        // its wait list is satisfied at the bumped epoch
   int32_t* plan_scratch;
