@@ -16,9 +16,10 @@
 //            depends only on (token, slot), never on atomics or scheduling;
 //   control  (last CTA, concurrently): the same sums give expert offsets and
 //            per-chunk counts (dataplane.hpp:224-240); it stores this node's
-//            counts into every expert-parallel peer's count table over NVLink,
-//            raises their flags, waits for theirs and plans (plan_block) from
-//            a shared-memory copy of its arguments prefetched while phase 1 ran.
+//            counts into every expert-parallel peer's count table over NVLink
+//            as self-validating {count | epoch} words, polls until the peers'
+//            words carry this epoch and plans (plan_block) from a shared-memory
+//            copy of its arguments prefetched while phase 1 ran.
 #include <algorithm>
 #include <vector>
 
