@@ -39,8 +39,16 @@ def main():
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    ngpu = torch.cuda.device_count()
+    if world > ngpu:
+        # oversubscribed (test-only): several cards per GPU, one process each,
+        # time-sliced; NCCL refuses duplicate GPUs, so the plumbing runs on gloo
+        local %= ngpu
+        torch.cuda.set_device(local)
+        dist.init_process_group("gloo")
+    else:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
     dt = {"bf16": torch.bfloat16, "f32": torch.float32}[a.dtype]
     layer = MoeLayer(a.e, a.t, a.E, a.k, a.T, a.h, dtype=dt, max_chunks=16, device=local, rank=rank,
                      world_size=world)

@@ -29,15 +29,16 @@ def _port():
     return p
 
 
-def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0, persistent=1):
+def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0, persistent=1,
+            per_gpu=1):
     world = e * t
-    if torch.cuda.device_count() < world:
-        pytest.skip(f"needs {world} GPUs, have {torch.cuda.device_count()}")
+    if torch.cuda.device_count() * per_gpu < world:
+        pytest.skip(f"needs {world // per_gpu} GPUs, have {torch.cuda.device_count()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--out", str(tmp), "--groups", str(e), "--tp", str(t), "--experts", str(E), "--topk", str(k), "--tokens", str(T),
            "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs), "--persistent", str(persistent)]
-    res = subprocess.run(cmd, capture_output=True, text=True, timeout=240)
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=240 * per_gpu)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
 
@@ -110,3 +111,31 @@ def test_four_gpus_2x2_deep_chunking(cuda, tmp_path):
     # many chunks through the persistent exchange (per-chunk flags in-kernel)
     runs = "3:16:0,2:8:1,3:16:1"
     _check(_launch(tmp_path, 2, 2, runs=runs, T=1024, h=256), 2, 2, 8, runs)
+
+
+# 8-card topologies (the bench's N=8 shape 2x4 and DeepSeek's 4x2) with two
+# card processes per GPU: the GPUs time-slice the two contexts, so every
+# cross-card wait must survive its peer being descheduled; the layer logic
+# (tables, offsets, flags) is the 8-GPU one.
+def test_eight_cards_2x4_two_per_gpu(cuda, tmp_path):
+    if torch.cuda.device_count() >= 8:
+        pytest.skip("8 GPUs present: covered one card per GPU")
+    runs = "0:1:0,1:1:0,2:2:1,3:4:0"
+    _check(_launch(tmp_path, 2, 4, runs=runs, T=256, h=512, per_gpu=2), 2, 4, 8, runs)
+
+
+def test_eight_cards_4x2_two_per_gpu(cuda, tmp_path):
+    if torch.cuda.device_count() >= 8:
+        pytest.skip("8 GPUs present: covered one card per GPU")
+    runs = "0:1:0,1:1:0,3:2:1"
+    _check(_launch(tmp_path, 4, 2, E=16, k=4, runs=runs, T=256, h=512, per_gpu=2), 4, 2, 16, runs)
+
+
+def test_eight_gpus_2x4(cuda, tmp_path):
+    runs = "0:1:0,1:1:0,2:2:1,3:4:0"
+    _check(_launch(tmp_path, 2, 4, runs=runs, T=512, h=512, graphs=1), 2, 4, 8, runs)
+
+
+def test_eight_gpus_4x2_finegrained(cuda, tmp_path):
+    runs = "0:1:0,1:1:0,3:2:1"
+    _check(_launch(tmp_path, 4, 2, E=16, k=4, runs=runs, T=512, h=512), 4, 2, 16, runs)
