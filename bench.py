@@ -150,6 +150,39 @@ def role_stats(trace):
     return busy, exp
 
 
+NVLINK_PEAK_GBS = 770.0  # B200_PROFILING.md: measured peer copy per direction (nominal 900)
+
+
+def nvlink_legs(experts, e, t, E, T, h, node, dedup, recv_rows, busy):
+    """NVLink bytes this card stores to peers per step, per leg (SURVEY §8(d)
+    numerators with MEASURED counts), and GB/s over each leg's busy time:
+    aa   cross-node pairs x (h/t or h) x 2 B   (dispatch AllToAll)
+    ag   received cross-node rows x h/t x 2 B x (t-1)   (dispatch AllGather)
+    caa  received cross-node rows x (h/t or h) x 2 B   (combine reverse AllToAll)
+    out  T x h/t x 2 B x (t-1)   (output AllGather fused into the un-permute)"""
+    L = E // e
+    valid = experts >= 0
+    own = valid & (experts // L == node)
+    cross_pairs = int((valid & ~own).sum())
+    recv_cross = int(recv_rows) - int(own.sum())
+    sl = (h // t if dedup else h) * 2
+    legs = {"aa": cross_pairs * sl, "ag": recv_cross * sl * (t - 1) if dedup else 0,
+            "caa": recv_cross * sl, "unpermute": T * sl * (t - 1) if dedup else 0}
+    out = {}
+    for r, b in legs.items():
+        us = busy.get(r, 0.0)
+        out[r] = {"bytes": b, "busy_us": us, "gbs": b / us / 1e3 if us and b else None}
+    disp_b = legs["aa"] + legs["ag"]
+    disp_us = busy.get("aa", 0.0) + busy.get("ag", 0.0)
+    comb_b = legs["caa"] + legs["unpermute"]
+    comb_us = busy.get("caa", 0.0) + busy.get("unpermute", 0.0)
+    return {"peak": NVLINK_PEAK_GBS, "legs": out,
+            "dispatch": {"bytes": disp_b, "busy_us": disp_us, "gbs": disp_b / disp_us / 1e3 if disp_us else None},
+            "combine": {"bytes": comb_b, "busy_us": comb_us, "gbs": comb_b / comb_us / 1e3 if comb_us else None},
+            "note": "bytes this card stores to peer GPUs per step / role busy time from the persistent kernels' "
+                    "traces (legs of one kernel run back to back at n=1)"}
+
+
 # ---------------------------------------------------------------------------
 def cpu_port_layer(e, t, E, k, T, h, seed=0):
     """One full layer of the oracle port (oracle/moe_oracle.c: the C
@@ -428,10 +461,11 @@ def main():
         for _ in range(3):
             host_step()
         torch.cuda.synchronize()
-        etot, _ = timed(host_step, args.steps)
+        etot, eper = timed(host_step, args.steps)
         layer.sync()
         e2e = {"value": etot * 1e3 / args.steps, "unit": "us/layer",
-               "h2d_bytes_per_step": hx.numel() * 2 + hl.numel() * 4, "d2h_bytes_per_step": ho.numel() * 2}
+               "h2d_bytes_per_step": hx.numel() * 2 + hl.numel() * 4, "d2h_bytes_per_step": ho.numel() * 2,
+               "step_us_median": statistics.median(eper) * 1e3, "step_us_min": min(eper) * 1e3}
 
     # ---- correctness spot check of the timed configuration (identity experts)
     layer.forward(level, n, landing, stream)
@@ -478,11 +512,20 @@ def main():
                 "frac": ach / peak, "traffic": ncu_traffic, "algorithmic_bytes_per_launch": traffic_alg,
                 "peak_kind": peak_kind, "kernels_gbs": kern}
 
-    # NVLink: bytes this card pushed to peers per step / time of the exchange kernels
+    # NVLink: bytes this card stores to peer GPUs per step, per leg, over the
+    # leg's busy time in the persistent kernels' role traces (first CTA start
+    # to last CTA's release; stores may still be draining at the release)
     nvlink = None
     if world > 1:
-        nvlink = {"note": "bytes stored to peer GPUs per step / sum of exchange-kernel time",
-                  "recv_rows": Rdst}
+        nvlink = nvlink_legs(cd.experts.cpu().numpy(), e, t, E, T, h, node, level != BASELINE and t > 1, Rdst,
+                             roles or {})
+        if nvlink["dispatch"]["gbs"]:
+            roofline = {"bound": "nvlink", "kernel": "k_xchg (persistent dispatch exchange: AllToAll + AllGather legs)",
+                        "achieved": nvlink["dispatch"]["gbs"], "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                        "frac": nvlink["dispatch"]["gbs"] / NVLINK_PEAK_GBS, "traffic": None,
+                        "algorithmic_bytes_per_launch": nvlink["dispatch"]["bytes"],
+                        "peak_kind": "B200_PROFILING.md measured peer copy per direction",
+                        "hbm": roofline}
 
     cpu = None
     if rank == 0 and world == 1 and not args.quick:

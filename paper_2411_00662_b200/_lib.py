@@ -189,6 +189,7 @@ SIGNATURES = {
     "moe_ctx_launch_count": (C.c_int64, [_P]),
     "moe_ctx_xfer": (C.c_int, [_P, _PI64, _I32, _I32, _P]),
     "moe_ctx_set_persistent": (C.c_int, [_P, C.c_int]),
+    "moe_ctx_set_lone": (C.c_int, [_P, C.c_int]),
     "moe_ctx_xchg_trace": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), _I32, _PI32]),
     "moe_ctx_debug_front": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     "moe_lookup_efficiency": (C.c_int, [C.POINTER(Curve), _D, _PD]),
@@ -234,6 +235,8 @@ def load(path: str | os.PathLike | None = None):
             raise ImportError(f"libmonta.so missing at {p} and could not be built: {exc}") from exc
     lib = C.CDLL(str(p), mode=C.RTLD_GLOBAL)
     for name, (res, args) in SIGNATURES.items():
+        if os.environ.get("MONTA_LIB") and not hasattr(lib, name):
+            continue  # A/B against an older build: symbols it predates stay unbound
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
