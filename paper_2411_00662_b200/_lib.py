@@ -189,7 +189,6 @@ SIGNATURES = {
     "moe_ctx_launch_count": (C.c_int64, [_P]),
     "moe_ctx_xfer": (C.c_int, [_P, _PI64, _I32, _I32, _P]),
     "moe_ctx_set_persistent": (C.c_int, [_P, C.c_int]),
-    "moe_ctx_set_lone": (C.c_int, [_P, C.c_int]),
     "moe_ctx_xchg_trace": (C.c_int, [_P, C.c_int, C.POINTER(C.c_uint64), _I32, _PI32]),
     "moe_ctx_debug_front": (C.c_int, [_P, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
     "moe_lookup_efficiency": (C.c_int, [C.POINTER(Curve), _D, _PD]),
