@@ -95,6 +95,39 @@ __device__ __forceinline__ void sum_hists(const int32_t* hist, int rows, int E, 
   const int N = (tot ? rows : b_pre) * E;
   const double inv_tpc = 1.0 / double(tpc);
   int row = threadIdx.x / E, x = threadIdx.x - (threadIdx.x / E) * E;
+  if (dr == 0 && (cnt == nullptr || (n == 1 && tpc >= rows))) {
+    // common case: every thread keeps one expert x; sum in registers, fold
+    // the lanes of a warp that share x, then one shared atomic per (warp, x)
+    // (per-value atomics were 64-way conflicts on E addresses: ~1 us)
+    int st = 0, sp = 0;
+    for (int base = threadIdx.x; base < N; base += kB * bd) {
+      int v[kB];
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        const int i = base + u * bd;
+        v[u] = i < N ? __ldcg(hist + i) : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < kB; ++u) {
+        st += v[u];
+        sp += row < b_pre ? v[u] : 0;
+        row += dq;
+      }
+    }
+    if (32 % E == 0) {
+      for (int off = 16; off >= E; off >>= 1) {
+        st += __shfl_xor_sync(0xffffffffu, st, off);
+        sp += __shfl_xor_sync(0xffffffffu, sp, off);
+      }
+      if ((threadIdx.x & 31) >= E) st = sp = 0;
+    }
+    if (st) {
+      if (tot) atomicAdd(tot + x, st);
+      if (cnt) atomicAdd(cnt + x, st);  // one chunk holding every tile
+    }
+    if (sp && pre) atomicAdd(pre + x, sp);
+    return;
+  }
   for (int base = threadIdx.x; base < N; base += kB * bd) {
     int v[kB];
 #pragma unroll
@@ -165,22 +198,16 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
       a.counts_acc[q] = 0;
     }
   __syncthreads();
-  block_exscan(offs, E, ctot);
-  #pragma unroll 1
-  for (int x = tid; x <= E; x += blockDim.x)
-    a.expert_offsets[x] = offs[x];
-  #pragma unroll 1
-  for (int q = tid; q < n * E; q += blockDim.x)
-    a.counts[q] = cnt[q];
   // count exchange: this node's [n][E] block of every EP peer's table, as
   // 8-byte {count | epoch << 32} words — each word is single-copy atomic, so a
   // reader that sees this epoch sees the count, with no flag round trip and
-  // no fence waiting for the words' own acknowledgement.  Each storing thread
-  // fences first (fence + relaxed store = release; cheap here, nothing of
-  // ours is in flight to a peer): with the reader's acquire this orders this
-  // card's earlier reads of the buffers the peer is about to overwrite.
+  // no fence waiting for the words' own acknowledgement.  No fence before the
+  // push either (a system fence costs ~1.7 us here): a peer that sees these
+  // words goes on to STORE into this card's buffers, and every read this card
+  // makes of those buffers (the previous combine, the host) was made by a
+  // kernel that completed before this one started — all cross-GPU traffic is
+  // stores into the receiver, so there is no read left for them to overtake.
   const unsigned long long tag = (unsigned long long)(uint32_t(epoch)) << 32;
-  if (tid < n * E) __threadfence_system();
   #pragma unroll 1
   for (int d = 0; d < a.n_dst; ++d) {
     unsigned long long* dst =
@@ -188,6 +215,13 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
     #pragma unroll 1
     for (int q = tid; q < n * E; q += blockDim.x) st_relaxed_sys(dst + q, tag | uint32_t(cnt[q]));
   }
+  block_exscan(offs, E, ctot);
+  #pragma unroll 1
+  for (int x = tid; x <= E; x += blockDim.x)
+    a.expert_offsets[x] = offs[x];
+  #pragma unroll 1
+  for (int q = tid; q < n * E; q += blockDim.x)
+    a.counts[q] = cnt[q];
   __syncthreads();
   if (tid == 0 && a.dbg) a.dbg[2] = globaltimer();
   if (!a.do_plan) return;
