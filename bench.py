@@ -479,9 +479,13 @@ def main():
     # ---- e2e through the C ABI with host buffers
     e2e = None
     if not args.quick:
-        hx = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
-        hl = torch.empty(T, E, dtype=torch.float32).pin_memory()
-        ho = torch.empty(T, h, dtype=torch.bfloat16).pin_memory()
+        # staging buffers from the ABI's host allocator (moe_host_alloc: cudaHostAlloc,
+        # portable): on some boxes torch's pin_memory() pages copy host->device at
+        # 37 GB/s against 55 GB/s for cudaHostAlloc'd ones (scripts/pcie_probe.py)
+        from paper_2411_00662_b200.ops import host_empty
+        hx = host_empty((T, h), torch.bfloat16)
+        hl = host_empty((T, E), torch.float32)
+        ho = host_empty((T, h), torch.bfloat16)
         hx.copy_(x0.cpu())
         hl.copy_(l0.cpu())
 
