@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """MoE dispatch+combine benchmark (BASELINE.json metric: us/layer).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config mixtral|toy|70b|deepseek]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
 Workload (configs[1], Mixtral-8x7B MoE layer, bf16): T = 4096 tokens per
@@ -36,9 +36,32 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
 
-CONFIG = {"workload": "mixtral-8x7b-moe-layer", "tokens_per_node": 4096, "hidden": 4096, "experts": 8,
-          "top_k": 2, "dtype": "bf16", "logits": "f32"}
-TOPOLOGY = {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}
+# BASELINE.json configs as workloads (--config); the default, configs[1], is the metric's workload and the
+# others are reported the same way for completeness.  Topology (e x t) per GPU count.
+WORKLOADS = {
+    "mixtral": ({"workload": "mixtral-8x7b-moe-layer", "tokens_per_node": 4096, "hidden": 4096, "experts": 8,
+                 "top_k": 2, "dtype": "bf16", "logits": "f32"}, {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}),
+    "toy": ({"workload": "toy-moe-layer-fp32", "tokens_per_node": 2048, "hidden": 1024, "experts": 8,
+             "top_k": 2, "dtype": "f32", "logits": "f32"}, {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}),
+    "70b": ({"workload": "2x70b-moe-layer", "tokens_per_node": 8192, "hidden": 8192, "experts": 2,
+             "top_k": 1, "dtype": "bf16", "logits": "f32"}, {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (2, 4)}),
+    "deepseek": ({"workload": "deepseek-v2-finegrained-moe-layer", "tokens_per_node": 8192, "hidden": 5120,
+                  "experts": 160, "top_k": 6, "dtype": "bf16", "logits": "f32"},
+                 {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}),
+}
+CONFIG, TOPOLOGY = WORKLOADS["mixtral"]
+ELEM = 2  # payload bytes per element
+
+
+def select_workload(name: str) -> None:
+    global CONFIG, TOPOLOGY, ELEM
+    CONFIG, TOPOLOGY = WORKLOADS[name]
+    ELEM = 4 if CONFIG["dtype"] == "f32" else 2
+
+
+def payload_dtype():
+    import torch
+    return torch.float32 if CONFIG["dtype"] == "f32" else torch.bfloat16
 METRIC = "moe_dispatch_combine_us_per_layer"
 SPAN_LEAD_CYCLES = 2_000_000  # ~1 ms spin ahead of each per-kernel span pass
 L2_FLUSH_BYTES = 256 << 20
@@ -165,7 +188,7 @@ def nvlink_legs(experts, e, t, E, T, h, node, dedup, recv_rows, busy):
     own = valid & (experts // L == node)
     cross_pairs = int((valid & ~own).sum())
     recv_cross = int(recv_rows) - int(own.sum())
-    sl = (h // t if dedup else h) * 2
+    sl = (h // t if dedup else h) * ELEM
     legs = {"aa": cross_pairs * sl, "ag": recv_cross * sl * (t - 1) if dedup else 0,
             "caa": recv_cross * sl, "unpermute": T * sl * (t - 1) if dedup else 0}
     out = {}
@@ -193,7 +216,10 @@ def cpu_port_layer(e, t, E, k, T, h, seed=0):
     import oracle
     rng = np.random.default_rng(seed)
     x = rng.standard_normal((e, T, h)).astype(np.float32)
-    xbytes = (x.view(np.uint32) >> 16).astype(np.uint16).view(np.uint8).reshape(e, T, h * 2)  # bf16 bits
+    if ELEM == 4:
+        xbytes = x.view(np.uint8).reshape(e, T, h * 4)
+    else:
+        xbytes = (x.view(np.uint32) >> 16).astype(np.uint16).view(np.uint8).reshape(e, T, h * 2)  # bf16 bits
     logits = rng.standard_normal((e, T, E))
     t0 = time.perf_counter()
     experts = np.zeros((e, T, k), np.int32)
@@ -201,8 +227,8 @@ def cpu_port_layer(e, t, E, k, T, h, seed=0):
     for g in range(e):
         experts[g], probs[g] = oracle.route_topk(logits[g], k)
     nodes = oracle.Nodes(e, t, E, xbytes, experts)
-    fin = nodes.dispatch_chunked(oracle.O1, 1, 2)[0] if t > 1 else nodes.dispatch_monolithic()
-    nodes.combine(oracle.BF16, fin, probs)
+    fin = nodes.dispatch_chunked(oracle.O1, 1, ELEM)[0] if t > 1 else nodes.dispatch_monolithic()
+    nodes.combine(oracle.F32 if ELEM == 4 else oracle.BF16, fin, probs)
     return time.perf_counter() - t0
 
 
@@ -232,7 +258,7 @@ def run_reference(args):
     v = statistics.mean(vals)
     line = {"metric": METRIC, "value": v, "unit": "us/layer", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic", "impl": "reference",
+            "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic", "impl": "reference",
             "config": dict(CONFIG, topology=f"{e}x{t}", level="O1" if t > 1 else "Baseline"),
             "cpu_baseline": {"value": v, "unit": "us/layer", "cores": 1, "kind": "port",
                              "sample": f"full layer ({T} tokens x {e} nodes) per step, {args.steps} steps; "
@@ -248,6 +274,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="mixtral", choices=sorted(WORKLOADS),
+                    help="BASELINE.json workload (default: configs[1], the metric's)")
     ap.add_argument("--level", default="auto", help="auto|baseline|o1|o2|o3")
     ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--landing", default="final", choices=["final", "staged"])
@@ -256,6 +284,7 @@ def main():
     ap.add_argument("--no-persistent", action="store_true",
                     help="multi-GPU: one launch per (leg, chunk) instead of the persistent exchange kernels")
     args = ap.parse_args()
+    select_workload(args.config)
     if args.warmup < 3:
         args.warmup = 3
     if args.impl == "reference":
@@ -296,14 +325,15 @@ def main():
             curves = P.CurveSet(P.EfficiencyCurve.constant(0.8), P.EfficiencyCurve.constant(0.8),
                                 P.EfficiencyCurve.constant(0.8))
             ov = P.OverheadModel(8e-6, 4e-6)
-        model = P.ModelSpec(b=1, s=T * k, h=h, k=k, bpe=2)  # routed rows: s_eff = T*k
+        model = P.ModelSpec(b=1, s=T * k, h=h, k=k, bpe=ELEM)  # routed rows: s_eff = T*k
         decision = P.select_strategy(model, P.ParallelSpec(t=t, e=e), P.b200_cluster(e, t), curves, ov, n_cap=16)
         level, n = int(decision.level), decision.n
         while T % n:
             n -= 1
     landing = LAND_STAGED if args.landing == "staged" else LAND_FINAL
 
-    layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, logit_dtype=torch.float32, max_chunks=16,
+    PD = payload_dtype()
+    layer = MoeLayer(e, t, E, k, T, h, dtype=PD, logit_dtype=torch.float32, max_chunks=16,
                      device=local, rank=rank if world > 1 else 0, world_size=world)
     layer.connect()
     layer.enable_graphs(not args.no_graphs)
@@ -311,7 +341,7 @@ def main():
         layer.set_persistent(False)
     cd = layer.cards[0]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + node)
-    x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(torch.bfloat16)
+    x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(PD)
     l0 = torch.randn(T, E, generator=gen, device=f"cuda:{local}")
     cd.x.copy_(x0)
     cd.logits.copy_(l0)
@@ -483,9 +513,9 @@ def main():
         # portable): on some boxes torch's pin_memory() pages copy host->device at
         # 37 GB/s against 55 GB/s for cudaHostAlloc'd ones (scripts/pcie_probe.py)
         from paper_2411_00662_b200.ops import host_empty
-        hx = host_empty((T, h), torch.bfloat16)
+        hx = host_empty((T, h), PD)
         hl = host_empty((T, E), torch.float32)
-        ho = host_empty((T, h), torch.bfloat16)
+        ho = host_empty((T, h), PD)
         hx.copy_(x0.cpu())
         hl.copy_(l0.cpu())
 
@@ -498,7 +528,7 @@ def main():
         etot, eper = timed(host_step, args.steps)
         layer.sync()
         e2e = {"value": etot * 1e3 / args.steps, "unit": "us/layer",
-               "h2d_bytes_per_step": hx.numel() * 2 + hl.numel() * 4, "d2h_bytes_per_step": ho.numel() * 2,
+               "h2d_bytes_per_step": hx.numel() * ELEM + hl.numel() * 4, "d2h_bytes_per_step": ho.numel() * ELEM,
                "step_us_median": statistics.median(eper) * 1e3, "step_us_min": min(eper) * 1e3}
 
     # ---- correctness spot check of the timed configuration (identity experts)
@@ -510,7 +540,7 @@ def main():
     # ---- roofline of the dominant kernel (HBM-bound: algorithmic bytes / live duration)
     peak, peak_kind = load_peaks()
     R = T * k
-    row = h * 2
+    row = h * ELEM
     Rdst = layer.recv_rows(cd.card)
     # algorithmic bytes per launch
     if world == 1:
@@ -520,7 +550,7 @@ def main():
     else:
         aa_bytes = None  # NVLink-bound: reported under "nvlink"
     unp_cols = h // t if (level != BASELINE and t > 1) else h
-    unp_bytes = R * unp_cols * 2 + T * unp_cols * 2 * (t if (level != BASELINE and t > 1) else 1) + 12 * R
+    unp_bytes = R * unp_cols * ELEM + T * unp_cols * ELEM * (t if (level != BASELINE and t > 1) else 1) + 12 * R
     kern = {}
     if "aa" in stages and aa_bytes:
         kern["fused_permute_aa"] = (aa_bytes * stages["aa"]["launches_per_step"] / max(stages["aa"]["sum_us_per_step"], 1e-9)) / 1e3
@@ -543,7 +573,8 @@ def main():
     else:
         ach = kern.get("unpermute_combine", 0.0)
         traffic_alg = unp_bytes
-        dom_name = "unpermute_combine (k_unpermute_k2<bf16,bf16,f32>)"
+        dom_name = ("unpermute_combine (k_unpermute_k2<bf16,bf16,f32>)" if ELEM == 2 and k <= 2
+                    else "unpermute_combine (k_unpermute)")
     ncu_traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
@@ -577,7 +608,7 @@ def main():
 
     line = {"metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "weak",
-            "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn x, randn f32 gate logits)",
+            "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic (randn x, randn f32 gate logits)",
             "config": dict(CONFIG, topology=f"{e}x{t}", level=_lib.LEVEL_NAMES[level], chunks=n,
                            landing=args.landing, parallelism=f"ep{e}xtp{t}", cuda_graphs=not args.no_graphs,
                            l2="flushed between steps (256 MiB memset + 256 MiB read outside the events: cold, clean L2)",

@@ -37,6 +37,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
   const int64_t pieces = (nvec + kPieceVec - 1) / kPieceVec;
   const int64_t n_items = (a.tok_end - a.tok_begin) * pieces;
   const int64_t warps = int64_t(gridDim.x) * (kTokThreads / 32);
+  const uint64_t pol = l2_evict_first_policy();  // x is read once: keep L2 for the stored rows
   for (int64_t it = int64_t(blockIdx.x) * (kTokThreads / 32) + (threadIdx.x >> 5); it < n_items; it += warps) {
     const int64_t i = a.tok_begin + it / pieces;
     const int64_t v0 = (it % pieces) * kPieceVec;
@@ -64,7 +65,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t v = v0 + u * 32 + lane;
-      if (v < nvec) r[u] = ld_stream(src + v);
+      if (v < nvec) r[u] = ld_stream_ef(src + v, pol);
     }
     const int64_t piece_lo = v0 * V, piece_hi = piece_lo + int64_t(kPieceVec) * V;
     for (int s = 0; s < k; ++s) {

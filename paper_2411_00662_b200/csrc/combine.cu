@@ -187,6 +187,7 @@ __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_co
   const TProb* probs = static_cast<const TProb*>(a.probs);
   const int k = a.k;
   const int warps = int(gridDim.x) * (kThreads / 32);
+  const uint64_t pol = l2_evict_first_policy();
   for (int it = int(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); it < n_items; it += warps) {
     const int64_t i = a.tok_begin + it / nb;
     const int cv = (it % nb) * (32 * UV);  // first vector of the item
@@ -214,9 +215,15 @@ __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_co
     if (k < 2) r1 = nullptr;
     Pack<TIn, N> y0[UV], y1[UV];
 #pragma unroll
-    for (int w = 0; w < UV; ++w) {
-      if (r0) y0[w] = *reinterpret_cast<const Pack<TIn, N>*>(r0 + w * 512 + lane * 16);
-      if (r1) y1[w] = *reinterpret_cast<const Pack<TIn, N>*>(r1 + w * 512 + lane * 16);
+    for (int w = 0; w < UV; ++w) {  // rows are read once: L2 evict-first (1% per layer, A/B)
+      if (r0) {
+        const int4 q = ld_stream_ef(reinterpret_cast<const int4*>(r0 + w * 512 + lane * 16), pol);
+        y0[w] = *reinterpret_cast<const Pack<TIn, N>*>(&q);
+      }
+      if (r1) {
+        const int4 q = ld_stream_ef(reinterpret_cast<const int4*>(r1 + w * 512 + lane * 16), pol);
+        y1[w] = *reinterpret_cast<const Pack<TIn, N>*>(&q);
+      }
     }
     const int64_t obase = i * a.out_stride + (a.col_begin + int64_t(cv + lane) * N) * int64_t(sizeof(TOut));
 #pragma unroll

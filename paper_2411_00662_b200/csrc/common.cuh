@@ -69,6 +69,20 @@ __device__ __forceinline__ int4 ld_stream(const int4* p) {
                : "l"(p));
   return r;
 }
+// Read-once source rows that should not displace data a later kernel of the
+// step re-reads from L2 (L2 evict-first policy).
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ int4 ld_stream_ef(const int4* p, uint64_t pol) {
+  int4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.s32 {%0,%1,%2,%3}, [%4], %5;"
+               : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+               : "l"(p), "l"(pol));
+  return r;
+}
 __device__ __forceinline__ int2 ld_stream(const int2* p) {
   int2 r;
   asm volatile("ld.global.nc.L1::no_allocate.v2.s32 {%0,%1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
@@ -81,6 +95,7 @@ __device__ __forceinline__ int ld_stream(const int* p) {
 }
 __device__ __forceinline__ short ld_stream(const short* p) { return *p; }
 __device__ __forceinline__ char ld_stream(const char* p) { return *p; }
+template <class V> __device__ __forceinline__ V ld_stream_ef(const V* p, uint64_t) { return ld_stream(p); }
 
 // Plain (coherent) loads for buffers another GPU may have written during
 // this launch's lifetime window (after an acquire).
