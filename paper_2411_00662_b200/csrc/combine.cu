@@ -170,7 +170,7 @@ __device__ __forceinline__ void unpermute_tokens(const UnpermArgs& a, int64_t to
 // CTAs (32 warps) fit per SM — occupancy is what keeps the gather at HBM
 // speed (scripts/micro/gather_bench.cu: 5.7 TB/s at 16 warps/SM, 6.3 TB/s at
 // 32 warps/SM for the same bytes in flight).
-template <class TIn, class TOut, class TProb, int UV, int MinB>
+template <class TIn, class TOut, class TProb, int UV, int MinB, int KMAX = 2>
 __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_constant__ UnpermArgs a) {
   constexpr int N = 16 / sizeof(TIn);
   __shared__ int s_delta[kDeltaSmem];
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_co
     const char* r0 = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row), 0));
     const char* r1 = reinterpret_cast<const char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(row), 1));
     const float p0 = __shfl_sync(0xffffffffu, p, 0), p1 = __shfl_sync(0xffffffffu, p, 1);
-    if (k < 2) r1 = nullptr;
+    if (KMAX < 2 || k < 2) r1 = nullptr;  // KMAX == 1: top-1 instance, wider items instead of a second slot
     Pack<TIn, N> y0[UV], y1[UV];
 #pragma unroll
     for (int w = 0; w < UV; ++w) {  // rows are read once: L2 evict-first (1% per layer, A/B)
@@ -395,7 +395,10 @@ static cudaError_t launch_n(const UnpermArgs& a, int grid, cudaStream_t s) {
       (a.tok_end - a.tok_begin) * (a.cols / 8) < (int64_t(1) << 31)) {
     // top-1/top-2: lean kernel, both slots' loads in flight (2 KiB items, 3 CTAs/SM;
     // 1 KiB items at 4 CTAs/SM measured slower)
-    k_unpermute_k2<TIn, TOut, TProb, 4, 3><<<g(8, 4, 3), kThreads, 0, s>>>(a);
+    if (a.k == 1 && (a.cols / 8) % (32 * 8) == 0)  // top-1: 4 KiB items keep as many bytes in flight per warp
+      k_unpermute_k2<TIn, TOut, TProb, 8, 3, 1><<<g(8, 8, 3), kThreads, 0, s>>>(a);
+    else
+      k_unpermute_k2<TIn, TOut, TProb, 4, 3><<<g(8, 4, 3), kThreads, 0, s>>>(a);
   } else if (N16 >= 8 && fits(8)) {
     k_unpermute<TIn, TAcc, TOut, TProb, 8><<<g(8, unperm_uv<8>()), kThreads, 0, s>>>(a);
   } else if (N16 >= 4 && fits(4)) {

@@ -342,3 +342,10 @@ def test_full_size_configs_round_trip(cuda, cfg):
             assert err <= 1e-2, (cd.card, err)
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("e,t,level", [(1, 1, BASELINE), (2, 1, BASELINE), (2, 2, O1), (2, 2, O3)])
+def test_top1_wide_rows(cuda, e, t, level):
+    """Top-1 routing over rows of >= 2048 columns per slice takes the 4 KiB-item
+    top-1 un-permute (the 2x70B config's shape class)."""
+    _run(e, t, 2 * e, 1, 300, 2048 * t, torch.bfloat16, level, 1 if level != O3 else 2, LAND_FINAL, seed=7 + e + t)
