@@ -382,8 +382,26 @@ def main():
             dist.all_reduce(total, op=dist.ReduceOp.MAX)
         return float(total.item()), ms
 
-    def step(lv=level, nn=n, ld=landing):
-        layer.forward(lv, nn, ld, stream)
+    def step(lv=None, nn=None, ld=None):  # defaults: the (possibly re-chosen) level, n, landing
+        layer.forward(level if lv is None else lv, n if nn is None else nn, landing if ld is None else ld, stream)
+
+    # The planner's model assumes the AllToAll and AllGather legs own separate
+    # links (inter- vs intra-node); on one NVSwitch box they share each GPU's
+    # ports, so a chunked proposal is checked in place against O1 (a short
+    # trial of each, max over ranks) and the faster one runs.  The reference's
+    # selection itself is unchanged (decision is reported as is).
+    autotune = None
+    if decision is not None and args.level == "auto" and (level, n) != (O1, 1):
+        def trial(lv, nn):
+            for _ in range(3):
+                step(lv, nn)
+            layer.sync()
+            return timed(lambda: step(lv, nn), 5)[0] * 1e3 / 5
+        t_plan, t_o1 = trial(level, n), trial(O1, 1)
+        autotune = {"planner": [_lib.LEVEL_NAMES[level], n, t_plan], "O1": ["O1", 1, t_o1]}
+        if t_o1 < t_plan:
+            level, n = O1, 1
+        autotune["chosen"] = [_lib.LEVEL_NAMES[level], n]
 
     for _ in range(args.warmup):
         step()
@@ -614,7 +632,7 @@ def main():
                            l2="flushed between steps (256 MiB memset + 256 MiB read outside the events: cold, clean L2)",
                            planner=None if decision is None else
                            {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
-                            "t_pred_us": decision.t_pred * 1e6}),
+                            "t_pred_us": decision.t_pred * 1e6, "in_place_check_us": autotune}),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "stages": stages, "roles_busy_us": roles, "exposed_alltoall_us": exp_aa,
             "naive": naive,
