@@ -298,6 +298,18 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const __grid_constant__
   if (tid == 0) {
     s_epoch = *a.epoch_dev + 1;  // read before this CTA arrives: the bump happens after every arrival
     if (a.dbg && blockIdx.x == 0) a.dbg[0] = globaltimer();
+    // the CTA's tiles of gate logits are contiguous: one bulk L2 prefetch up
+    // front, so the router's passes over a wide tile (E = 160: four passes)
+    // do not each wait for HBM
+    if (a.route && !control && blockIdx.x < nt) {
+      const size_t lb = sizeof(T) * size_t(E);
+      const int64_t i0 = int64_t(blockIdx.x) * a.tile_tokens;
+      const int64_t i1 = i0 + a.tile_tokens < a.T ? i0 + a.tile_tokens : a.T;
+      const uint32_t bytes = uint32_t(size_t(i1 - i0) * lb) & ~15u;
+      const char* src = static_cast<const char*>(a.logits) + size_t(i0) * lb;
+      if (bytes >= 16 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && bytes <= (1u << 20))
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
   }
   // ---------------- phase 1: route + tile histograms (tile CTAs)
   if (!control) {
