@@ -131,6 +131,43 @@ moe_status moe_unpermute_combine(const void* y, int y_dtype, int64_t y_row_elems
                                  int64_t out_row_elems, void* stream);
 
 /* ------------------------------------------------------------------------
+ * 1b. Backward of the stateless ops.  The reference
+ * has no backward; these are the adjoints of moe_unpermute_combine,
+ * moe_permute_rows and moe_route_topk so a training step can run through the
+ * same index.  On a multi-card layer the cross-card legs of the backward are
+ * the forward exchanges in the opposite direction; these are the per-card
+ * kernels either side of them.
+ * ------------------------------------------------------------------------ */
+
+/* Adjoint of moe_unpermute_combine:
+ *   grad_y[slot_pos[i,s], 0:width) = probs[i,s] * grad_out[i, 0:width)   (y's dtype)
+ *   grad_probs[i,s]                = sum_q grad_out[i,q] * y[slot_pos[i,s], q]  (probs' dtype)
+ * fp32 arithmetic (fp64 if any operand is f64).  grad_y or grad_probs may be
+ * NULL to skip that output; grad_probs needs y.  Dtypes: grad_out and y
+ * f32/bf16/f16/f64, probs f32/f64. */
+moe_status moe_combine_backward(const void* grad_out, int grad_dtype, int64_t grad_row_elems,
+                                const void* y, int y_dtype, int64_t y_row_elems, int64_t width,
+                                const int32_t* slot_pos, const void* probs, int probs_dtype,
+                                int64_t T, int32_t k, void* grad_y, int64_t grad_y_row_elems,
+                                void* grad_probs, void* stream);
+
+/* Adjoint of the dispatch gather (moe_permute_rows through slot_pos):
+ *   grad_x[i, 0:width) = sum_s grad_rows[slot_pos[i,s], 0:width)
+ * accumulated from zero in ascending slot order, fp32 (fp64 if f64).
+ * 1 <= k <= 32. */
+moe_status moe_dispatch_backward(const void* grad_rows, int rows_dtype, int64_t row_elems, int64_t width,
+                                 const int32_t* slot_pos, int64_t T, int32_t k, void* grad_x,
+                                 int out_dtype, int64_t out_row_elems, void* stream);
+
+/* Adjoint of moe_route_topk with respect to the logits (the selection is
+ * piecewise constant):  grad_logits[i,e] = P_e * (G_e - sum_s g_s P_{x_s})
+ * where P = softmax(logits[i]), g = grad_probs[i], G_e = g_s if e == x_s.
+ * logits, grad_probs and grad_logits share logit_dtype (MOE_F32 or MOE_F64). */
+moe_status moe_route_backward(const void* logits, int logit_dtype, int64_t T, int32_t E, int32_t k,
+                              const int32_t* experts, const void* grad_probs, void* grad_logits,
+                              void* stream);
+
+/* ------------------------------------------------------------------------
  * 2. Layer context: one MoE layer's dispatch + combine over e x t cards
  * ------------------------------------------------------------------------
  * Topology (dataplane::VirtualTopology, dataplane.hpp:25-33): card c =

@@ -165,7 +165,11 @@ SIGNATURES = {
     "moe_build_index": (C.c_int, [_P, _I64, _I32, _I32, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "moe_permute_rows": (C.c_int, [_P, _I64, _I64, _I64, _P, _I64, _P, _I64, _P]),
     "moe_unpermute_combine": (C.c_int, [_P, C.c_int, _I64, _I64, _P, _P, C.c_int, _I64, _I32, _P, C.c_int, _I64, _P]),
-    "moe_ctx_create": (C.c_int, [C.POINTER(LayerDesc), C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
+    "moe_combine_backward": (C.c_int, [_P, C.c_int, _I64, _P, C.c_int, _I64, _I64, _P, _P, C.c_int, _I64, _I32,
+                                       _P, _I64, _P, _P]),
+    "moe_dispatch_backward": (C.c_int, [_P, C.c_int, _I64, _I64, _P, _I64, _I32, _P, C.c_int, _I64, _P]),
+    "moe_route_backward": (C.c_int, [_P, C.c_int, _I64, _I32, _I32, _P, _P, _P, _P]),
+    "moe_ctx_create": (C.c_int,[C.POINTER(LayerDesc), C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "moe_ctx_destroy": (C.c_int, [_P]),
     "moe_ctx_card_view": (C.c_int, [_P, C.c_int, C.POINTER(CardView)]),
     "moe_ctx_num_local_cards": (C.c_int, [_P]),

@@ -1,0 +1,366 @@
+// Backward pass of the lone-card data path.
+//
+// The reference has no backward (it is a planner + data-plane simulator); these
+// are the adjoints of the three forward ops this library exports, so a
+// training step can run router -> dispatch -> experts -> combine and back:
+//
+//   combine    out[i]  = sum_s p[i,s] * y[pos[i,s]]          (dataplane.hpp:325-342)
+//     grad_y[pos[i,s]] = p[i,s] * grad_out[i]
+//     grad_p[i,s]      = <grad_out[i], y[pos[i,s]]>
+//   dispatch   rows[pos[i,s]] = x[i]                          (dataplane.hpp:118-140)
+//     grad_x[i]        = sum_s grad_rows[pos[i,s]]             (un-permute with unit weights)
+//   route      p[i,s]  = softmax(z[i])[x_s]  (not renormalised, dataplane.hpp:72-106)
+//     grad_z[i,e]      = P_e * (G_e - sum_s g_s P_{x_s}),  G_e = g_s if e == x_s else 0
+//
+// On a multi-card layer the cross-card legs of the backward are the forward
+// exchanges run in the opposite direction (combine backward = dispatch of the
+// weighted gradient rows, dispatch backward = combine's reverse AllToAll); the
+// kernels here are the per-card compute either side of them.
+//
+// All three are HBM-bound streaming kernels: one warp per token, 8-element
+// packs moved with 16-byte vector accesses (bf16/f16: one int4, f32: two,
+// f64: four), fp32 accumulation (fp64 for f64), no atomics: every output
+// element has exactly one writer.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "common.cuh"
+
+namespace monta {
+namespace {
+
+// fp32 accumulation unless any operand is fp64.
+template <class... T> struct AccOf {
+  using type = std::conditional_t<(std::is_same_v<T, double> || ...), double, float>;
+};
+
+template <class A, class T> __device__ __forceinline__ A cvt_in(T v) { return A(to_f32(v)); }
+template <> __device__ __forceinline__ double cvt_in<double, double>(double v) { return v; }
+
+template <class T, class A> __device__ __forceinline__ T cvt_out(A v) { return from_f32<T>(float(v)); }
+template <> __device__ __forceinline__ double cvt_out<double, double>(double v) { return v; }
+template <> __device__ __forceinline__ float cvt_out<float, double>(double v) { return float(v); }
+
+// N consecutive elements of T, loaded/stored with 16-byte accesses when N == 8
+// (8 * sizeof(T) is a multiple of 16 for every supported dtype) and the
+// caller guaranteed alignment; N == 1 is the scalar fallback.
+template <class T, int N> struct Pack {
+  static_assert(N == 1 || N == 8, "pack of 1 or 8");
+  template <class A> __device__ __forceinline__ static void load(const T* p, A* out) {
+    if constexpr (N == 1) {
+      out[0] = cvt_in<A>(*p);
+    } else {
+      constexpr int kVec = int(8 * sizeof(T) / 16);  // int4 accesses per pack of 8
+      union { int4 v[kVec]; T e[8]; } u;
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) u.v[j] = ld_stream(reinterpret_cast<const int4*>(p) + j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) out[j] = cvt_in<A>(u.e[j]);
+    }
+  }
+  template <class A> __device__ __forceinline__ static void store(T* p, const A* in) {
+    if constexpr (N == 1) {
+      *p = cvt_out<T>(in[0]);
+    } else {
+      constexpr int kVec = int(8 * sizeof(T) / 16);  // int4 accesses per pack of 8
+      union { int4 v[kVec]; T e[8]; } u;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) u.e[j] = cvt_out<T>(in[j]);
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) st_vec(reinterpret_cast<int4*>(p) + j, u.v[j]);
+    }
+  }
+};
+
+template <class A> __device__ __forceinline__ A warp_sum(A v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <class P> __device__ __forceinline__ double load_p(const P* p) { return double(*p); }
+
+// combine backward: warp per token; for each slot the warp streams the
+// token's gradient row (L1/L2 after the first slot) and the expert output
+// row, writes p * grad into the expert-gradient row and reduces the dot
+// product for grad_probs.
+template <class TG, class TY, class PT, int N>
+__global__ void __launch_bounds__(256) k_combine_bwd(const TG* __restrict__ g, int64_t g_stride,
+                                                     const TY* __restrict__ y, int64_t y_stride,
+                                                     int64_t width, const int32_t* __restrict__ pos,
+                                                     const PT* __restrict__ probs, int64_t T, int k,
+                                                     TY* __restrict__ gy, int64_t gy_stride,
+                                                     PT* __restrict__ gp) {
+  using A = typename AccOf<TG, TY, PT>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t packs = width / N;
+  for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < T; i += warps) {
+    const TG* grow = g + i * g_stride;
+    for (int s = 0; s < k; ++s) {
+      const int64_t r = pos[i * k + s];
+      const A p = A(load_p(probs + i * k + s));
+      A dot = 0;
+      for (int64_t c = lane; c < packs; c += 32) {
+        A gv[N];
+        Pack<TG, N>::load(grow + c * N, gv);
+        if (gp) {
+          A yv[N];
+          Pack<TY, N>::load(y + r * y_stride + c * N, yv);
+#pragma unroll
+          for (int j = 0; j < N; ++j) dot += gv[j] * yv[j];
+        }
+        if (gy) {
+          A ov[N];
+#pragma unroll
+          for (int j = 0; j < N; ++j) ov[j] = p * gv[j];
+          Pack<TY, N>::store(gy + r * gy_stride + c * N, ov);
+        }
+      }
+      if (gp) {
+        dot = warp_sum(dot);
+        if (lane == 0) gp[i * k + s] = PT(dot);
+      }
+    }
+  }
+}
+
+// dispatch backward: grad_x[i] = sum_s grad_rows[pos[i,s]], accumulated from
+// zero in ascending slot order (the order of a sequential CPU sum).
+template <class TI, class TO, int N>
+__global__ void __launch_bounds__(256) k_dispatch_bwd(const TI* __restrict__ rows, int64_t in_stride,
+                                                      int64_t width, const int32_t* __restrict__ pos,
+                                                      int64_t T, int k, TO* __restrict__ out,
+                                                      int64_t out_stride) {
+  using A = typename AccOf<TI, TO>::type;
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  const int64_t packs = width / N;
+  for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < T; i += warps) {
+    // Row indices of this token's slots, one per lane (k <= 32), broadcast by
+    // shuffle; every lane runs the same number of pack iterations so the
+    // shuffles stay warp-uniform.
+    const int32_t my_r = lane < k ? pos[i * k + lane] : 0;
+    for (int64_t c0 = 0; c0 < packs; c0 += 32) {
+      const int64_t c = c0 + lane;
+      const bool act = c < packs;
+      A acc[N];
+#pragma unroll
+      for (int j = 0; j < N; ++j) acc[j] = 0;
+      for (int s = 0; s < k; ++s) {
+        const int64_t r = __shfl_sync(0xffffffffu, my_r, s);
+        if (act) {
+          A v[N];
+          Pack<TI, N>::load(rows + r * in_stride + c * N, v);
+#pragma unroll
+          for (int j = 0; j < N; ++j) acc[j] += v[j];
+        }
+      }
+      if (act) Pack<TO, N>::store(out + i * out_stride + c * N, acc);
+    }
+  }
+}
+
+// route backward: warp per token, softmax recomputed in the logit dtype with
+// the forward's recipe (max-subtract, exp, sum, divide).
+template <class F>
+__global__ void __launch_bounds__(256) k_route_bwd(const F* __restrict__ z, int64_t T, int E, int k,
+                                                   const int32_t* __restrict__ experts,
+                                                   const F* __restrict__ gp, F* __restrict__ gz) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < T; i += warps) {
+    const F* zr = z + i * E;
+    F m = -INFINITY;
+    for (int e = lane; e < E; e += 32) m = fmax(m, zr[e]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    F sum = 0;
+    for (int e = lane; e < E; e += 32) sum += exp(zr[e] - m);
+    sum = warp_sum(sum);
+    // S = sum_s g_s * P_{x_s}
+    F S = 0;
+    for (int s = lane; s < k; s += 32) S += gp[i * k + s] * (exp(zr[experts[i * k + s]] - m) / sum);
+    S = warp_sum(S);
+    for (int e = lane; e < E; e += 32) {
+      F G = 0;
+      for (int s = 0; s < k; ++s)
+        if (experts[i * k + s] == e) G = gp[i * k + s];
+      const F P = exp(zr[e] - m) / sum;
+      gz[i * E + e] = P * (G - S);
+    }
+  }
+}
+
+int grid_for(int64_t T) {
+  static int sms[16] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int& n = sms[dev & 15];
+  if (n == 0) {
+    n = 148;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  // 8 warps per CTA, up to 8 resident CTAs per SM; never more warps than tokens.
+  const int64_t want = (T + 7) / 8;
+  const int64_t cap = int64_t(n) * 8;
+  return int(want < cap ? (want < 1 ? 1 : want) : cap);
+}
+
+bool aligned16(const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15u) == 0; }
+
+template <class TG, class TY, class PT>
+cudaError_t launch_cbwd(const void* g, int64_t gs, const void* y, int64_t ys, int64_t w, const int32_t* pos,
+                        const void* p, int64_t T, int k, void* gy, int64_t gys, void* gp, cudaStream_t st) {
+  const bool vec = w % 8 == 0 && gs % 8 == 0 && ys % 8 == 0 && gys % 8 == 0 && aligned16(g) &&
+                   (!y || aligned16(y)) && (!gy || aligned16(gy));
+  const int grid = grid_for(T);
+  if (vec)
+    k_combine_bwd<TG, TY, PT, 8><<<grid, 256, 0, st>>>(
+        static_cast<const TG*>(g), gs, static_cast<const TY*>(y), ys, w, pos, static_cast<const PT*>(p), T, k,
+        static_cast<TY*>(gy), gys, static_cast<PT*>(gp));
+  else
+    k_combine_bwd<TG, TY, PT, 1><<<grid, 256, 0, st>>>(
+        static_cast<const TG*>(g), gs, static_cast<const TY*>(y), ys, w, pos, static_cast<const PT*>(p), T, k,
+        static_cast<TY*>(gy), gys, static_cast<PT*>(gp));
+  return cudaGetLastError();
+}
+
+template <class TG, class TY>
+cudaError_t cbwd_p(int pdt, const void* g, int64_t gs, const void* y, int64_t ys, int64_t w, const int32_t* pos,
+                   const void* p, int64_t T, int k, void* gy, int64_t gys, void* gp, cudaStream_t st) {
+  if (pdt == MOE_F64) return launch_cbwd<TG, TY, double>(g, gs, y, ys, w, pos, p, T, k, gy, gys, gp, st);
+  return launch_cbwd<TG, TY, float>(g, gs, y, ys, w, pos, p, T, k, gy, gys, gp, st);
+}
+
+template <class TG>
+cudaError_t cbwd_y(int ydt, int pdt, const void* g, int64_t gs, const void* y, int64_t ys, int64_t w,
+                   const int32_t* pos, const void* p, int64_t T, int k, void* gy, int64_t gys, void* gp,
+                   cudaStream_t st) {
+  switch (ydt) {
+    case MOE_F32: return cbwd_p<TG, float>(pdt, g, gs, y, ys, w, pos, p, T, k, gy, gys, gp, st);
+    case MOE_BF16: return cbwd_p<TG, __nv_bfloat16>(pdt, g, gs, y, ys, w, pos, p, T, k, gy, gys, gp, st);
+    case MOE_F16: return cbwd_p<TG, __half>(pdt, g, gs, y, ys, w, pos, p, T, k, gy, gys, gp, st);
+    default: return cbwd_p<TG, double>(pdt, g, gs, y, ys, w, pos, p, T, k, gy, gys, gp, st);
+  }
+}
+
+template <class TI, class TO>
+cudaError_t launch_dbwd(const void* in, int64_t is, int64_t w, const int32_t* pos, int64_t T, int k, void* out,
+                        int64_t os, cudaStream_t st) {
+  const bool vec = w % 8 == 0 && is % 8 == 0 && os % 8 == 0 && aligned16(in) && aligned16(out);
+  const int grid = grid_for(T);
+  if (vec)
+    k_dispatch_bwd<TI, TO, 8><<<grid, 256, 0, st>>>(static_cast<const TI*>(in), is, w, pos, T, k,
+                                                    static_cast<TO*>(out), os);
+  else
+    k_dispatch_bwd<TI, TO, 1><<<grid, 256, 0, st>>>(static_cast<const TI*>(in), is, w, pos, T, k,
+                                                    static_cast<TO*>(out), os);
+  return cudaGetLastError();
+}
+
+template <class TI>
+cudaError_t dbwd_o(int odt, const void* in, int64_t is, int64_t w, const int32_t* pos, int64_t T, int k,
+                   void* out, int64_t os, cudaStream_t st) {
+  switch (odt) {
+    case MOE_F32: return launch_dbwd<TI, float>(in, is, w, pos, T, k, out, os, st);
+    case MOE_BF16: return launch_dbwd<TI, __nv_bfloat16>(in, is, w, pos, T, k, out, os, st);
+    case MOE_F16: return launch_dbwd<TI, __half>(in, is, w, pos, T, k, out, os, st);
+    default: return launch_dbwd<TI, double>(in, is, w, pos, T, k, out, os, st);
+  }
+}
+
+bool float_dtype(int dt) { return dt == MOE_F32 || dt == MOE_BF16 || dt == MOE_F16 || dt == MOE_F64; }
+
+}  // namespace
+}  // namespace monta
+
+using namespace monta;
+
+extern "C" moe_status moe_combine_backward(const void* grad_out, int grad_dtype, int64_t grad_row_elems,
+                                           const void* y, int y_dtype, int64_t y_row_elems, int64_t width,
+                                           const int32_t* slot_pos, const void* probs, int probs_dtype,
+                                           int64_t T, int32_t k, void* grad_y, int64_t grad_y_row_elems,
+                                           void* grad_probs, void* stream) {
+  if (T < 0 || k < 1 || width < 0 || width > grad_row_elems || (y && width > y_row_elems) ||
+      (grad_y && width > grad_y_row_elems))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: bad geometry");
+  if (probs_dtype != MOE_F32 && probs_dtype != MOE_F64)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: probs must be f32 or f64");
+  if (!float_dtype(grad_dtype) || !float_dtype(y_dtype))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: gradient and expert rows must be f32/bf16/f16/f64");
+  if (grad_probs && !y)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: grad_probs needs the expert rows y");
+  if (T == 0 || (!grad_y && !grad_probs)) return MOE_OK;
+  if (!grad_out || !slot_pos || !probs) return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t err;
+  switch (grad_dtype) {
+    case MOE_F32:
+      err = cbwd_y<float>(y_dtype, probs_dtype, grad_out, grad_row_elems, y, y_row_elems, width, slot_pos, probs, T,
+                          k, grad_y, grad_y_row_elems, grad_probs, st);
+      break;
+    case MOE_BF16:
+      err = cbwd_y<__nv_bfloat16>(y_dtype, probs_dtype, grad_out, grad_row_elems, y, y_row_elems, width, slot_pos,
+                                  probs, T, k, grad_y, grad_y_row_elems, grad_probs, st);
+      break;
+    case MOE_F16:
+      err = cbwd_y<__half>(y_dtype, probs_dtype, grad_out, grad_row_elems, y, y_row_elems, width, slot_pos, probs,
+                           T, k, grad_y, grad_y_row_elems, grad_probs, st);
+      break;
+    default:
+      err = cbwd_y<double>(y_dtype, probs_dtype, grad_out, grad_row_elems, y, y_row_elems, width, slot_pos, probs,
+                           T, k, grad_y, grad_y_row_elems, grad_probs, st);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "combine_backward launch");
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_dispatch_backward(const void* grad_rows, int rows_dtype, int64_t row_elems, int64_t width,
+                                            const int32_t* slot_pos, int64_t T, int32_t k, void* grad_x,
+                                            int out_dtype, int64_t out_row_elems, void* stream) {
+  if (T < 0 || k < 1 || k > 32 || width < 0 || width > row_elems || width > out_row_elems)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_backward: bad geometry (1 <= k <= 32)");
+  if (!float_dtype(rows_dtype) || !float_dtype(out_dtype))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_backward: dtypes must be f32/bf16/f16/f64");
+  if (T == 0 || width == 0) return MOE_OK;
+  if (!grad_rows || !slot_pos || !grad_x) return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_backward: null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  cudaError_t err;
+  switch (rows_dtype) {
+    case MOE_F32: err = dbwd_o<float>(out_dtype, grad_rows, row_elems, width, slot_pos, T, k, grad_x, out_row_elems, st); break;
+    case MOE_BF16: err = dbwd_o<__nv_bfloat16>(out_dtype, grad_rows, row_elems, width, slot_pos, T, k, grad_x, out_row_elems, st); break;
+    case MOE_F16: err = dbwd_o<__half>(out_dtype, grad_rows, row_elems, width, slot_pos, T, k, grad_x, out_row_elems, st); break;
+    default: err = dbwd_o<double>(out_dtype, grad_rows, row_elems, width, slot_pos, T, k, grad_x, out_row_elems, st);
+  }
+  if (err != cudaSuccess) return cuda_fail(err, "dispatch_backward launch");
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_route_backward(const void* logits, int logit_dtype, int64_t T, int32_t E, int32_t k,
+                                         const int32_t* experts, const void* grad_probs, void* grad_logits,
+                                         void* stream) {
+  if (T < 0 || E < 1 || k < 1 || k > E) return fail(MOE_ERR_INVALID_ARGUMENT, "route_backward: need 1 <= k <= E");
+  if (logit_dtype != MOE_F32 && logit_dtype != MOE_F64)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "route_backward: logits must be f32 or f64");
+  if (T == 0) return MOE_OK;
+  if (!logits || !experts || !grad_probs || !grad_logits)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "route_backward: null pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(stream);
+  const int grid = grid_for(T);
+  if (logit_dtype == MOE_F64)
+    k_route_bwd<double><<<grid, 256, 0, st>>>(static_cast<const double*>(logits), T, E, k, experts,
+                                              static_cast<const double*>(grad_probs),
+                                              static_cast<double*>(grad_logits));
+  else
+    k_route_bwd<float><<<grid, 256, 0, st>>>(static_cast<const float*>(logits), T, E, k, experts,
+                                             static_cast<const float*>(grad_probs),
+                                             static_cast<float*>(grad_logits));
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return cuda_fail(err, "route_backward launch");
+  return MOE_OK;
+}

@@ -4,6 +4,7 @@
     build_index       dataplane::permute, index form (dataplane.hpp:118-140)
     permute_rows      gather-permute of rows (or a hidden_shard column slice)
     unpermute_combine weighted un-permute (dataplane.hpp:325-342)
+    combine_backward / dispatch_backward / route_backward   their adjoints
     host_empty        page-locked host tensor (moe_host_alloc) for forward_host
 
 All run on the current CUDA stream; nothing here synchronises unless
@@ -119,3 +120,62 @@ def unpermute_combine(y: torch.Tensor, slot_pos: torch.Tensor, probs: torch.Tens
                                             _lib.dtype_code(probs.dtype), T, k, out.data_ptr(),
                                             _lib.dtype_code(out.dtype), out.stride(0), _stream()))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Backward of the stateless ops (include/monta.h section 1b).
+
+def combine_backward(grad_out: torch.Tensor, y: torch.Tensor | None, slot_pos: torch.Tensor, probs: torch.Tensor,
+                     need_grad_y: bool = True, need_grad_probs: bool = True, num_rows: int | None = None):
+    """Adjoint of unpermute_combine.  Returns (grad_y [R, h] in y's dtype or
+    None, grad_probs [T, k] in probs' dtype or None)."""
+    grad_out = grad_out.contiguous()
+    T, h = grad_out.shape
+    k = slot_pos.shape[1]
+    slot_pos = slot_pos.contiguous()
+    if y is not None:
+        y = y.contiguous()
+        R, ydt = y.shape[0], y.dtype
+    else:
+        if need_grad_probs:
+            raise ValueError("combine_backward: grad_probs needs y")
+        R, ydt = (T * k if num_rows is None else num_rows), grad_out.dtype
+    probs = probs.contiguous()
+    grad_y = torch.empty((R, h), dtype=ydt, device=grad_out.device) if need_grad_y else None
+    grad_probs = torch.empty_like(probs) if need_grad_probs else None
+    check(_lib.load().moe_combine_backward(
+        grad_out.data_ptr(), _lib.dtype_code(grad_out.dtype), h,
+        y.data_ptr() if y is not None else None, _lib.dtype_code(ydt), h, h,
+        slot_pos.data_ptr(), probs.data_ptr(), _lib.dtype_code(probs.dtype), T, k,
+        grad_y.data_ptr() if grad_y is not None else None, h,
+        grad_probs.data_ptr() if grad_probs is not None else None, _stream()))
+    return grad_y, grad_probs
+
+
+def dispatch_backward(grad_rows: torch.Tensor, slot_pos: torch.Tensor, out_dtype: torch.dtype | None = None,
+                      out: torch.Tensor | None = None) -> torch.Tensor:
+    """Adjoint of the dispatch gather: grad_x[i] = sum_s grad_rows[slot_pos[i, s]]."""
+    grad_rows = grad_rows.contiguous()
+    R, h = grad_rows.shape
+    T, k = slot_pos.shape
+    slot_pos = slot_pos.contiguous()
+    if out is None:
+        out = torch.empty((T, h), dtype=out_dtype or grad_rows.dtype, device=grad_rows.device)
+    check(_lib.load().moe_dispatch_backward(grad_rows.data_ptr(), _lib.dtype_code(grad_rows.dtype), h, h,
+                                            slot_pos.data_ptr(), T, k, out.data_ptr(),
+                                            _lib.dtype_code(out.dtype), out.stride(0), _stream()))
+    return out
+
+
+def route_backward(logits: torch.Tensor, experts: torch.Tensor, grad_probs: torch.Tensor) -> torch.Tensor:
+    """Adjoint of route_topk with respect to the logits."""
+    logits = logits.contiguous()
+    T, E = logits.shape
+    k = experts.shape[1]
+    grad_logits = torch.empty_like(logits)
+    experts = experts.contiguous().to(torch.int32)
+    grad_probs = grad_probs.contiguous().to(logits.dtype)
+    check(_lib.load().moe_route_backward(logits.data_ptr(), _lib.dtype_code(logits.dtype), T, E, k,
+                                         experts.data_ptr(), grad_probs.data_ptr(), grad_logits.data_ptr(),
+                                         _stream()))
+    return grad_logits

@@ -1,0 +1,161 @@
+"""GPU checks of the backward kernels (include/monta.h section 1b, SURVEY.md
+§8(f) item 2) against plain PyTorch fp64/fp32 references of the same ops.
+
+The reference has no backward, so there is no oracle row for it; the bar is
+the forward's: index-exact placement, bit-exact where the arithmetic is a
+single rounding (grad_y = p * g) or a sequential fp32 sum (grad_x), and
+relative 1e-5 (fp32 arithmetic) for the dot products and the softmax
+adjoint, measured against fp64.
+"""
+import pytest
+import torch
+
+from paper_2411_00662_b200 import _lib
+from paper_2411_00662_b200 import autograd as mag
+from paper_2411_00662_b200 import ops
+
+pytestmark = pytest.mark.gpu
+
+
+def _index(T, E, k, seed, dev, logit_dtype=torch.float32):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    logits = torch.randn(T, E, generator=g, dtype=torch.float64).to(logit_dtype).to(dev)
+    experts, probs = ops.route_topk(logits, k)
+    return logits, experts, probs, ops.build_index(experts, E)
+
+
+def _rand(shape, dtype, seed, dev):
+    g = torch.Generator(device="cpu").manual_seed(seed)
+    return torch.randn(*shape, generator=g, dtype=torch.float64).to(dtype).to(dev)
+
+
+@pytest.mark.parametrize("T,h,E,k", [(300, 1000, 8, 2), (257, 1001, 8, 2), (1000, 256, 160, 6), (64, 40, 2, 1),
+                                     (33, 8, 4, 4)])
+@pytest.mark.parametrize("ydt,gdt,pdt", [(torch.float32, torch.float32, torch.float32),
+                                         (torch.bfloat16, torch.bfloat16, torch.float32),
+                                         (torch.bfloat16, torch.float32, torch.float32),
+                                         (torch.float16, torch.float16, torch.float32),
+                                         (torch.float64, torch.float64, torch.float64)])
+def test_combine_backward(cuda, T, h, E, k, ydt, gdt, pdt):
+    _, _, probs, idx = _index(T, E, k, seed=T + h, dev=cuda, logit_dtype=pdt)
+    R = T * k
+    y = _rand((R, h), ydt, 1, cuda)
+    g = _rand((T, h), gdt, 2, cuda)
+    gy, gp = ops.combine_backward(g, y, idx.slot_pos, probs)
+    torch.cuda.synchronize()
+    # grad_y: one multiply in the accumulation precision, one rounding to y's dtype.
+    acc = torch.float64 if torch.float64 in (ydt, gdt, pdt) else torch.float32
+    want = torch.empty((R, h), dtype=ydt, device=cuda)
+    for s in range(k):
+        want[idx.slot_pos[:, s].long()] = (probs[:, s:s + 1].to(acc) * g.to(acc)).to(ydt)
+    assert torch.equal(gy, want)
+    # grad_probs against fp64 dot products, relative to sum |g y|.
+    yr = y.double()[idx.slot_pos.long()]                      # [T, k, h]
+    ref = (g.double()[:, None, :] * yr).sum(-1)
+    mag_ = (g.double()[:, None, :] * yr).abs().sum(-1) + 1e-30
+    tol = 1e-12 if acc is torch.float64 else 1e-5
+    assert ((gp.double() - ref).abs() / mag_).max().item() < tol
+
+
+@pytest.mark.parametrize("T,h,E,k", [(300, 1000, 8, 2), (257, 1001, 8, 2), (1000, 256, 160, 6), (100, 64, 64, 32)])
+@pytest.mark.parametrize("idt,odt", [(torch.float32, torch.float32), (torch.bfloat16, torch.bfloat16),
+                                     (torch.bfloat16, torch.float32), (torch.float64, torch.float64)])
+def test_dispatch_backward_is_sequential_sum(cuda, T, h, E, k, idt, odt):
+    _, _, _, idx = _index(T, E, k, seed=7 * T + h, dev=cuda)
+    rows = _rand((T * k, h), idt, 3, cuda)
+    gx = ops.dispatch_backward(rows, idx.slot_pos, out_dtype=odt)
+    torch.cuda.synchronize()
+    acc = torch.float64 if torch.float64 in (idt, odt) else torch.float32
+    want = torch.zeros((T, h), dtype=acc, device=cuda)
+    for s in range(k):                                          # ascending slot order, as the kernel
+        want += rows[idx.slot_pos[:, s].long()].to(acc)
+    assert torch.equal(gx, want.to(odt))
+
+
+@pytest.mark.parametrize("T,E,k", [(2048, 8, 2), (8192, 2, 1), (1000, 160, 6), (77, 33, 3), (5, 4, 4)])
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_route_backward_matches_autograd(cuda, T, E, k, dtype):
+    logits, experts, _, _ = _index(T, E, k, seed=T + E, dev=cuda, logit_dtype=dtype)
+    gp = _rand((T, k), dtype, 4, cuda)
+    gz = ops.route_backward(logits, experts, gp)
+    torch.cuda.synchronize()
+    z = logits.double().clone().requires_grad_(True)
+    p = torch.softmax(z, dim=-1).gather(1, experts.long())
+    (p * gp.double()).sum().backward()
+    tol = 1e-12 if dtype is torch.float64 else 1e-5
+    assert (gz.double() - z.grad).abs().max().item() < tol
+
+
+def test_backward_empty_and_errors(cuda):
+    e = torch.empty((0, 2), dtype=torch.int32, device=cuda)
+    g = torch.empty((0, 16), dtype=torch.float32, device=cuda)
+    assert ops.dispatch_backward(torch.empty((0, 16), device=cuda), e).shape == (0, 16)
+    gy, gp = ops.combine_backward(g, torch.empty((0, 16), device=cuda), e, torch.empty((0, 2), device=cuda))
+    assert gy.shape == (0, 16) and gp.shape == (0, 2)
+    with pytest.raises(_lib.InvalidArgument):
+        ops.dispatch_backward(torch.zeros((33, 16), device=cuda), torch.zeros((1, 33), dtype=torch.int32,
+                                                                                 device=cuda))
+    with pytest.raises(_lib.InvalidArgument):
+        ops.route_backward(torch.zeros((4, 2), device=cuda), torch.zeros((4, 3), dtype=torch.int32, device=cuda),
+                           torch.zeros((4, 3), device=cuda))
+
+
+def _torch_layer(x, logits, k, experts_w):
+    """Plain fp64 PyTorch MoE layer with the reference's routing (stable top-k
+    on raw scores, unrenormalised softmax probs)."""
+    p_all = torch.softmax(logits, dim=-1)
+    order = torch.sort(logits.detach(), dim=-1, descending=True, stable=True).indices[:, :k]
+    sel = torch.sort(order, dim=-1).values
+    probs = p_all.gather(1, sel)
+    out = torch.zeros_like(x)
+    for s in range(k):
+        ys = torch.einsum("th,thd->td", x, experts_w[sel[:, s]])
+        out = out + probs[:, s:s + 1] * ys
+    return out
+
+
+@pytest.mark.parametrize("T,h,E,k", [(256, 64, 8, 2), (128, 32, 16, 4)])
+def test_layer_gradients_match_torch(cuda, T, h, E, k):
+    x0 = _rand((T, h), torch.float32, 10, cuda)
+    z0 = _rand((T, E), torch.float32, 11, cuda)
+    w0 = _rand((E, h, h), torch.float32, 12, cuda) / h ** 0.5
+    gout = _rand((T, h), torch.float32, 13, cuda)
+
+    x, z, w = (t.clone().requires_grad_(True) for t in (x0, z0, w0))
+
+    def experts_fn(rows, index):
+        offs = index.expert_offsets.tolist()
+        return torch.cat([rows[offs[e]:offs[e + 1]] @ w[e] for e in range(E)])
+
+    out = mag.moe_local(x, z, k, E, experts_fn)
+    (out * gout).sum().backward()
+
+    xr, zr, wr = (t.double().clone().requires_grad_(True) for t in (x0, z0, w0))
+    ref = _torch_layer(xr, zr, k, wr)
+    (ref * gout.double()).sum().backward()
+    torch.cuda.synchronize()
+    for got, want in ((out, ref), (x.grad, xr.grad), (z.grad, zr.grad), (w.grad, wr.grad)):
+        scale = want.abs().max().item() + 1e-30
+        assert (got.double() - want).abs().max().item() / scale < 1e-4
+
+
+def test_full_size_deepseek_adjoint_properties(cuda):
+    """DeepSeek-V2 layer size (T=8192, h=5120, E=160, top-6, bf16): dispatch
+    backward of the dispatched rows is exactly k*x (small integer multiples
+    of a bf16 value are exact in fp32), and combine backward with y = the
+    dispatched rows gives grad_probs[i, s] = <g_i, x_i> for every slot."""
+    T, h, E, k = 8192, 5120, 160, 6
+    _, _, probs, idx = _index(T, E, k, seed=5, dev=cuda)
+    x = _rand((T, h), torch.bfloat16, 6, cuda)
+    rows = ops.permute_rows(x, idx.perm_src)
+    gx = ops.dispatch_backward(rows, idx.slot_pos)
+    torch.cuda.synchronize()
+    assert torch.equal(gx, (k * x.float()).to(torch.bfloat16))
+    g = _rand((T, h), torch.bfloat16, 7, cuda)
+    gy, gp = ops.combine_backward(g, rows, idx.slot_pos, probs)
+    torch.cuda.synchronize()
+    ref = (g.double() * x.double()).sum(-1, keepdim=True).expand(T, k)
+    mag_ = (g.double() * x.double()).abs().sum(-1, keepdim=True)
+    assert ((gp.double() - ref).abs() / mag_).max().item() < 1e-5
+    # grad_y rows land exactly where the forward put the token's rows.
+    assert torch.equal(gy[idx.slot_pos[:, 0].long()], (probs[:, :1] * g.float()).to(torch.bfloat16))
