@@ -144,7 +144,7 @@ moe_status moe_unpermute_combine(const void* y, int y_dtype, int64_t y_row_elems
  *   grad_probs[i,s]                = sum_q grad_out[i,q] * y[slot_pos[i,s], q]  (probs' dtype)
  * fp32 arithmetic (fp64 if any operand is f64).  grad_y or grad_probs may be
  * NULL to skip that output; grad_probs needs y.  Dtypes: grad_out and y
- * f32/bf16/f16/f64, probs f32/f64. */
+ * f32/bf16/f16/f64, probs f32/f64.  1 <= k <= 64. */
 moe_status moe_combine_backward(const void* grad_out, int grad_dtype, int64_t grad_row_elems,
                                 const void* y, int y_dtype, int64_t y_row_elems, int64_t width,
                                 const int32_t* slot_pos, const void* probs, int probs_dtype,
@@ -154,7 +154,7 @@ moe_status moe_combine_backward(const void* grad_out, int grad_dtype, int64_t gr
 /* Adjoint of the dispatch gather (moe_permute_rows through slot_pos):
  *   grad_x[i, 0:width) = sum_s grad_rows[slot_pos[i,s], 0:width)
  * accumulated from zero in ascending slot order, fp32 (fp64 if f64).
- * 1 <= k <= 32. */
+ * 1 <= k <= 64. */
 moe_status moe_dispatch_backward(const void* grad_rows, int rows_dtype, int64_t row_elems, int64_t width,
                                  const int32_t* slot_pos, int64_t T, int32_t k, void* grad_x,
                                  int out_dtype, int64_t out_row_elems, void* stream);

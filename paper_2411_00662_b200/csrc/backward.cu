@@ -17,7 +17,8 @@
 // weighted gradient rows, dispatch backward = combine's reverse AllToAll); the
 // kernels here are the per-card compute either side of them.
 //
-// All three are HBM-bound streaming kernels: one warp per token, 8-element
+// All three are HBM-bound streaming kernels (CTA per token for the row
+// kernels, warp per token for the router), 8-element
 // packs moved with 16-byte vector accesses (bf16/f16: one int4, f32: two,
 // f64: four), fp32 accumulation (fp64 for f64), no atomics: every output
 // element has exactly one writer.
@@ -50,6 +51,21 @@ template <> __device__ __forceinline__ float cvt_out<float, double>(double v) { 
 // caller guaranteed alignment; N == 1 is the scalar fallback.
 template <class T, int N> struct Pack {
   static_assert(N == 1 || N == 8, "pack of 1 or 8");
+  static constexpr int kVec = N == 8 ? int(8 * sizeof(T) / 16) : 1;  // int4 accesses per pack of 8
+  // A pack as loaded (kept in this form while other loads are in flight, so
+  // the in-flight registers are the bytes, not their fp32 expansion).
+  union Raw {
+    int4 v[kVec];
+    T e[N];
+  };
+  __device__ __forceinline__ static void load_raw(const T* p, Raw& r) {
+    if constexpr (N == 1) {
+      r.e[0] = *p;
+    } else {
+#pragma unroll
+      for (int j = 0; j < kVec; ++j) r.v[j] = ld_stream(reinterpret_cast<const int4*>(p) + j);
+    }
+  }
   template <class A> __device__ __forceinline__ static void load(const T* p, A* out) {
     if constexpr (N == 1) {
       out[0] = cvt_in<A>(*p);
@@ -84,47 +100,107 @@ template <class A> __device__ __forceinline__ A warp_sum(A v) {
 
 template <class P> __device__ __forceinline__ double load_p(const P* p) { return double(*p); }
 
-// combine backward: warp per token; for each slot the warp streams the
-// token's gradient row (L1/L2 after the first slot) and the expert output
-// row, writes p * grad into the expert-gradient row and reduces the dot
-// product for grad_probs.
+// Both streaming kernels give each token to one CTA whose threads split its
+// row: thread t owns packs t, t + blockDim.x, ...  and keeps unroll_for() of
+// them in flight.  The host sizes the CTA so that every round is full (the
+// fewest rounds of <= 160 threads, then the fewest warps covering the row in
+// that many rounds: Mixtral 128, DeepSeek 160, 2x70B 128 threads x 2
+// rounds), and small layers (toy: T = 2048) still spread over the SMs.
+constexpr int kMaxThreads = 256;
+constexpr int kSizingThreads = 160;
+constexpr int kMaxSlots = 64;  // combine backward keeps per-slot partial dots in shared memory
+
+// Packs in flight per thread and stream: 64 bytes (4 for 16-bit types, 2 for
+// f32, 1 for f64), so the raw in-flight bytes fit the register budget of
+// 16 resident CTAs per SM.
+template <class T, int N> __host__ __device__ constexpr int unroll_for() { return N == 1 ? 4 : int(64 / (8 * sizeof(T))); }
+template <class TG, class TY, int N> __host__ __device__ constexpr int combine_unroll() {
+  return unroll_for<TG, N>() < unroll_for<TY, N>() ? unroll_for<TG, N>() : unroll_for<TY, N>();
+}
+
+inline int block_for(int64_t packs, int unroll) {
+  // Fewest rounds of at most 160 threads, then the fewest whole warps that
+  // cover the row in that many rounds.
+  const int64_t per_round = int64_t(kSizingThreads) * unroll;
+  const int64_t rounds = packs <= 0 ? 1 : (packs + per_round - 1) / per_round;
+  int64_t t = (packs + unroll * rounds - 1) / (unroll * rounds);
+  t = (t + 31) / 32 * 32;
+  return int(t < 32 ? 32 : (t > kMaxThreads ? kMaxThreads : t));
+}
+
+// combine backward: per round the CTA loads its slice of the token's
+// gradient row once into registers, then for each slot streams the expert
+// output row, writes p * grad into the expert-gradient row and reduces the
+// dot product for grad_probs in a fixed order (lanes, then rounds, then
+// warps): deterministic, no atomics.  Every thread runs the same number of
+// rounds so the warp reductions inside them stay converged.
 template <class TG, class TY, class PT, int N>
-__global__ void __launch_bounds__(256) k_combine_bwd(const TG* __restrict__ g, int64_t g_stride,
-                                                     const TY* __restrict__ y, int64_t y_stride,
-                                                     int64_t width, const int32_t* __restrict__ pos,
-                                                     const PT* __restrict__ probs, int64_t T, int k,
-                                                     TY* __restrict__ gy, int64_t gy_stride,
-                                                     PT* __restrict__ gp) {
+__global__ void __launch_bounds__(kMaxThreads) k_combine_bwd(const TG* __restrict__ g, int64_t g_stride,
+                                                          const TY* __restrict__ y, int64_t y_stride,
+                                                          int64_t width, const int32_t* __restrict__ pos,
+                                                          const PT* __restrict__ probs, int64_t T, int k,
+                                                          TY* __restrict__ gy, int64_t gy_stride,
+                                                          PT* __restrict__ gp) {
   using A = typename AccOf<TG, TY, PT>::type;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  using PG = Pack<TG, N>;
+  using PY = Pack<TY, N>;
+  constexpr int U = combine_unroll<TG, TY, N>();
+  __shared__ A part[kMaxSlots][kMaxThreads / 32];
+  const int warps = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t packs = width / N;
-  for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < T; i += warps) {
+  const int64_t step = int64_t(blockDim.x) * U;
+  for (int64_t i = blockIdx.x; i < T; i += gridDim.x) {
     const TG* grow = g + i * g_stride;
-    for (int s = 0; s < k; ++s) {
-      const int64_t r = pos[i * k + s];
-      const A p = A(load_p(probs + i * k + s));
-      A dot = 0;
-      for (int64_t c = lane; c < packs; c += 32) {
-        A gv[N];
-        Pack<TG, N>::load(grow + c * N, gv);
+    for (int64_t base = 0; base < packs; base += step) {
+      typename PG::Raw gv[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = base + threadIdx.x + int64_t(u) * blockDim.x;
+        if (c < packs) PG::load_raw(grow + c * N, gv[u]);
+      }
+      for (int s = 0; s < k; ++s) {
+        const int64_t r = pos[i * k + s];
+        const A p = A(load_p(probs + i * k + s));
+        A dot = 0;
+        typename PY::Raw yv[U];
         if (gp) {
-          A yv[N];
-          Pack<TY, N>::load(y + r * y_stride + c * N, yv);
 #pragma unroll
-          for (int j = 0; j < N; ++j) dot += gv[j] * yv[j];
+          for (int u = 0; u < U; ++u) {
+            const int64_t c = base + threadIdx.x + int64_t(u) * blockDim.x;
+            if (c < packs) PY::load_raw(y + r * y_stride + c * N, yv[u]);
+          }
         }
-        if (gy) {
-          A ov[N];
 #pragma unroll
-          for (int j = 0; j < N; ++j) ov[j] = p * gv[j];
-          Pack<TY, N>::store(gy + r * gy_stride + c * N, ov);
+        for (int u = 0; u < U; ++u) {
+          const int64_t c = base + threadIdx.x + int64_t(u) * blockDim.x;
+          if (c < packs) {
+            if (gp) {
+#pragma unroll
+              for (int j = 0; j < N; ++j) dot += cvt_in<A>(gv[u].e[j]) * cvt_in<A>(yv[u].e[j]);
+            }
+            if (gy) {
+              A ov[N];
+#pragma unroll
+              for (int j = 0; j < N; ++j) ov[j] = p * cvt_in<A>(gv[u].e[j]);
+              PY::store(gy + r * gy_stride + c * N, ov);
+            }
+          }
+        }
+        if (gp) {
+          dot = warp_sum(dot);
+          if (lane == 0) part[s][warp] = base == 0 ? dot : part[s][warp] + dot;
         }
       }
-      if (gp) {
-        dot = warp_sum(dot);
-        if (lane == 0) gp[i * k + s] = PT(dot);
+    }
+    if (gp) {
+      __syncthreads();
+      if (threadIdx.x < k) {
+        A sum = 0;
+        for (int w = 0; w < warps; ++w) sum += part[threadIdx.x][w];
+        gp[i * k + threadIdx.x] = PT(sum);
       }
+      __syncthreads();  // part[] is reused by the next token
     }
   }
 }
@@ -132,35 +208,39 @@ __global__ void __launch_bounds__(256) k_combine_bwd(const TG* __restrict__ g, i
 // dispatch backward: grad_x[i] = sum_s grad_rows[pos[i,s]], accumulated from
 // zero in ascending slot order (the order of a sequential CPU sum).
 template <class TI, class TO, int N>
-__global__ void __launch_bounds__(256) k_dispatch_bwd(const TI* __restrict__ rows, int64_t in_stride,
-                                                      int64_t width, const int32_t* __restrict__ pos,
-                                                      int64_t T, int k, TO* __restrict__ out,
-                                                      int64_t out_stride) {
+__global__ void __launch_bounds__(kMaxThreads) k_dispatch_bwd(const TI* __restrict__ rows, int64_t in_stride,
+                                                           int64_t width, const int32_t* __restrict__ pos,
+                                                           int64_t T, int k, TO* __restrict__ out,
+                                                           int64_t out_stride) {
   using A = typename AccOf<TI, TO>::type;
-  const int lane = threadIdx.x & 31;
-  const int64_t warps = int64_t(gridDim.x) * (blockDim.x >> 5);
+  using PI = Pack<TI, N>;
+  constexpr int U = unroll_for<TI, N>();
   const int64_t packs = width / N;
-  for (int64_t i = int64_t(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < T; i += warps) {
-    // Row indices of this token's slots, one per lane (k <= 32), broadcast by
-    // shuffle; every lane runs the same number of pack iterations so the
-    // shuffles stay warp-uniform.
-    const int32_t my_r = lane < k ? pos[i * k + lane] : 0;
-    for (int64_t c0 = 0; c0 < packs; c0 += 32) {
-      const int64_t c = c0 + lane;
-      const bool act = c < packs;
-      A acc[N];
+  for (int64_t i = blockIdx.x; i < T; i += gridDim.x) {
+    for (int64_t c0 = threadIdx.x; c0 < packs; c0 += int64_t(blockDim.x) * U) {
+      A acc[U][N];
 #pragma unroll
-      for (int j = 0; j < N; ++j) acc[j] = 0;
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[u][j] = 0;
       for (int s = 0; s < k; ++s) {
-        const int64_t r = __shfl_sync(0xffffffffu, my_r, s);
-        if (act) {
-          A v[N];
-          Pack<TI, N>::load(rows + r * in_stride + c * N, v);
+        const int64_t r = pos[i * k + s];
+        typename PI::Raw v[U];
 #pragma unroll
-          for (int j = 0; j < N; ++j) acc[j] += v[j];
+        for (int u = 0; u < U; ++u) {
+          const int64_t c = c0 + int64_t(u) * blockDim.x;
+          if (c < packs) PI::load_raw(rows + r * in_stride + c * N, v[u]);
         }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int j = 0; j < N; ++j) acc[u][j] += cvt_in<A>(v[u].e[j]);
       }
-      if (act) Pack<TO, N>::store(out + i * out_stride + c * N, acc);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t c = c0 + int64_t(u) * blockDim.x;
+        if (c < packs) Pack<TO, N>::store(out + i * out_stride + c * N, acc[u]);
+      }
     }
   }
 }
@@ -196,7 +276,7 @@ __global__ void __launch_bounds__(256) k_route_bwd(const F* __restrict__ z, int6
   }
 }
 
-int grid_for(int64_t T) {
+int sm_count() {
   static int sms[16] = {0};
   int dev = 0;
   cudaGetDevice(&dev);
@@ -205,9 +285,19 @@ int grid_for(int64_t T) {
     n = 148;
     cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   }
-  // 8 warps per CTA, up to 8 resident CTAs per SM; never more warps than tokens.
+  return n;
+}
+
+// Streaming kernels: one CTA per token, at most 16 resident CTAs per SM.
+int stream_grid(int64_t T) {
+  const int64_t cap = int64_t(sm_count()) * 16;
+  return int(T < cap ? (T < 1 ? 1 : T) : cap);
+}
+
+// Warp-per-token kernels (route backward): 8 warps per CTA, up to 8 CTAs per SM.
+int grid_for(int64_t T) {
   const int64_t want = (T + 7) / 8;
-  const int64_t cap = int64_t(n) * 8;
+  const int64_t cap = int64_t(sm_count()) * 8;
   return int(want < cap ? (want < 1 ? 1 : want) : cap);
 }
 
@@ -218,13 +308,14 @@ cudaError_t launch_cbwd(const void* g, int64_t gs, const void* y, int64_t ys, in
                         const void* p, int64_t T, int k, void* gy, int64_t gys, void* gp, cudaStream_t st) {
   const bool vec = w % 8 == 0 && gs % 8 == 0 && ys % 8 == 0 && gys % 8 == 0 && aligned16(g) &&
                    (!y || aligned16(y)) && (!gy || aligned16(gy));
-  const int grid = grid_for(T);
+  const int grid = stream_grid(T);
+  const int block = vec ? block_for(w / 8, combine_unroll<TG, TY, 8>()) : block_for(w, combine_unroll<TG, TY, 1>());
   if (vec)
-    k_combine_bwd<TG, TY, PT, 8><<<grid, 256, 0, st>>>(
+    k_combine_bwd<TG, TY, PT, 8><<<grid, block, 0, st>>>(
         static_cast<const TG*>(g), gs, static_cast<const TY*>(y), ys, w, pos, static_cast<const PT*>(p), T, k,
         static_cast<TY*>(gy), gys, static_cast<PT*>(gp));
   else
-    k_combine_bwd<TG, TY, PT, 1><<<grid, 256, 0, st>>>(
+    k_combine_bwd<TG, TY, PT, 1><<<grid, block, 0, st>>>(
         static_cast<const TG*>(g), gs, static_cast<const TY*>(y), ys, w, pos, static_cast<const PT*>(p), T, k,
         static_cast<TY*>(gy), gys, static_cast<PT*>(gp));
   return cudaGetLastError();
@@ -253,12 +344,13 @@ template <class TI, class TO>
 cudaError_t launch_dbwd(const void* in, int64_t is, int64_t w, const int32_t* pos, int64_t T, int k, void* out,
                         int64_t os, cudaStream_t st) {
   const bool vec = w % 8 == 0 && is % 8 == 0 && os % 8 == 0 && aligned16(in) && aligned16(out);
-  const int grid = grid_for(T);
+  const int grid = stream_grid(T);
+  const int block = vec ? block_for(w / 8, unroll_for<TI, 8>()) : block_for(w, unroll_for<TI, 1>());
   if (vec)
-    k_dispatch_bwd<TI, TO, 8><<<grid, 256, 0, st>>>(static_cast<const TI*>(in), is, w, pos, T, k,
+    k_dispatch_bwd<TI, TO, 8><<<grid, block, 0, st>>>(static_cast<const TI*>(in), is, w, pos, T, k,
                                                     static_cast<TO*>(out), os);
   else
-    k_dispatch_bwd<TI, TO, 1><<<grid, 256, 0, st>>>(static_cast<const TI*>(in), is, w, pos, T, k,
+    k_dispatch_bwd<TI, TO, 1><<<grid, block, 0, st>>>(static_cast<const TI*>(in), is, w, pos, T, k,
                                                     static_cast<TO*>(out), os);
   return cudaGetLastError();
 }
@@ -286,9 +378,9 @@ extern "C" moe_status moe_combine_backward(const void* grad_out, int grad_dtype,
                                            const int32_t* slot_pos, const void* probs, int probs_dtype,
                                            int64_t T, int32_t k, void* grad_y, int64_t grad_y_row_elems,
                                            void* grad_probs, void* stream) {
-  if (T < 0 || k < 1 || width < 0 || width > grad_row_elems || (y && width > y_row_elems) ||
+  if (T < 0 || k < 1 || k > kMaxSlots || width < 0 || width > grad_row_elems || (y && width > y_row_elems) ||
       (grad_y && width > grad_y_row_elems))
-    return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: bad geometry");
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: bad geometry (1 <= k <= 64)");
   if (probs_dtype != MOE_F32 && probs_dtype != MOE_F64)
     return fail(MOE_ERR_INVALID_ARGUMENT, "combine_backward: probs must be f32 or f64");
   if (!float_dtype(grad_dtype) || !float_dtype(y_dtype))
@@ -323,8 +415,8 @@ extern "C" moe_status moe_combine_backward(const void* grad_out, int grad_dtype,
 extern "C" moe_status moe_dispatch_backward(const void* grad_rows, int rows_dtype, int64_t row_elems, int64_t width,
                                             const int32_t* slot_pos, int64_t T, int32_t k, void* grad_x,
                                             int out_dtype, int64_t out_row_elems, void* stream) {
-  if (T < 0 || k < 1 || k > 32 || width < 0 || width > row_elems || width > out_row_elems)
-    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_backward: bad geometry (1 <= k <= 32)");
+  if (T < 0 || k < 1 || k > kMaxSlots || width < 0 || width > row_elems || width > out_row_elems)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_backward: bad geometry (1 <= k <= 64)");
   if (!float_dtype(rows_dtype) || !float_dtype(out_dtype))
     return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_backward: dtypes must be f32/bf16/f16/f64");
   if (T == 0 || width == 0) return MOE_OK;

@@ -56,9 +56,9 @@ def test_errors_map_to_exceptions_without_gpu():
 def test_backward_entry_points_validate_without_gpu():
     lib = _lib.load()
     assert lib.moe_route_backward(None, _lib.F32, 4, 2, 3, None, None, None, None) == _lib.ERR_INVALID_ARGUMENT
-    assert lib.moe_dispatch_backward(None, _lib.F32, 16, 16, None, 4, 33, None, _lib.F32, 16, None) \
+    assert lib.moe_dispatch_backward(None, _lib.F32, 16, 16, None, 4, 65, None, _lib.F32, 16, None) \
         == _lib.ERR_INVALID_ARGUMENT
-    assert b"k <= 32" in lib.moe_last_error()
+    assert b"k <= 64" in lib.moe_last_error()
     assert lib.moe_combine_backward(None, _lib.F32, 16, None, _lib.F32, 16, 16, None, None, _lib.F32, 4, 2,
                                     None, 16, C.c_void_p(1), None) == _lib.ERR_INVALID_ARGUMENT
     assert b"needs the expert rows" in lib.moe_last_error()

@@ -30,7 +30,7 @@ def _rand(shape, dtype, seed, dev):
 
 
 @pytest.mark.parametrize("T,h,E,k", [(300, 1000, 8, 2), (257, 1001, 8, 2), (1000, 256, 160, 6), (64, 40, 2, 1),
-                                     (33, 8, 4, 4)])
+                                     (33, 8, 4, 4), (5, 4104, 80, 32), (2, 9000, 8, 3)])
 @pytest.mark.parametrize("ydt,gdt,pdt", [(torch.float32, torch.float32, torch.float32),
                                          (torch.bfloat16, torch.bfloat16, torch.float32),
                                          (torch.bfloat16, torch.float32, torch.float32),
@@ -57,7 +57,7 @@ def test_combine_backward(cuda, T, h, E, k, ydt, gdt, pdt):
     assert ((gp.double() - ref).abs() / mag_).max().item() < tol
 
 
-@pytest.mark.parametrize("T,h,E,k", [(300, 1000, 8, 2), (257, 1001, 8, 2), (1000, 256, 160, 6), (100, 64, 64, 32)])
+@pytest.mark.parametrize("T,h,E,k", [(300, 1000, 8, 2), (257, 1001, 8, 2), (1000, 256, 160, 6), (100, 64, 64, 32), (3, 4104, 80, 31)])
 @pytest.mark.parametrize("idt,odt", [(torch.float32, torch.float32), (torch.bfloat16, torch.bfloat16),
                                      (torch.bfloat16, torch.float32), (torch.float64, torch.float64)])
 def test_dispatch_backward_is_sequential_sum(cuda, T, h, E, k, idt, odt):
@@ -93,7 +93,7 @@ def test_backward_empty_and_errors(cuda):
     gy, gp = ops.combine_backward(g, torch.empty((0, 16), device=cuda), e, torch.empty((0, 2), device=cuda))
     assert gy.shape == (0, 16) and gp.shape == (0, 2)
     with pytest.raises(_lib.InvalidArgument):
-        ops.dispatch_backward(torch.zeros((33, 16), device=cuda), torch.zeros((1, 33), dtype=torch.int32,
+        ops.dispatch_backward(torch.zeros((65, 16), device=cuda), torch.zeros((1, 65), dtype=torch.int32,
                                                                                  device=cuda))
     with pytest.raises(_lib.InvalidArgument):
         ops.route_backward(torch.zeros((4, 2), device=cuda), torch.zeros((4, 3), dtype=torch.int32, device=cuda),
