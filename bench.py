@@ -268,6 +268,59 @@ def run_reference(args):
 
 
 # ---------------------------------------------------------------------------
+def backward_kernels(T, h, E, k, cold_l2, peak, iters=10):
+    """SURVEY §8(f) item 2 at the workload's size, outside the timed region:
+    the three backward kernels (ops.*_backward) each timed alone with CUDA
+    events after a cold-L2 flush, median of `iters`, with their algorithmic
+    HBM bytes (scripts/micro/backward_bench.py has the per-kernel formulas)."""
+    from paper_2411_00662_b200 import _lib, ops
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dt = payload_dtype()
+    b = ELEM
+    gen = torch.Generator(device="cpu").manual_seed(7)
+    logits = torch.randn(T, E, generator=gen).to(dev)
+    experts, probs = ops.route_topk(logits, k)
+    idx = ops.build_index(experts, E)
+    R = T * k
+    y = torch.randn(R, h, generator=gen).to(dt).to(dev)
+    g = torch.randn(T, h, generator=gen).to(dt).to(dev)
+    gy, gp, gx, gz = torch.empty_like(y), torch.empty_like(probs), torch.empty_like(g), torch.empty_like(logits)
+    lib, dc, sp = _lib.load(), _lib.dtype_code(dt), idx.slot_pos
+
+    def st():
+        return torch.cuda.current_stream().cuda_stream
+
+    runs = {
+        "combine_backward": (lambda: _lib.check(lib.moe_combine_backward(
+            g.data_ptr(), dc, h, y.data_ptr(), dc, h, h, sp.data_ptr(), probs.data_ptr(), _lib.F32, T, k,
+            gy.data_ptr(), h, gp.data_ptr(), st())), T * h * b + 2 * R * h * b + 12 * R),
+        "dispatch_backward": (lambda: _lib.check(lib.moe_dispatch_backward(
+            y.data_ptr(), dc, h, h, sp.data_ptr(), T, k, gx.data_ptr(), dc, h, st())), R * h * b + T * h * b + 4 * R),
+        "route_backward": (lambda: _lib.check(lib.moe_route_backward(
+            logits.data_ptr(), _lib.F32, T, E, k, experts.data_ptr(), probs.data_ptr(), gz.data_ptr(), st())),
+            8 * T * E + 8 * R),
+    }
+    out = {}
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for name, (fn, nbytes) in runs.items():
+        fn()
+        ts = []
+        for _ in range(iters):
+            cold_l2()
+            torch.cuda.synchronize()
+            ev0.record()
+            fn()
+            ev1.record()
+            torch.cuda.synchronize()
+            ts.append(ev0.elapsed_time(ev1) * 1e3)
+        us = sorted(ts)[len(ts) // 2]
+        out[name] = {"us": us, "bytes": nbytes, "gbs": nbytes / us / 1e3, "frac": nbytes / us / 1e3 / peak}
+    out["sum_us"] = sum(v["us"] for v in out.values() if isinstance(v, dict))
+    out["note"] = ("per-card adjoints of combine/dispatch/route (include/monta.h 1b), C-ABI calls into "
+                   "preallocated buffers; cold L2; each timed alone, outside the bench's timed region")
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -624,6 +677,10 @@ def main():
                "sample": f"{reps} full layers ({T} tokens, {secs:.1f} s CPU); oracle/moe_oracle.c "
                          f"route+permute+dispatch+combine, 1 thread of {os.cpu_count()} host threads"}
 
+    backward = None
+    if world == 1 and not args.quick:
+        backward = backward_kernels(T, h, E, k, cold_l2, peak)
+
     line = {"metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic (randn x, randn f32 gate logits)",
@@ -638,7 +695,7 @@ def main():
             "naive": naive,
             "pipelined": pipelined,
             "skewed": skewed,
-            "nvlink": nvlink, "check_max_rel_err": err}
+            "nvlink": nvlink, "check_max_rel_err": err, "backward": backward}
     if rank == 0:
         print(json.dumps(line), flush=True)
     layer.close()

@@ -102,14 +102,17 @@ extern "C" moe_status moe_unpermute_combine(const void* y, int y_dtype, int64_t 
   a.out[0] = static_cast<char*>(out);
   a.wait.n = 0;
   a.sig.n = 0;
-  static int32_t* scratch = nullptr;
-  if (!scratch) {
-    cudaError_t e = cudaMalloc(&scratch, 16);
-    if (e != cudaSuccess) return cuda_fail(e, "unpermute_combine scratch");
-  }
-  a.err = scratch;
+  // Device-side error word, one per device (the stateless op runs on the
+  // caller's current device).
+  static int32_t* scratch[64] = {nullptr};
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
+  if (dev < 0 || dev >= 64) return fail(MOE_ERR_UNSUPPORTED, "unpermute_combine: device ordinal >= 64");
+  if (!scratch[dev]) {
+    cudaError_t e = cudaMalloc(&scratch[dev], 16);
+    if (e != cudaSuccess) return cuda_fail(e, "unpermute_combine scratch");
+  }
+  a.err = scratch[dev];
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int grid = sms;  // SM budget: the launcher sizes the grid per kernel
   bool ok = true;
