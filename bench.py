@@ -273,6 +273,8 @@ def backward_kernels(T, h, E, k, cold_l2, peak, iters=10):
     the three backward kernels (ops.*_backward) each timed alone with CUDA
     events after a cold-L2 flush, median of `iters`, with their algorithmic
     HBM bytes (scripts/micro/backward_bench.py has the per-kernel formulas)."""
+    import torch
+
     from paper_2411_00662_b200 import _lib, ops
     dev = torch.device("cuda", torch.cuda.current_device())
     dt = payload_dtype()
@@ -679,7 +681,10 @@ def main():
 
     backward = None
     if world == 1 and not args.quick:
-        backward = backward_kernels(T, h, E, k, cold_l2, peak)
+        try:
+            backward = backward_kernels(T, h, E, k, cold_l2, peak)
+        except Exception as exc:  # the backward figures are extra; never lose the bench line to them
+            backward = {"error": f"{type(exc).__name__}: {exc}"}
 
     line = {"metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "weak",
