@@ -22,8 +22,9 @@ context (cd.experts / cd.probs / cd.slot_pos untouched):
 Expert outputs are taken to be consistent across the t cards of a node (each
 card's combine leg reads its own column slice of them), which is what the
 forward combine assumes.  Only the per-row metadata (probabilities, slots,
-partial dots: a few bytes per routed pair) moves through torch.distributed;
-every row of payload moves through the library's kernels.
+partial dots: a few bytes per routed pair) moves through torch.distributed
+collectives on the device; every row of payload moves through the library's
+kernels.
 """
 from __future__ import annotations
 
@@ -97,10 +98,19 @@ def combine_backward(layer: MoeLayer, grad_out: dict, expert_out: dict, level: i
         parts.append(torch.stack([src.to(dot.dtype), pos.to(dot.dtype), slot.to(dot.dtype), dot], dim=1))
     part = torch.cat(parts) if parts else torch.empty((0, 4), dtype=layer.logit_dtype)
     if layer.world_size > 1:
+        # device-side all-gather of the (source, position, slot, partial) rows,
+        # padded to the largest card's row count (padding rows carry 0)
         import torch.distributed as dist
-        allp = [None] * layer.world_size
-        dist.all_gather_object(allp, part.cpu())
-        part = torch.cat(allp).to(ex_all.device)
+        part = part.to(ex_all.device)
+        cnt = torch.tensor([part.shape[0]], dtype=torch.int64, device=part.device)
+        cnts = [torch.empty_like(cnt) for _ in range(layer.world_size)]
+        dist.all_gather(cnts, cnt)
+        cnts = [int(v.item()) for v in cnts]
+        pad = torch.zeros((max(cnts), 4), dtype=part.dtype, device=part.device)
+        pad[:part.shape[0]] = part
+        allp = [torch.empty_like(pad) for _ in range(layer.world_size)]
+        dist.all_gather(allp, pad)
+        part = torch.cat([a[:c] for a, c in zip(allp, cnts)])
     n_src = layer.e * layer.t
     gp_all = torch.zeros((n_src, layer.T, layer.k), dtype=layer.logit_dtype, device=ex_all.device)
     s_, p_, l_ = part[:, 0].long(), part[:, 1].long(), part[:, 2].long()
@@ -114,8 +124,9 @@ def combine_backward(layer: MoeLayer, grad_out: dict, expert_out: dict, level: i
 def dispatch_backward(layer: MoeLayer, grad_rows: dict, level: int, n: int = 1):
     """grad_rows: {card: [>= rows, h]} gradient of the dispatched rows
     (consistent over a node's TP cards), in the layout of the last dispatch
-    with this level and n.  Returns {card: grad_x [T, h]} in the layer's
-    output dtype.  The forward combine with unit weights; cd.probs and the
+    with this level and n.  The combine exchange mirrors the last dispatch,
+    so this follows combine_backward (backprop order: combine, then
+    dispatch).  Returns {card: grad_x [T, h]} in the layer's output dtype.  The forward combine with unit weights; cd.probs and the
     expert-output binding are restored afterwards."""
     saved = {cd.card: cd.probs.clone() for cd in layer.cards}
     try:
