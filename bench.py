@@ -647,10 +647,13 @@ def main():
         traffic_alg = unp_bytes
         dom_name = ("unpermute_combine (k_unpermute_k2<bf16,bf16,f32>)" if ELEM == 2 and k <= 2
                     else "unpermute_combine (k_unpermute)")
+    # DRAM bytes of the same kernel from an ncu --set full capture of this
+    # workload (profiles/ncu_traffic.json, keyed by workload then stage); null
+    # when that workload has no capture or the kernel differs from the one timed
     ncu_traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            ncu_traffic = json.load(f).get(dom_name.split(" ")[0])
+            ncu_traffic = json.load(f)["workloads"][CONFIG["workload"]].get(dom_name.split(" ")[0])
     except Exception:
         pass
     roofline = {"bound": "hbm", "kernel": dom_name, "achieved": ach, "peak": peak, "unit": "GB/s",
