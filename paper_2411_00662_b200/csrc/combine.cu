@@ -166,10 +166,12 @@ __device__ __forceinline__ void unpermute_tokens(const UnpermArgs& a, int64_t to
 // Lean top-1/top-2 un-permute (16-byte vectors, fp32 accumulation): warp per
 // item of (token, 32*UV vectors); both slots' UV loads are in flight at once;
 // row addresses and weights are broadcast by shuffle from lanes 0..k-1 (no
-// staging); 32-bit item arithmetic keeps it within 64 registers, so four
-// CTAs (32 warps) fit per SM — occupancy is what keeps the gather at HBM
-// speed (scripts/micro/gather_bench.cu: 5.7 TB/s at 16 warps/SM, 6.3 TB/s at
-// 32 warps/SM for the same bytes in flight).
+// staging); 32-bit item arithmetic keeps registers low — occupancy is what
+// keeps the gather at HBM speed (scripts/micro/gather_bench.cu: 5.7 TB/s at
+// 16 warps/SM, 6.3 TB/s at 32 warps/SM for the same bytes in flight).  The
+// bf16 top-2 launch runs 2 KiB items at 3 CTAs/SM (80 registers): 1 KiB items
+// at 4 CTAs/SM measured slower, and 2 KiB items under the 64-register cap of
+// 4 CTAs/SM spill (ptxas: 72 B of spill stores).
 template <class TIn, class TOut, class TProb, int UV, int MinB, int KMAX = 2>
 __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_constant__ UnpermArgs a) {
   constexpr int N = 16 / sizeof(TIn);
