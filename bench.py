@@ -1,14 +1,18 @@
 #!/usr/bin/env python
 """MoE dispatch+combine benchmark (BASELINE.json metric: us/layer).
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config mixtral|toy|70b|deepseek]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config deepseek|mixtral|toy|70b]
     torchrun --nproc-per-node N bench.py --gpus N ...
 
-Workload (configs[1], Mixtral-8x7B MoE layer, bf16): T = 4096 tokens per
-node group, hidden 4096, E = 8 experts, top-2.  One card per GPU; the node
-topology grows with N (weak scaling: every GPU routes and exchanges one node
-group's 4096 tokens):  N=1 -> 1x1, N=2 -> 2x1 (EP only), N=4 -> 2x2,
-N=8 -> 2x4 (EP=2 x TP=4).  A step is one layer: route (top-k gate) ->
+Workload: BASELINE.json's metric is not quoted on one config, so the default
+is the largest config that fits one GPU, configs[3] (DeepSeek-V2-style
+fine-grained MoE layer, bf16): T = 8192 tokens per node group, hidden 5120,
+E = 160 experts, top-6.  --config picks the others (mixtral = configs[1],
+70b = configs[2], toy = configs[0]).  One card per GPU; the node topology
+grows with N (weak scaling: every GPU routes and exchanges one node group's
+tokens): N=1 -> 1x1, N=2 -> 2x1 (EP only), N=4 -> 2x2, N=8 -> 4x2
+(EP=4 x TP=2, the config's own topology; Mixtral/70b/toy use 2x4).
+A step is one layer: route (top-k gate) ->
 dispatch (index, count exchange, fused permute+AllToAll, AllGather) ->
 combine (reverse AllToAll, weighted un-permute + output AllGather), with
 identity experts.  Level/chunks: the MoNTA planner's choice for t >= 2,
@@ -49,7 +53,8 @@ WORKLOADS = {
                   "experts": 160, "top_k": 6, "dtype": "bf16", "logits": "f32"},
                  {1: (1, 1), 2: (2, 1), 4: (2, 2), 8: (4, 2)}),
 }
-CONFIG, TOPOLOGY = WORKLOADS["mixtral"]
+DEFAULT_WORKLOAD = "deepseek"  # largest single-GPU config (configs[3]); see the docstring
+CONFIG, TOPOLOGY = WORKLOADS[DEFAULT_WORKLOAD]
 ELEM = 2  # payload bytes per element
 
 
@@ -57,6 +62,16 @@ def select_workload(name: str) -> None:
     global CONFIG, TOPOLOGY, ELEM
     CONFIG, TOPOLOGY = WORKLOADS[name]
     ELEM = 4 if CONFIG["dtype"] == "f32" else 2
+
+
+L2_NOTE = "flushed between steps (256 MiB memset + 256 MiB read outside the events: cold, clean L2)"
+
+
+def workload_config(e: int, t: int) -> dict:
+    """The `config` object of the JSON line — identical for both arms (the
+    schedule the repo arm ran, level/chunks/landing/planner, is reported
+    beside it under `schedule`)."""
+    return dict(CONFIG, topology=f"{e}x{t}", parallelism=f"ep{e}xtp{t}", l2=L2_NOTE)
 
 
 def payload_dtype():
@@ -259,7 +274,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": v, "unit": "us/layer", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic", "impl": "reference",
-            "config": dict(CONFIG, topology=f"{e}x{t}", level="O1" if t > 1 else "Baseline"),
+            "config": workload_config(e, t),
             "cpu_baseline": {"value": v, "unit": "us/layer", "cores": 1, "kind": "port",
                              "sample": f"full layer ({T} tokens x {e} nodes) per step, {args.steps} steps; "
                                        f"oracle/moe_oracle.c, 1 thread of {os.cpu_count()}"},
@@ -328,8 +343,8 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="mixtral", choices=sorted(WORKLOADS),
-                    help="BASELINE.json workload (default: configs[1], the metric's)")
+    ap.add_argument("--config", default=DEFAULT_WORKLOAD, choices=sorted(WORKLOADS),
+                    help="BASELINE.json workload (default: configs[3], the largest that fits one GPU)")
     ap.add_argument("--level", default="auto", help="auto|baseline|o1|o2|o3")
     ap.add_argument("--chunks", type=int, default=0)
     ap.add_argument("--landing", default="final", choices=["final", "staged"])
@@ -691,12 +706,12 @@ def main():
     line = {"metric": METRIC, "value": us, "unit": "us/layer", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": us / 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic (randn x, randn f32 gate logits)",
-            "config": dict(CONFIG, topology=f"{e}x{t}", level=_lib.LEVEL_NAMES[level], chunks=n,
-                           landing=args.landing, parallelism=f"ep{e}xtp{t}", cuda_graphs=not args.no_graphs,
-                           l2="flushed between steps (256 MiB memset + 256 MiB read outside the events: cold, clean L2)",
-                           planner=None if decision is None else
-                           {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
-                            "t_pred_us": decision.t_pred * 1e6, "in_place_check_us": autotune}),
+            "config": workload_config(e, t),
+            "schedule": {"level": _lib.LEVEL_NAMES[level], "chunks": n, "landing": args.landing,
+                         "cuda_graphs": not args.no_graphs,
+                         "planner": None if decision is None else
+                         {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
+                          "t_pred_us": decision.t_pred * 1e6, "in_place_check_us": autotune}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "stages": stages, "roles_busy_us": roles, "exposed_alltoall_us": exp_aa,
             "naive": naive,

@@ -252,7 +252,10 @@ moe_status moe_ctx_combine(moe_ctx* ctx, int level, int32_t n_chunks, void* stre
 moe_status moe_ctx_forward(moe_ctx* ctx, int level, int32_t n_chunks, int landing, void* stream);
 /* End-to-end from HOST buffers: H2D of x/logits for every local card
  * (node-major [local cards][T][...]), forward, D2H of `out`.  Host buffers
- * should be pinned for async copies. */
+ * should be pinned for async copies.  A lone card (1x1 context) with
+ * MOE_LAND_FINAL picks its own token chunking to overlap the copies with the
+ * layer (the result does not depend on n there); STAGED landing honours
+ * n_chunks and populates pre/pre_tags like moe_ctx_forward. */
 moe_status moe_ctx_forward_host(moe_ctx* ctx, int level, int32_t n_chunks, int landing,
                                 const void* host_x, const void* host_logits, void* host_out,
                                 void* stream);

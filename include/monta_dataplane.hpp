@@ -23,7 +23,14 @@
 // reference drops records of experts >= e, dataplane.hpp:151-160), every token
 // and nodes must hold the same number of tokens; violations throw
 // std::invalid_argument.  Tokens with fewer selections than others are padded
-// with empty slots (expert id -1), which every kernel skips.
+// with empty slots (expert id -1), which every kernel skips.  combine_unpermute
+// takes its row width from the expert outputs (which may differ from the
+// dispatched payload width, as in the reference) but needs every output row
+// to share it — rows move as one dense [rows, W] tensor — where the reference
+// only requires a token's own slots to agree (dataplane.hpp:335-338); a
+// ragged row throws CorruptRoutingError like the reference's mismatch.
+// Gates are paired with their expert by id (tr.experts[slot] <-> tr.probs[slot],
+// dataplane.hpp:340-343), so the routing's expert order need not ascend.
 #pragma once
 
 #include <cuda_runtime.h>
@@ -179,8 +186,10 @@ struct Layer {
   }
 };
 
+// hidden_override > 0: the context's row width (the combine's expert-output
+// width, which may differ from the dispatched payload width).
 inline void build_layer(Layer& L, const std::vector<PermutedBatch>& per_node, const VirtualTopology& topo, int n,
-                        const std::vector<RoutingDecision>* routing) {
+                        const std::vector<RoutingDecision>* routing, int hidden_override = 0) {
   device();
   L.topo = topo;
   const int e = topo.e;
@@ -195,6 +204,7 @@ inline void build_layer(Layer& L, const std::vector<PermutedBatch>& per_node, co
     for (const auto& inv : b.inverse_map) k = std::max(k, int(inv.size()));
   }
   L.W = width < 0 ? 0 : width;
+  if (hidden_override > 0) L.W = hidden_override;
   L.k = k < 1 ? 1 : k;
   moe_layer_desc d{};
   d.e = e;
@@ -227,11 +237,22 @@ inline void build_layer(Layer& L, const std::vector<PermutedBatch>& per_node, co
         if (rec.source_card != topo.canonical_card(g) || rec.source_position != i)
           throw std::invalid_argument("monta: records must carry make_batch tags");
         ids[i] = rec.token_id;
-        std::copy(rec.payload.begin(), rec.payload.end(), x.begin() + std::ptrdiff_t(i) * d.hidden);
+        const std::size_t w = std::min<std::size_t>(rec.payload.size(), std::size_t(d.hidden));
+        std::copy(rec.payload.begin(), rec.payload.begin() + std::ptrdiff_t(w), x.begin() + std::ptrdiff_t(i) * d.hidden);
       }
       if (routing) {
+        // the reference pairs tr.probs[slot] with tr.experts[slot]
+        // (dataplane.hpp:335-343); the device slots follow the inverse map
+        // (ascending expert), so each slot's gate is looked up by expert id
         const auto& tr = (*routing)[g].per_token[i];
-        for (int s = 0; s < int(tr.probs.size()) && s < L.k; ++s) probs[std::size_t(i) * L.k + s] = tr.probs[s];
+        for (int s = 0; s < int(inv.size()) && s < L.k; ++s) {
+          const int ex = b.expert_of[inv[s]];
+          int j = 0;
+          while (j < int(tr.experts.size()) && tr.experts[j] != ex) ++j;
+          if (j == int(tr.experts.size()) || j >= int(tr.probs.size()))
+            throw CorruptRoutingError("combine_unpermute: inverse map does not match routing");
+          probs[std::size_t(i) * L.k + s] = tr.probs[j];
+        }
       }
     }
     for (int rho = 0; rho < topo.t; ++rho) {
@@ -429,8 +450,17 @@ inline std::vector<std::vector<CombinedToken>> combine_unpermute(const CardBuffe
         throw CorruptRoutingError("combine_unpermute: inverse map does not match routing");
     }
   }
+  // the expert outputs' width (the reference only requires a token's slots
+  // to agree, dataplane.hpp:335-338); rows move as one dense [rows, W]
+  // tensor, so every output row must share it (documented deviation)
+  int out_w = -1;
+  for (int x = 0; x < topo.e && out_w < 0; ++x)
+    for (const auto& rec : expert_outputs[topo.canonical_card(x)]) {
+      out_w = int(rec.payload.size());
+      break;
+    }
   detail::Layer L;
-  detail::build_layer(L, permuted, topo, 1, &routing);
+  detail::build_layer(L, permuted, topo, 1, &routing, out_w > 0 ? out_w : 0);
   // the index and plan of this layer; then the expert outputs replace the
   // dispatched rows (located by their tags, like the reference's lookup)
   detail::check(moe_ctx_dispatch(L.ctx, MOE_BASELINE, 1, MOE_LAND_FINAL, nullptr));

@@ -128,7 +128,12 @@ class Nodes:
             ps, eo, iv, il = permute(self.experts[g])
             self.perm_src[g], self.expert_of[g], self.inv[g], self.inv_len[g] = ps, eo, iv, il
         self.n_records = self.inv_len.sum(axis=1).astype(np.int32)
-        self.cap = max(1, e * self.T * min(self.k, E // e))
+        # exact per-node landing count (the routed pairs whose expert the node
+        # hosts), so full-size layers do not allocate e*T*k rows per node
+        L = max(1, E // e)
+        ex = self.experts[self.experts >= 0]
+        per_node = np.bincount((ex // L)[ex // L < e], minlength=e) if ex.size else np.zeros(e, np.int64)
+        self.cap = max(1, int(per_node.max()))
         self._s = _Batches(e, t, E, self.T, self.k, self.row_bytes, self.x.ctypes.data, self.token_ids.ctypes.data,
                            self.perm_src.ctypes.data, self.expert_of.ctypes.data, self.n_records.ctypes.data)
 

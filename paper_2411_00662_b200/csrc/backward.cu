@@ -160,11 +160,15 @@ __global__ void __launch_bounds__(kMaxThreads) k_combine_bwd(const TG* __restric
         if (c < packs) PG::load_raw(grow + c * N, gv[u]);
       }
       for (int s = 0; s < k; ++s) {
+        // an empty slot (r < 0, no expert: front.cuh index_block) has no row:
+        // nothing to read or write, and its grad_prob is 0.  r is uniform over
+        // the CTA, so the warp reductions below stay converged.
         const int64_t r = pos[i * k + s];
-        const A p = A(load_p(probs + i * k + s));
+        const bool live = r >= 0;
+        const A p = live ? A(load_p(probs + i * k + s)) : A(0);
         A dot = 0;
         typename PY::Raw yv[U];
-        if (gp) {
+        if (gp && live) {
 #pragma unroll
           for (int u = 0; u < U; ++u) {
             const int64_t c = base + threadIdx.x + int64_t(u) * blockDim.x;
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_combine_bwd(const TG* __restric
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int64_t c = base + threadIdx.x + int64_t(u) * blockDim.x;
-          if (c < packs) {
+          if (c < packs && live) {
             if (gp) {
 #pragma unroll
               for (int j = 0; j < N; ++j) dot += cvt_in<A>(gv[u].e[j]) * cvt_in<A>(yv[u].e[j]);
@@ -225,6 +229,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_dispatch_bwd(const TI* __restri
         for (int j = 0; j < N; ++j) acc[u][j] = 0;
       for (int s = 0; s < k; ++s) {
         const int64_t r = pos[i * k + s];
+        if (r < 0) continue;  // empty slot: contributes nothing
         typename PI::Raw v[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -264,7 +269,8 @@ __global__ void __launch_bounds__(256) k_route_bwd(const F* __restrict__ z, int6
     sum = warp_sum(sum);
     // S = sum_s g_s * P_{x_s}
     F S = 0;
-    for (int s = lane; s < k; s += 32) S += gp[i * k + s] * (exp(zr[experts[i * k + s]] - m) / sum);
+    for (int s = lane; s < k; s += 32)
+      if (experts[i * k + s] >= 0) S += gp[i * k + s] * (exp(zr[experts[i * k + s]] - m) / sum);
     S = warp_sum(S);
     for (int e = lane; e < E; e += 32) {
       F G = 0;

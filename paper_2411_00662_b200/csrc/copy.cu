@@ -29,6 +29,16 @@ __global__ void __launch_bounds__(kCopyThreads) k_seg_copy(const __grid_constant
 }
 
 template <int V>
+__device__ __forceinline__ void store_zero(char* p) {
+  if constexpr (V == 16) *reinterpret_cast<uint4*>(p) = make_uint4(0, 0, 0, 0);
+  else if constexpr (V == 8) *reinterpret_cast<uint2*>(p) = make_uint2(0, 0);
+  else if constexpr (V == 4) *reinterpret_cast<uint32_t*>(p) = 0u;
+  else if constexpr (V == 2) *reinterpret_cast<uint16_t*>(p) = 0;
+  else *p = 0;
+}
+
+// out[r] = x[perm[r]] (column slice); perm[r] < 0 -> a zero row.
+template <int V>
 __global__ void __launch_bounds__(kCopyThreads)
     k_gather_rows(const char* __restrict__ src, int64_t src_stride, int64_t col_off, int64_t width,
                   const int32_t* __restrict__ perm, int64_t R, char* __restrict__ out,
@@ -38,6 +48,10 @@ __global__ void __launch_bounds__(kCopyThreads)
   for (int64_t r = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) / 32; r < R; r += warps) {
     const int64_t s = __ldg(perm + r);
     char* d = out + r * out_stride;
+    if (s < 0) {  // no source row (the index's tail past expert_offsets[E]): zero-fill
+      for (int64_t c = int64_t(lane) * V; c < width; c += 32 * V) store_zero<V>(d + c);
+      continue;
+    }
     copy_bytes<V>(src + s * src_stride + col_off, &d, 1, width, lane);
   }
 }

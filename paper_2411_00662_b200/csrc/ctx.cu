@@ -1412,7 +1412,10 @@ moe_status forward_host_pipelined(moe_ctx* c, int level, int landing, const void
 moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
                         cudaStream_t s) {
   const moe_layer_desc& d = c->d;
-  if (hx && is_virtual(c) && c->local.size() == 1 && !c->timing && c->d.tokens > 0)
+  // a lone card with FINAL landing: its result does not depend on the chunk
+  // count, so forward_host picks its own (pipelining) chunking; STAGED
+  // landing (pre/pre_tags populated per the caller's n) takes the plain path
+  if (hx && is_virtual(c) && c->local.size() == 1 && !c->timing && c->d.tokens > 0 && landing == MOE_LAND_FINAL)
     return forward_host_pipelined(c, level, landing, hx, hl, ho, s);
   const size_t xbytes = size_t(d.tokens) * c->row_bytes;
   const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;

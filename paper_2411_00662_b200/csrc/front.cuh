@@ -75,7 +75,11 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
       for (int m = 0; m < PER; ++m) {
         const int x = sub + m * G;
         if (x < E && !((taken >> m) & 1u)) {
-          const unsigned b = __float_as_uint(float(v[m]));
+          // -0.0 is canonicalised to +0.0 first: the reference compares
+          // values (scores[l] > scores[r], dataplane.hpp:97-98), for which
+          // the two zeros tie and the lower index wins
+          unsigned b = __float_as_uint(float(v[m]));
+          b = (b == 0x80000000u) ? 0u : b;
           const unsigned u = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
           if (u > key) {  // x ascends within the lane: strict > keeps the lower index on ties
             key = u;

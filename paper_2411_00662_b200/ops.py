@@ -74,7 +74,9 @@ def build_index(experts: torch.Tensor, num_experts: int, n_chunks: int = 1, chec
     T, k = experts.shape
     dev = experts.device
     R = T * k
-    idx = Index(torch.empty(R, dtype=torch.int32, device=dev), torch.empty(R, dtype=torch.int32, device=dev),
+    # rows past expert_offsets[E] (empty slots / out-of-range ids) keep -1:
+    # permute_rows zero-fills them instead of gathering garbage
+    idx = Index(torch.full((R,), -1, dtype=torch.int32, device=dev), torch.full((R,), -1, dtype=torch.int32, device=dev),
                 torch.empty((T, k), dtype=torch.int32, device=dev),
                 torch.empty((n_chunks, num_experts), dtype=torch.int32, device=dev),
                 torch.empty(num_experts + 1, dtype=torch.int32, device=dev))
@@ -141,7 +143,8 @@ def combine_backward(grad_out: torch.Tensor, y: torch.Tensor | None, slot_pos: t
             raise ValueError("combine_backward: grad_probs needs y")
         R, ydt = (T * k if num_rows is None else num_rows), grad_out.dtype
     probs = probs.contiguous()
-    grad_y = torch.empty((R, h), dtype=ydt, device=grad_out.device) if need_grad_y else None
+    # rows no slot references (empty slots, padding) get no store: start from zero
+    grad_y = torch.zeros((R, h), dtype=ydt, device=grad_out.device) if need_grad_y else None
     grad_probs = torch.empty_like(probs) if need_grad_probs else None
     check(_lib.load().moe_combine_backward(
         grad_out.data_ptr(), _lib.dtype_code(grad_out.dtype), h,

@@ -13,7 +13,7 @@ for c in ("toy", "mixtral", "70b", "deepseek"):
         except Exception as exc:
             print(c, n, "FAILED", exc); continue
         nv = (d.get("naive") or {})
-        print(f"{c:9s} N={n} {d['config']['topology']} {d['config']['level']:8s} {d['value']:9.1f} us  naive {nv.get('us_per_layer')}  "
+        print(f"{c:9s} N={n} {d['config']['topology']} {d['schedule']['level']:8s} {d['value']:9.1f} us  naive {nv.get('us_per_layer')}  "
               f"exposedAA {d.get('exposed_alltoall_us')} / {nv.get('exposed_alltoall_us')}  roofline {d['roofline']['bound']} {d['roofline']['frac']:.2f}  "
               f"cpu {(d.get('cpu_baseline') or {}).get('value')}  e2e {(d.get('e2e') or {}).get('value')}")
 PY

@@ -13,6 +13,9 @@ Fixtures (all small; committed):
                   dispatch_monolithic, dispatch_chunked (+ pre_copy) and
                   combine_unpermute outputs
   router.npz      route_topk on seeded score matrices (incl. exact ties)
+  router_special.npz  route_topk on float32-representable special values:
+                  signed zeros, +-inf, subnormals, +-FLT_MAX (value ties the
+                  fp32 GPU key path must break exactly as the reference does)
   planner.npz     cost model / chunk search / strategy on seeded inputs
 """
 import os
@@ -104,6 +107,26 @@ def router(seed=7):
     np.savez_compressed(os.path.join(HERE, "router.npz"), **out)
 
 
+def router_special(seed=11):
+    rng = np.random.default_rng(seed)
+    f32 = np.float32
+    tiny = float(np.finfo(f32).smallest_subnormal)
+    pool_finite = np.array([-0.0, 0.0, tiny, -tiny, 2 * tiny, -2 * tiny, float(np.finfo(f32).tiny),
+                            1.0, -1.0, float(np.finfo(f32).max), -float(np.finfo(f32).max)], np.float64)
+    pool_inf = np.concatenate([pool_finite, [np.inf, -np.inf]])
+    out = {"signed_zero_scores": np.array([[-0.0, 0.0], [0.0, -0.0], [-0.0, -0.0]])}
+    out["signed_zero_experts"], out["signed_zero_probs"] = oracle.ref_route_topk(out["signed_zero_scores"], 1)
+    cases = [(300, 8, 2, pool_finite), (300, 2, 1, pool_finite), (200, 160, 6, pool_finite),
+             (300, 37, 5, pool_finite), (300, 8, 2, pool_inf), (200, 160, 6, pool_inf), (100, 4, 4, pool_inf)]
+    for c, (T, E, k, pool) in enumerate(cases):
+        s = rng.choice(pool, (T, E))
+        assert np.array_equal(s.astype(f32).astype(np.float64), s)  # exact in fp32
+        e, p = oracle.ref_route_topk(s, k)
+        out[f"c{c}_scores"], out[f"c{c}_k"], out[f"c{c}_experts"], out[f"c{c}_probs"] = s, np.array(k), e, p
+    out["count"] = np.array(len(cases))
+    np.savez_compressed(os.path.join(HERE, "router_special.npz"), **out)
+
+
 def planner(seed=41, count=60):
     rng = np.random.default_rng(seed)
     out = {}
@@ -145,5 +168,6 @@ if __name__ == "__main__":
     kats()
     dataplane()
     router()
+    router_special()
     planner()
     print("golden fixtures written to", HERE)

@@ -159,3 +159,63 @@ def test_full_size_deepseek_adjoint_properties(cuda):
     assert ((gp.double() - ref).abs() / mag_).max().item() < 1e-5
     # grad_y rows land exactly where the forward put the token's rows.
     assert torch.equal(gy[idx.slot_pos[:, 0].long()], (probs[:, :1] * g.float()).to(torch.bfloat16))
+
+
+@pytest.mark.parametrize("dt", [torch.float32, torch.bfloat16])
+def test_backward_skips_empty_slots(cuda, dt):
+    """Tokens padded with empty slots (expert -1, as the drop-in pads ragged
+    routing): the index gives them slot position -1; the forward skips them and
+    so must every adjoint (no store before the allocation, grad_prob 0)."""
+    T, h, E, k = 257, 136, 8, 3
+    g0 = torch.Generator().manual_seed(3)
+    experts = torch.sort(torch.stack([torch.randperm(E, generator=g0)[:k] for _ in range(T)]), dim=1).values
+    experts = experts.to(torch.int32)
+    experts[::3, 0] = -1                      # one empty slot on every third token
+    experts[1::7, :2] = -1                    # two on every seventh
+    experts = torch.sort(experts, dim=1).values.to(cuda)
+    idx = ops.build_index(experts, E)
+    pos = idx.slot_pos
+    live = pos >= 0
+    assert (~live).any() and torch.equal(~live, experts < 0)
+    rows_used = int(idx.expert_offsets[-1].item())
+    # permute: the tail past expert_offsets[E] is -1 and gathers zero rows
+    x = _rand((T, h), dt, 5, cuda)
+    perm = ops.permute_rows(x, idx.perm_src)
+    assert torch.all(idx.perm_src[rows_used:] == -1)
+    assert torch.all(perm[rows_used:] == 0)
+    assert torch.equal(perm[:rows_used], x[idx.perm_src[:rows_used].long()])
+    # combine backward
+    probs = torch.rand(T, k, generator=g0).to(cuda)
+    y = _rand((T * k, h), dt, 6, cuda)
+    g = _rand((T, h), dt, 7, cuda)
+    gy, gp = ops.combine_backward(g, y, pos, probs)
+    torch.cuda.synchronize()
+    assert torch.all(gp[~live] == 0)
+    want_gy = torch.zeros((T * k, h), dtype=dt, device=cuda)
+    for s in range(k):
+        m = live[:, s]
+        want_gy[pos[m, s].long()] = (probs[m, s:s + 1] * g[m].float()).to(dt)
+    assert torch.equal(gy, want_gy)
+    ref = torch.zeros(T, k, dtype=torch.float64, device=cuda)
+    for s in range(k):
+        m = live[:, s]
+        ref[m, s] = (g[m].double() * y[pos[m, s].long()].double()).sum(-1)
+    assert torch.allclose(gp.double(), ref, rtol=1e-4, atol=1e-3)
+    # dispatch backward
+    gx = ops.dispatch_backward(y, pos, out_dtype=torch.float32)
+    want = torch.zeros((T, h), dtype=torch.float32, device=cuda)
+    for s in range(k):
+        m = live[:, s]
+        want[m] += y[pos[m, s].long()].float()
+    assert torch.equal(gx, want)
+    # route backward with an empty slot's gradient ignored
+    logits = _rand((T, E), torch.float32, 8, cuda)
+    gpr = _rand((T, k), torch.float32, 9, cuda)
+    gz = ops.route_backward(logits, experts, gpr)
+    P = torch.softmax(logits.double(), -1)
+    G = torch.zeros(T, E, dtype=torch.float64, device=cuda)
+    for s in range(k):
+        m = live[:, s]
+        G[m, experts[m, s].long()] = gpr[m, s].double()
+    want_z = P * (G - (G * P).sum(-1, keepdim=True))
+    assert torch.allclose(gz.double(), want_z, rtol=1e-4, atol=1e-6)

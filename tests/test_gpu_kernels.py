@@ -46,6 +46,35 @@ def test_route_topk_ties_break_low(cuda, E, k):
     _route_case(777, E, k, torch.float32, seed=E + 1, ties=True)
 
 
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_route_topk_signed_zero_ties(cuda, dtype):
+    # -0.0 == +0.0 for the reference's comparator (dataplane.hpp:97-98): lower index wins
+    s = torch.tensor([[-0.0, 0.0], [0.0, -0.0], [-0.0, -0.0], [0.0, 0.0]], dtype=dtype, device="cuda")
+    ex, _ = ops.route_topk(s, 1)
+    assert ex.cpu().flatten().tolist() == [0, 0, 0, 0]
+    # a whole warp group (E=32, G=32 redux path) and a sub-warp group (E=5)
+    for E in (32, 5, 160):
+        row = torch.zeros(3, E, dtype=dtype)
+        row[:, ::2] = -0.0
+        row[1, E - 1] = 1e-45 if dtype is torch.float32 else 5e-324  # the smallest subnormal beats both zeros
+        ex, _ = ops.route_topk(row.cuda(), 3)
+        want = oracle.route_topk(row.double().numpy(), 3)[0]
+        np.testing.assert_array_equal(ex.cpu().numpy(), want)
+
+
+@pytest.mark.parametrize("E,k", [(8, 2), (160, 6), (37, 5)])
+def test_route_topk_special_values_vs_oracle(cuda, E, k):
+    rng = np.random.default_rng(E * 7 + k)
+    f = np.finfo(np.float32)
+    pool = np.array([-0.0, 0.0, f.smallest_subnormal, -f.smallest_subnormal, f.tiny, 1.0, -1.0, f.max, -f.max,
+                     -np.inf], np.float32)
+    logits = rng.choice(pool, (513, E))
+    ex_ref, pr_ref = oracle.route_topk(logits.astype(np.float64), k)
+    ex, pr = ops.route_topk(torch.from_numpy(logits).cuda(), k)
+    np.testing.assert_array_equal(ex.cpu().numpy(), ex_ref)
+    np.testing.assert_allclose(pr.cpu().double().numpy(), pr_ref, rtol=1e-5, atol=0)
+
+
 def test_route_topk_known_answers(cuda):
     # dataplane.hpp / test_dataplane.cpp:72-93
     ex, pr = ops.route_topk(torch.tensor([[10.0, 0.0, 0.0, 0.0]], dtype=torch.float64, device="cuda"), 1)
