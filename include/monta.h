@@ -168,6 +168,40 @@ moe_status moe_route_backward(const void* logits, int logit_dtype, int64_t T, in
                               void* stream);
 
 /* ------------------------------------------------------------------------
+ * 1c. Expert compute between dispatch and combine (
+ * the reference's expert task gated on the dispatch terminals,
+ * pipesim.hpp:102 — the reference models it, it computes nothing).
+ * ------------------------------------------------------------------------
+ * Grouped bf16 GEMM over expert-major rows (tcgen05.mma + TMEM accumulators,
+ * TMA-fed, fp32 accumulation, bf16 out): for expert l in [0, num_experts),
+ *   y[r, :] = x[r, :] . w[l]^T   for r in [expert_offsets[l], expert_offsets[l+1])
+ * w is [num_experts][n][k] bf16 (nn.Linear layout, k contiguous).  x has
+ * x_rows addressable rows (>= expert_offsets[num_experts]; rows past an
+ * expert's end are read but never written), row stride ldx elements; y row
+ * stride ldy.  k % 64 == 0, n % 128 == 0, 16-byte aligned rows.
+ * act == MOE_ACT_SWIGLU: w holds gate and up rows tile-interleaved
+ * (moe_interleave_w13) and y gets n/2 columns silu(gate) * up. */
+#define MOE_ACT_NONE 0
+#define MOE_ACT_SWIGLU 1
+#define MOE_W13_BLOCK 128 /* features per gate/up block of an interleaved w13 */
+moe_status moe_grouped_gemm(const void* x, int64_t ldx, int64_t x_rows, const void* w,
+                            const int32_t* expert_offsets, int32_t num_experts, int64_t n, int64_t k,
+                            void* y, int64_t ldy, int act, void* stream);
+/* w13[l] = blocks of MOE_W13_BLOCK gate rows then the matching up rows:
+ * rows [256 b, 256 b + 128) = gate[l][128 b ..], [256 b + 128, 256 b + 256) =
+ * up[l][128 b ..].  gate/up [num_experts][ffn][hidden], ffn % 128 == 0. */
+moe_status moe_interleave_w13(const void* w_gate, const void* w_up, int32_t num_experts, int64_t ffn,
+                              int64_t hidden, void* w13, void* stream);
+/* SwiGLU expert FFN (Mixtral / DeepSeek experts):
+ *   y = (silu(x . Wg^T) * (x . Wu^T)) . W2^T  per expert segment,
+ * w13 from moe_interleave_w13 ([E][2 ffn][hidden]), w2 [E][hidden][ffn];
+ * workspace >= x_rows * ffn bf16.  y may alias x (x is fully consumed by the
+ * first GEMM before the second writes y). */
+moe_status moe_expert_ffn(const void* x, int64_t ldx, int64_t x_rows, const void* w13, const void* w2,
+                          const int32_t* expert_offsets, int32_t num_experts, int64_t hidden, int64_t ffn,
+                          void* workspace, void* y, int64_t ldy, void* stream);
+
+/* ------------------------------------------------------------------------
  * 2. Layer context: one MoE layer's dispatch + combine over e x t cards
  * ------------------------------------------------------------------------
  * Topology (dataplane::VirtualTopology, dataplane.hpp:25-33): card c =

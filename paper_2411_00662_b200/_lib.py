@@ -34,6 +34,9 @@ LEVEL_NAMES = {BASELINE: "Baseline", O1: "O1", O2: "O2", O3: "O3"}
 F32, BF16, F16, F64, I64 = 0, 1, 2, 3, 4
 # moe_landing
 LAND_FINAL, LAND_STAGED = 0, 1
+# expert activations (moe_grouped_gemm)
+ACT_NONE, ACT_SWIGLU = 0, 1
+W13_BLOCK = 128
 # moe_stage
 STAGES = ["route", "index", "aa", "ag", "d2d", "caa", "unpermute", "total"]
 
@@ -169,6 +172,9 @@ SIGNATURES = {
                                        _P, _I64, _P, _P]),
     "moe_dispatch_backward": (C.c_int, [_P, C.c_int, _I64, _I64, _P, _I64, _I32, _P, C.c_int, _I64, _P]),
     "moe_route_backward": (C.c_int, [_P, C.c_int, _I64, _I32, _I32, _P, _P, _P, _P]),
+    "moe_grouped_gemm": (C.c_int, [_P, _I64, _I64, _P, _P, _I32, _I64, _I64, _P, _I64, C.c_int, _P]),
+    "moe_interleave_w13": (C.c_int, [_P, _P, _I32, _I64, _I64, _P, _P]),
+    "moe_expert_ffn": (C.c_int, [_P, _I64, _I64, _P, _P, _P, _I32, _I64, _I64, _P, _P, _I64, _P]),
     "moe_ctx_create": (C.c_int,[C.POINTER(LayerDesc), C.c_int, C.c_int, C.c_int, C.POINTER(_P)]),
     "moe_ctx_destroy": (C.c_int, [_P]),
     "moe_ctx_card_view": (C.c_int, [_P, C.c_int, C.POINTER(CardView)]),

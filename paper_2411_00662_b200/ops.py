@@ -182,3 +182,47 @@ def route_backward(logits: torch.Tensor, experts: torch.Tensor, grad_probs: torc
                                          experts.data_ptr(), grad_probs.data_ptr(), grad_logits.data_ptr(),
                                          _stream()))
     return grad_logits
+
+
+# ---------------------------------------------------------------------------
+# Expert compute (include/monta.h section 1c): tcgen05 grouped GEMM / SwiGLU FFN.
+
+def grouped_gemm(x: torch.Tensor, w: torch.Tensor, expert_offsets: torch.Tensor, act: int = _lib.ACT_NONE,
+                 out: torch.Tensor | None = None) -> torch.Tensor:
+    """y[r] = x[r] . w[l]^T for r in [offs[l], offs[l+1]); x [rows, K] bf16,
+    w [L, N, K] bf16; act=ACT_SWIGLU -> y has N/2 columns silu(gate)*up
+    (w from interleave_w13)."""
+    L, N, K = w.shape
+    rows = x.shape[0]
+    ncol = N // 2 if act == _lib.ACT_SWIGLU else N
+    if out is None:
+        out = torch.empty((rows, ncol), dtype=torch.bfloat16, device=x.device)
+    check(_lib.load().moe_grouped_gemm(x.data_ptr(), x.stride(0), rows, w.contiguous().data_ptr(),
+                                       expert_offsets.contiguous().data_ptr(), L, N, K, out.data_ptr(),
+                                       out.stride(0), act, _stream()))
+    return out
+
+
+def interleave_w13(w_gate: torch.Tensor, w_up: torch.Tensor) -> torch.Tensor:
+    """[L, F, h] gate + up -> [L, 2F, h] in the grouped GEMM's SwiGLU tile order."""
+    L, F, h = w_gate.shape
+    w13 = torch.empty((L, 2 * F, h), dtype=w_gate.dtype, device=w_gate.device)
+    check(_lib.load().moe_interleave_w13(w_gate.contiguous().data_ptr(), w_up.contiguous().data_ptr(), L, F, h,
+                                         w13.data_ptr(), _stream()))
+    return w13
+
+
+def expert_ffn(x: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor, expert_offsets: torch.Tensor,
+               out: torch.Tensor | None = None, workspace: torch.Tensor | None = None) -> torch.Tensor:
+    """SwiGLU experts over expert-major rows: (silu(x Wg^T) * x Wu^T) W2^T per segment."""
+    L, F2, h = w13.shape
+    F = F2 // 2
+    rows = x.shape[0]
+    if out is None:
+        out = torch.empty((rows, h), dtype=torch.bfloat16, device=x.device)
+    if workspace is None:
+        workspace = torch.empty((rows, F), dtype=torch.bfloat16, device=x.device)
+    check(_lib.load().moe_expert_ffn(x.data_ptr(), x.stride(0), rows, w13.data_ptr(), w2.contiguous().data_ptr(),
+                                     expert_offsets.contiguous().data_ptr(), L, h, F, workspace.data_ptr(),
+                                     out.data_ptr(), out.stride(0), _stream()))
+    return out
