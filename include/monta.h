@@ -250,6 +250,8 @@ typedef struct moe_card_view {
   void* out;               /* [T, h] combined output in out_dtype                 */
   int64_t rows_permuted;   /* T*k                                                 */
   int64_t recv_cap;        /* e*T*min(k, L)                                       */
+  int32_t* recv_expert_offsets; /* [L + 1] row offsets of this node's local experts in
+                                 * recv after a FINAL-landing dispatch (expert-major) */
 } moe_card_view;
 
 moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int rank, int world_size,
@@ -269,6 +271,21 @@ moe_status moe_ctx_ipc_connect(moe_ctx* ctx, const void* all_blobs);
  * an expert computed in place).  Rebind to any [recv_cap, h] buffer. */
 moe_status moe_ctx_bind_expert_out(moe_ctx* ctx, int card, void* expert_out);
 
+/* Expert FFN of a card's local experts, run between dispatch and combine by
+ * moe_ctx_forward (or explicitly with moe_ctx_experts): SwiGLU experts over
+ * the card's recv rows, segment l = [recv_expert_offsets[l], [l+1]) uses
+ * expert l's weights; output into expert_out (in place over recv by
+ * default).  w13 [L][2 ffn][h] from moe_interleave_w13, w2 [L][h][ffn], bf16,
+ * owned by the caller; the context allocates a [recv_cap, ffn] workspace.
+ * Under TP (t > 1) every rank of a node holds the node's full rows after the
+ * AllGather and computes the full FFN with the weights bound to it.  Pass
+ * w13 == NULL to unbind (identity experts).  Needs dtype bf16, h % 64 == 0,
+ * ffn % 128 == 0. */
+moe_status moe_ctx_bind_experts(moe_ctx* ctx, int card, const void* w13, const void* w2, int64_t ffn);
+/* Run the bound experts of every local card on the rows of the last
+ * dispatch (waits for every incoming row first).  No-op when none bound. */
+moe_status moe_ctx_experts(moe_ctx* ctx, void* stream);
+
 /* Route every local card (moe_route_topk on its logits). */
 moe_status moe_ctx_route(moe_ctx* ctx, void* stream);
 /* Materialise the permuted batch of every local card (dataplane::permute). */
@@ -282,7 +299,7 @@ moe_status moe_ctx_dispatch(moe_ctx* ctx, int level, int32_t n_chunks, int landi
  * receiving rank's 1/t slice, un-permute it and all-gather the output
  * slices inside the node.  Must follow a dispatch with the same n. */
 moe_status moe_ctx_combine(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
-/* route + dispatch + combine. */
+/* route + dispatch + (bound experts) + combine. */
 moe_status moe_ctx_forward(moe_ctx* ctx, int level, int32_t n_chunks, int landing, void* stream);
 /* End-to-end from HOST buffers: H2D of x/logits for every local card
  * (node-major [local cards][T][...]), forward, D2H of `out`.  Host buffers
@@ -309,7 +326,8 @@ typedef enum moe_stage {
   MOE_STAGE_D2D = 4,
   MOE_STAGE_CAA = 5,
   MOE_STAGE_UNPERMUTE = 6,
-  MOE_STAGE_TOTAL = 7
+  MOE_STAGE_TOTAL = 7,
+  MOE_STAGE_EXPERTS = 8
 } moe_stage;
 typedef struct moe_span {
   int32_t stage;

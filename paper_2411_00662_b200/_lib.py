@@ -38,7 +38,7 @@ LAND_FINAL, LAND_STAGED = 0, 1
 ACT_NONE, ACT_SWIGLU = 0, 1
 W13_BLOCK = 128
 # moe_stage
-STAGES = ["route", "index", "aa", "ag", "d2d", "caa", "unpermute", "total"]
+STAGES = ["route", "index", "aa", "ag", "d2d", "caa", "unpermute", "total", "experts"]
 
 
 class MoeError(RuntimeError):
@@ -83,7 +83,7 @@ class CardView(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in (
         "x", "logits", "token_ids", "experts", "probs", "perm_src", "expert_of", "slot_pos", "counts",
         "expert_offsets", "permuted", "recv", "recv_tags", "pre", "pre_tags", "expert_out", "comb", "out")] + [
-        ("rows_permuted", C.c_int64), ("recv_cap", C.c_int64)]
+        ("rows_permuted", C.c_int64), ("recv_cap", C.c_int64), ("recv_expert_offsets", C.c_void_p)]
 
 
 class Span(C.Structure):
@@ -172,6 +172,8 @@ SIGNATURES = {
                                        _P, _I64, _P, _P]),
     "moe_dispatch_backward": (C.c_int, [_P, C.c_int, _I64, _I64, _P, _I64, _I32, _P, C.c_int, _I64, _P]),
     "moe_route_backward": (C.c_int, [_P, C.c_int, _I64, _I32, _I32, _P, _P, _P, _P]),
+    "moe_ctx_bind_experts": (C.c_int, [_P, C.c_int, _P, _P, _I64]),
+    "moe_ctx_experts": (C.c_int, [_P, _P]),
     "moe_grouped_gemm": (C.c_int, [_P, _I64, _I64, _P, _P, _I32, _I64, _I64, _P, _I64, C.c_int, _P]),
     "moe_interleave_w13": (C.c_int, [_P, _P, _I32, _I64, _I64, _P, _P]),
     "moe_expert_ffn": (C.c_int, [_P, _I64, _I64, _P, _P, _P, _I32, _I64, _I64, _P, _P, _I64, _P]),

@@ -47,7 +47,7 @@ struct PeerPtrs {
 struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
-  size_t lists, local_delta, recv_rows, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
+  size_t lists, local_delta, recv_rows, recv_offs, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
       ready, xchg_counters, xchg_flags, xtrace, aa_table, total;
 };
 
@@ -75,6 +75,12 @@ struct Card {
   unsigned long long* xtrace = nullptr;  // [2 kernels][4 roles][max_chunks][2] role trace (ns)
   int32_t* aa_table = nullptr;        // [4 + max_chunks][E] token-side AA destinations
   unsigned* front_done = nullptr;  // CTA election counter of the front kernel
+  // bound expert FFN (moe_ctx_bind_experts)
+  const void* w13 = nullptr;
+  const void* w2 = nullptr;
+  int64_t ffn = 0;
+  void* ffn_ws = nullptr;             // [recv_cap, ffn] bf16
+  size_t ffn_ws_bytes = 0;
 };
 
 struct Span {
@@ -165,6 +171,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.lists = take(size_t(kNumPhases) * d.max_chunks * seglist_bytes(int(E)));
   s.local_delta = take(size_t(E) * 4);
   s.recv_rows = take(8);
+  s.recv_offs = take(size_t(c->L + 1) * 4);
   s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
   s.epoch = take(8);
   s.front_done = take(16);
@@ -207,6 +214,7 @@ void bind_card(moe_ctx* c, Card& cd) {
   v.out = b + s.out;
   v.rows_permuted = c->R;
   v.recv_cap = c->recv_cap;
+  v.recv_expert_offsets = reinterpret_cast<int32_t*>(b + s.recv_offs);
   cd.count_table = reinterpret_cast<uint64_t*>(b + s.count_table);
   cd.flags = reinterpret_cast<uint64_t*>(b + s.flags);
   cd.err = reinterpret_cast<int32_t*>(b + s.err);
@@ -424,7 +432,10 @@ extern "C" moe_status moe_ctx_destroy(moe_ctx* c) {
   for (void* p : c->opened) cudaIpcCloseMemHandle(p);
   if (c->xfer_list) cudaFree(c->xfer_list);
   if (c->xfer_host) cudaFreeHost(c->xfer_host);
-  for (auto& cd : c->local) cudaFree(cd.slab);
+  for (auto& cd : c->local) {
+    cudaFree(cd.slab);
+    if (cd.ffn_ws) cudaFree(cd.ffn_ws);
+  }
   for (auto& sp : c->spans) {
     cudaEventDestroy(sp.a);
     cudaEventDestroy(sp.b);
@@ -458,6 +469,42 @@ extern "C" moe_status moe_ctx_card_view(moe_ctx* c, int card, moe_card_view* out
 
 extern "C" int moe_ctx_num_local_cards(const moe_ctx* c) { return c ? int(c->local.size()) : 0; }
 extern "C" int moe_ctx_first_card(const moe_ctx* c) { return c && !c->local.empty() ? c->local[0].id : -1; }
+
+extern "C" moe_status moe_ctx_bind_experts(moe_ctx* c, int card, const void* w13, const void* w2, int64_t ffn) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: null ctx");
+  for (auto& cd : c->local) {
+    if (cd.id != card) continue;
+    MONTA_CUDA(cudaSetDevice(c->device));
+    // a captured graph holds the old expert launches (or none): drop them
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+    if (!w13) {
+      cd.w13 = cd.w2 = nullptr;
+      cd.ffn = 0;
+      return MOE_OK;
+    }
+    if (!w2) return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: null w2");
+    if (c->d.dtype != MOE_BF16) return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: experts need a bf16 payload");
+    if (c->d.hidden % 128)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: hidden must be a multiple of 128");
+    if (ffn < MOE_W13_BLOCK || ffn % MOE_W13_BLOCK)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: ffn must be a positive multiple of %d", MOE_W13_BLOCK);
+    const size_t need = size_t(std::max<int64_t>(c->recv_cap, 1)) * size_t(ffn) * 2;
+    if (need > cd.ffn_ws_bytes) {
+      if (cd.ffn_ws) cudaFree(cd.ffn_ws);
+      cd.ffn_ws = nullptr;
+      cd.ffn_ws_bytes = 0;
+      MONTA_CUDA(cudaMalloc(&cd.ffn_ws, need));
+      cd.ffn_ws_bytes = need;
+    }
+    cd.w13 = w13;
+    cd.w2 = w2;
+    cd.ffn = ffn;
+    return MOE_OK;
+  }
+  return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: card %d is not local", card);
+}
 
 extern "C" moe_status moe_ctx_bind_expert_out(moe_ctx* c, int card, void* expert_out) {
   if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "bind_expert_out: null ctx");
@@ -565,6 +612,7 @@ PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
   // the persistent exchange reads the segment lists instead
   a.aa_table = xchg_eligible(c, level) ? nullptr : cd.aa_table;
   a.recv_rows = cd.recv_rows;
+  a.recv_offs = cd.v.recv_expert_offsets;
   a.err = cd.err;
   a.wait = no_wait();
   a.wait.epoch_ptr = cd.epoch_dev;
@@ -1353,6 +1401,16 @@ moe_status combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
 
 }  // namespace
 
+namespace {
+moe_status experts_impl(moe_ctx* c, cudaStream_t s);
+}  // namespace
+
+extern "C" moe_status moe_ctx_experts(moe_ctx* c, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  return experts_impl(c, static_cast<cudaStream_t>(stream));
+}
+
 extern "C" moe_status moe_ctx_combine(moe_ctx* c, int level, int32_t n, void* stream) {
   if (moe_status st = check_ready(c)) return st;
   MONTA_CUDA(cudaSetDevice(c->device));
@@ -1409,13 +1467,40 @@ moe_status forward_host_pipelined(moe_ctx* c, int level, int landing, const void
   return MOE_OK;
 }
 
+// Bound experts between dispatch and combine.  Multi-GPU:
+// the persistent dispatch returns before the peers' rows have landed, so the
+// experts first wait for every incoming chunk (the flags the combine would
+// wait on); then the SwiGLU FFN over the card's expert-major recv segments.
+moe_status experts_impl(moe_ctx* c, cudaStream_t s) {
+  bool any = false;
+  for (auto& cd : c->local) any |= cd.w13 != nullptr;
+  if (!any) return MOE_OK;
+  if (c->last_level < 0 || !c->combine_ready)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "experts: no dispatched rows to compute on");
+  if (!is_virtual(c))
+    if (moe_status st = dispatch_tail_wait(c, c->local[0], c->last_level, c->last_n, MOE_LAND_FINAL, s)) return st;
+  const int64_t h = c->d.hidden;
+  for (auto& cd : c->local) {
+    if (!cd.w13) continue;
+    size_t sl;
+    span_begin(c, MOE_STAGE_EXPERTS, -1, s, &sl);
+    if (moe_status st = moe_expert_ffn(cd.v.recv, h, c->recv_cap, cd.w13, cd.w2, cd.v.recv_expert_offsets, c->L, h,
+                                       cd.ffn, cd.ffn_ws, cd.v.expert_out, h, s))
+      return st;
+    span_end(c, sl, s);
+    c->launches += 2;
+  }
+  return MOE_OK;
+}
+
 moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
                         cudaStream_t s) {
   const moe_layer_desc& d = c->d;
   // a lone card with FINAL landing: its result does not depend on the chunk
   // count, so forward_host picks its own (pipelining) chunking; STAGED
   // landing (pre/pre_tags populated per the caller's n) takes the plain path
-  if (hx && is_virtual(c) && c->local.size() == 1 && !c->timing && c->d.tokens > 0 && landing == MOE_LAND_FINAL)
+  if (hx && is_virtual(c) && c->local.size() == 1 && !c->timing && c->d.tokens > 0 && landing == MOE_LAND_FINAL &&
+      !c->local[0].w13)  // bound experts need every chunk's rows before they run
     return forward_host_pipelined(c, level, landing, hx, hl, ho, s);
   const size_t xbytes = size_t(d.tokens) * c->row_bytes;
   const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;
@@ -1435,6 +1520,7 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
   moe_status st = dispatch_impl(c, level, n, landing, s, true);
   c->in_forward = false;
   if (st != MOE_OK) return st;
+  if (moe_status st1 = experts_impl(c, s)) return st1;
   if (moe_status st2 = combine_impl(c, level, n, s)) return st2;
   if (ho)
     for (size_t i = 0; i < c->local.size(); ++i)

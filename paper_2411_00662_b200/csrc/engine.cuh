@@ -184,6 +184,7 @@ struct PlanArgs {
   int32_t* local_delta;        // [E]
   int32_t* aa_table;           // [4][E] {card, base_final, col_off, width} + [n][E] base_staged
   int64_t* recv_rows;          // [1]
+  int32_t* recv_offs;          // [L + 1] this node's local-expert row offsets in recv (final layout)
   WaitList wait;
   int32_t poll_peers;          // wait until every peer node's count words carry this epoch
   int32_t* err;

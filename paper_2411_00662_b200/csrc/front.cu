@@ -228,6 +228,8 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
   if (a.do_plan == 2) {
     // one card holding every expert, final landing: the final layout IS the
     // permuted order (every base 0, full rows, nothing crosses a node)
+    for (int x = tid; x <= E; x += blockDim.x)
+      if (p.recv_offs) p.recv_offs[x] = offs[x];
     for (int x = tid; x < E; x += blockDim.x) {
       p.local_delta[x] = 0;
       p.aa_table[x] = 0;

@@ -440,6 +440,15 @@ __device__ __forceinline__ void plan_block(const PlanArgs& a, const PlanTables& 
     const int x = a.node * L + l;
     a.local_delta[x] = tb.fin[(a.node * L + l) * e + a.node] - tb.eo[a.node * (E + 1) + x];
   }
+  // 6a. this node's local-expert row offsets in recv (final layout: for l,
+  //     for source g) — the grouped GEMM's segments (experts.cu)
+  if (a.recv_offs) {
+    #pragma unroll 1
+    for (int l = tid; l <= L; l += nth) {
+      if (l < L) a.recv_offs[l] = tb.fin[(a.node * L + l) * e];
+      else a.recv_offs[L] = tb.fin[(a.node * L + L - 1) * e + e - 1] + CUM(e - 1, n, a.node * L + L - 1);
+    }
+  }
   // 6b. per-expert destination table of this sender for the token-side AA:
   //     dst row of permuted position p = base[x] + p on card[x], columns
   //     [off, off + width) (this rank's slice on cross-node legs under dedup)

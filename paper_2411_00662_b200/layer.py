@@ -69,6 +69,7 @@ class CardTensors:
     pre_tags: torch.Tensor
     comb: torch.Tensor
     out: torch.Tensor
+    recv_expert_offsets: torch.Tensor
 
 
 def _stream_ptr(stream) -> int:
@@ -98,6 +99,7 @@ class MoeLayer:
         first = self.lib.moe_ctx_first_card(self._ctx)
         self.local_cards = list(range(first, first + n_local))
         self._cards = {c: self._make_card(c) for c in self.local_cards}
+        self._experts: dict = {}
 
     # ------------------------------------------------------------------ views
     def _make_card(self, card: int) -> CardTensors:
@@ -117,7 +119,8 @@ class MoeLayer:
             permuted=mk(v.permuted, (R, h), self.dtype), recv=mk(v.recv, (cap, h), self.dtype),
             recv_tags=mk(v.recv_tags, (cap, 4), i32), pre=mk(v.pre, (cap, h), self.dtype),
             pre_tags=mk(v.pre_tags, (cap, 4), i32), comb=mk(v.comb, (R, h), self.dtype),
-            out=mk(v.out, (T, h), self.out_dtype))
+            out=mk(v.out, (T, h), self.out_dtype),
+            recv_expert_offsets=mk(v.recv_expert_offsets, (self.L + 1,), i32))
 
     def card(self, c: int) -> CardTensors:
         return self._cards[c]
@@ -163,6 +166,19 @@ class MoeLayer:
         """End to end from host buffers (pinned for async copies)."""
         check(self.lib.moe_ctx_forward_host(self._ctx, level, n, landing, host_x.data_ptr(),
                                             host_logits.data_ptr(), host_out.data_ptr(), _stream_ptr(stream)))
+
+    def bind_experts(self, card: int, w13: torch.Tensor | None, w2: torch.Tensor | None = None) -> None:
+        """SwiGLU experts of this card's L local experts (w13 from ops.interleave_w13,
+        [L, 2F, h]; w2 [L, h, F]); they run between dispatch and combine.  None unbinds."""
+        if w13 is None:
+            check(self.lib.moe_ctx_bind_experts(self._ctx, card, None, None, 0))
+            self._experts.pop(card, None)
+            return
+        self._experts[card] = (w13, w2)  # keep the weights alive while bound
+        check(self.lib.moe_ctx_bind_experts(self._ctx, card, w13.data_ptr(), w2.data_ptr(), w13.shape[1] // 2))
+
+    def experts(self, stream=None) -> None:
+        check(self.lib.moe_ctx_experts(self._ctx, _stream_ptr(stream)))
 
     def bind_expert_out(self, card: int, tensor: torch.Tensor | None) -> None:
         check(self.lib.moe_ctx_bind_expert_out(self._ctx, card, tensor.data_ptr() if tensor is not None else None))

@@ -163,3 +163,85 @@ def test_grouped_gemm_rejects_bad_shapes(cuda):
     w = torch.zeros(1, 96, 128, dtype=torch.bfloat16, device=cuda)
     with pytest.raises(ValueError):
         ops.grouped_gemm(x, w, offs)  # N % 128 != 0
+
+
+# ---------------------------------------------------------------------------
+# Experts inside the layer context: dispatch -> expert FFN -> combine.
+from paper_2411_00662_b200.layer import MoeLayer, BASELINE, O1, O2, O3, LAND_FINAL, LAND_STAGED  # noqa: E402
+
+
+def _ffn_ref_rows(x, wg, wu, w2):
+    """fp32 SwiGLU FFN of rows x through one expert, intermediate and output
+    rounded to bf16 like the kernel's workspace and the recv rows.  Also
+    returns |hmid| . |w2|^T: the slack one bf16 ulp of the intermediate
+    (accumulation order inside the first GEMM) can move the output by."""
+    g = x.float() @ wg.float().T
+    u = x.float() @ wu.float().T
+    hmid = (torch.nn.functional.silu(g) * u).to(torch.bfloat16)
+    return (hmid.float() @ w2.float().T).to(torch.bfloat16), hmid.float().abs() @ w2.float().abs().T
+
+
+@pytest.mark.parametrize("e,t,E,k,level,n,landing", [
+    (1, 1, 16, 4, BASELINE, 1, LAND_FINAL),
+    (2, 2, 8, 2, O1, 1, LAND_FINAL),
+    (2, 2, 8, 2, BASELINE, 1, LAND_FINAL),
+    (2, 2, 8, 2, O2, 2, LAND_STAGED),
+    (4, 2, 16, 3, O3, 4, LAND_FINAL),
+])
+def test_layer_with_experts(cuda, e, t, E, k, level, n, landing):
+    T, h, F = 256, 256, 128
+    gen = torch.Generator(device="cpu").manual_seed(e * 100 + t * 10 + E + n)
+    layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, max_chunks=max(n, 1))
+    try:
+        L = E // e
+        wg = (torch.randn(E, F, h, generator=gen) / h ** 0.5).to(torch.bfloat16).to(cuda)
+        wu = (torch.randn(E, F, h, generator=gen) / h ** 0.5).to(torch.bfloat16).to(cuda)
+        w2 = (torch.randn(E, h, F, generator=gen) / F ** 0.5).to(torch.bfloat16).to(cuda)
+        w13 = ops.interleave_w13(wg, wu)
+        xs = [torch.randn(T, h, generator=gen).to(torch.bfloat16).to(cuda) for _ in range(e)]
+        ls = [torch.randn(T, E, generator=gen).to(cuda) for _ in range(e)]
+        for cd in layer.cards:
+            cd.x.copy_(xs[cd.node])
+            cd.logits.copy_(ls[cd.node])
+            lo = cd.node * L
+            layer.bind_experts(cd.card, w13[lo:lo + L].contiguous(), w2[lo:lo + L].contiguous())
+        layer.forward(level, n, landing)
+        layer.sync()
+        for cd in layer.cards:
+            # the experts' segments: this node's local experts in recv order
+            offs = cd.recv_expert_offsets.cpu()
+            want = torch.zeros(L, dtype=torch.int64)
+            for g in range(e):
+                ex = layer.card(g * t).experts.cpu().long()
+                for l in range(L):
+                    want[l] += int((ex == cd.node * L + l).sum())
+            assert offs[0] == 0 and torch.equal(offs[1:] - offs[:-1], want.to(offs.dtype))
+        for cd in layer.cards:
+            ex = cd.experts.long()
+            pr = cd.probs.float()
+            ref = torch.zeros(T, h, dtype=torch.float32, device=cuda)
+            mag = torch.zeros_like(ref)
+            for s in range(k):
+                for x in range(E):
+                    m = ex[:, s] == x
+                    if bool(m.any()):
+                        y, hw = _ffn_ref_rows(xs[cd.node][m], wg[x], wu[x], w2[x])
+                        ref[m] += pr[m, s:s + 1] * y.float()
+                        mag[m] += pr[m, s:s + 1] * (2.0 ** -7 * y.float().abs() + 2.0 ** -7 * hw)
+            got = cd.out.float()
+            # bf16 out (2^-8 |ref|) + per slot: one bf16 ulp of the expert row and one of
+            # its intermediate propagated through w2 (accumulation-order differences)
+            bound = 2.0 ** -8 * ref.abs() + mag + 1e-6
+            bad = (got - ref).abs() > bound
+            assert not bool(bad.any()), (cd.card, int(bad.sum()), float(((got - ref).abs() / bound).max()))
+        # unbinding restores identity experts: out = x * sum(p)
+        for cd in layer.cards:
+            layer.bind_experts(cd.card, None)
+        layer.forward(level, n, landing)
+        layer.sync()
+        for cd in layer.cards:
+            want = xs[cd.node].double() * cd.probs.double().sum(1, keepdim=True)
+            err = ((cd.out.double() - want).abs().max() / want.abs().max()).item()
+            assert err <= 1e-2
+    finally:
+        layer.close()
