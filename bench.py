@@ -337,6 +337,62 @@ def backward_kernels(T, h, E, k, cold_l2, peak, iters=10):
     return out
 
 
+FFN_DIM = {"deepseek-v2-finegrained-moe-layer": 1536, "mixtral-8x7b-moe-layer": 14336,
+           "2x70b-moe-layer": 28672}  # expert intermediate size of each workload's model
+
+
+def experts_leg(layer, cd, e, t, E, h, step, timed, steps, local):
+    """Layer step with the experts bound (random-init SwiGLU weights of the
+    workload's expert shape): us/layer, the experts stage's time and its
+    tensor-core throughput (2 * rows * 3 * F * h flops per card) against
+    MEASURED_PEAKS.json's sustained bf16 figure."""
+    import torch
+    from paper_2411_00662_b200 import ops
+    F = FFN_DIM.get(CONFIG["workload"])
+    if F is None:
+        return None
+    L = E // e
+    dev = f"cuda:{local}"
+    gen = torch.Generator(device=dev).manual_seed(99 + cd.node)
+    lo = cd.node * L
+    wg = (torch.randn(L, F, h, generator=gen, device=dev) * h ** -0.5).to(torch.bfloat16)
+    wu = (torch.randn(L, F, h, generator=gen, device=dev) * h ** -0.5).to(torch.bfloat16)
+    w13 = ops.interleave_w13(wg, wu)
+    del wg, wu
+    w2 = (torch.randn(L, h, F, generator=gen, device=dev) * F ** -0.5).to(torch.bfloat16)
+    layer.bind_experts(cd.card, w13, w2)
+    try:
+        for _ in range(3):
+            step()
+        layer.sync()
+        tot, _ = timed(step, steps)
+        layer.enable_timing(True)
+        sp = []
+        for _ in range(3):
+            step()
+            sp.append([b - a for st, j, a, b in layer.spans() if st == "experts"])
+        layer.enable_timing(False)
+        layer.sync()
+        rows = layer.recv_rows(cd.card)
+    finally:
+        layer.bind_experts(cd.card, None)
+    ex_us = 1e3 * statistics.median(sum(v) for v in sp)
+    flops = 2.0 * rows * 3 * F * h
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        peak, kind = float(pk["bf16_tflops_sustained"]), "measured bf16_tflops_sustained"
+    except Exception:
+        peak, kind = 1800.0, "fallback"
+    ach = flops / ex_us / 1e6
+    return {"us_per_layer_with_experts": tot * 1e3 / steps, "experts_us": ex_us, "rows": rows, "ffn": F,
+            "local_experts": L, "flops_per_card": flops,
+            "roofline": {"bound": "tensor", "kernel": "k_grouped_gemm x2 (SwiGLU gate/up, down)", "achieved": ach,
+                         "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "peak_kind": kind},
+            "note": "random-init SwiGLU experts of the workload's expert shape (h x F) between dispatch and "
+                    "combine; experts_us from the stage's in-graph events"}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -618,6 +674,16 @@ def main():
                "h2d_bytes_per_step": hx.numel() * ELEM + hl.numel() * 4, "d2h_bytes_per_step": ho.numel() * ELEM,
                "step_us_median": statistics.median(eper) * 1e3, "step_us_min": min(eper) * 1e3}
 
+    # ---- the same layer with SwiGLU experts between
+    # dispatch and combine (tcgen05 grouped GEMMs on the dispatched rows);
+    # reported beside the metric, which is dispatch+combine
+    experts = None
+    if not args.quick and CONFIG["dtype"] == "bf16":
+        try:
+            experts = experts_leg(layer, cd, e, t, E, h, step, timed, args.steps, local)
+        except Exception as exc:  # extra figures: never lose the bench line to them
+            experts = {"error": f"{type(exc).__name__}: {exc}"}
+
     # ---- correctness spot check of the timed configuration (identity experts)
     layer.forward(level, n, landing, stream)
     layer.sync()
@@ -717,7 +783,7 @@ def main():
             "naive": naive,
             "pipelined": pipelined,
             "skewed": skewed,
-            "nvlink": nvlink, "check_max_rel_err": err, "backward": backward}
+            "nvlink": nvlink, "check_max_rel_err": err, "backward": backward, "experts": experts}
     if rank == 0:
         print(json.dumps(line), flush=True)
     layer.close()

@@ -490,6 +490,7 @@ extern "C" moe_status moe_ctx_bind_experts(moe_ctx* c, int card, const void* w13
       return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: hidden must be a multiple of 128");
     if (ffn < MOE_W13_BLOCK || ffn % MOE_W13_BLOCK)
       return fail(MOE_ERR_INVALID_ARGUMENT, "bind_experts: ffn must be a positive multiple of %d", MOE_W13_BLOCK);
+    if (moe_status st = configure_grouped_gemm()) return st;
     const size_t need = size_t(std::max<int64_t>(c->recv_cap, 1)) * size_t(ffn) * 2;
     if (need > cd.ffn_ws_bytes) {
       if (cd.ffn_ws) cudaFree(cd.ffn_ws);

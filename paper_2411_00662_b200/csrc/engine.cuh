@@ -191,6 +191,7 @@ struct PlanArgs {
   unsigned long long* dbg;     // optional step timestamps (front kernel debug)
 };
 size_t plan_scratch_ints(int e, int E, int max_chunks);
+moe_status configure_grouped_gemm();  // experts.cu
 bool plan_fits_smem(int e, int E, int n);
 moe_status configure_plan();
 cudaError_t launch_plan_with_scratch(const PlanArgs& a, int32_t* scratch, cudaStream_t s);

@@ -401,16 +401,17 @@ moe_status make_map(CUtensorMap* m, const void* base, int64_t rows, int64_t K, i
   return MOE_OK;
 }
 
+bool g_configured[16] = {false};
+}  // namespace
+moe_status configure_grouped_gemm();
+namespace {
+
 template <int BN>
 moe_status launch_gemm(const CUtensorMap& ta, const CUtensorMap& tb, const GemmArgs& a, int grid, cudaStream_t s) {
-  static bool configured[16] = {false};
   int dev = 0;
   cudaGetDevice(&dev);
-  if (!configured[dev & 15]) {
-    MONTA_CUDA(cudaFuncSetAttribute(k_grouped_gemm<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    int(Cfg<BN>::kSmem)));
-    configured[dev & 15] = true;
-  }
+  if (!g_configured[dev & 15])
+    if (moe_status st = configure_grouped_gemm()) return st;
   k_grouped_gemm<BN><<<grid, kThreads, Cfg<BN>::kSmem, s>>>(ta, tb, a);
   MONTA_CHECK_LAUNCH("grouped_gemm launch");
   return MOE_OK;
@@ -438,6 +439,20 @@ int sm_count_of_current() {
 }
 
 }  // namespace
+
+// Kernel attributes (227 KB dynamic shared memory) of the current device; the
+// context calls this when experts are bound, outside any graph capture.
+moe_status configure_grouped_gemm() {
+  int dev = 0;
+  MONTA_CUDA(cudaGetDevice(&dev));
+  MONTA_CUDA(cudaFuncSetAttribute(k_grouped_gemm<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(Cfg<256>::kSmem)));
+  MONTA_CUDA(cudaFuncSetAttribute(k_grouped_gemm<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  int(Cfg<128>::kSmem)));
+  if (!encode_fn()) return fail(MOE_ERR_CUDA, "grouped_gemm: cuTensorMapEncodeTiled unavailable");
+  g_configured[dev & 15] = true;
+  return MOE_OK;
+}
 
 moe_status grouped_gemm(const void* x, int64_t ldx, int64_t x_rows, const void* w, const int32_t* offs, int L,
                         int64_t N, int64_t K, void* y, int64_t ldy, int act, int grid, cudaStream_t s) {
