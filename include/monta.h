@@ -491,6 +491,23 @@ typedef struct moe_sim_task {
 } moe_sim_task;
 moe_status moe_simulate_graph(const moe_sim_task* tasks, int32_t count, const int32_t* deps,
                               double* start, double* end, double* makespan);
+/* pipesim::build_pipeline (pipesim.hpp:91-105) as an explicit task graph:
+ * tasks[i] {stream, duration, dep range into deps}, kinds[i] (as in
+ * moe_sim_span), chunks[i] (1-based).  tasks == NULL: *count only. */
+moe_status moe_build_pipeline(int level, int32_t n, const moe_chunk_timing* timing, double expert_time,
+                              int32_t phases, moe_sim_task* tasks, int32_t* kinds, int32_t* chunks,
+                              int32_t capacity, int32_t* deps, int32_t dep_capacity, int32_t* count);
+
+/* config.hpp check(ModelSpec|ParallelSpec|ClusterSpec) and validate()
+ * (config.hpp:89-158): one message per violated rule, '\n'-separated into
+ * buf (truncated to capacity; *bytes_needed = full size + 1). */
+#define MOE_CHECK_MODEL 0
+#define MOE_CHECK_PARALLEL 1
+#define MOE_CHECK_CLUSTER 2
+#define MOE_CHECK_PLACEMENT 3
+moe_status moe_check_specs(int which, const moe_model_spec* m, const moe_parallel_spec* p,
+                           const moe_cluster_spec* c, char* buf, int64_t capacity, int32_t* n_messages,
+                           int64_t* bytes_needed);
 
 #ifdef __cplusplus
 } /* extern "C" */

@@ -227,6 +227,8 @@ SIGNATURES = {
     "moe_simulate_pipeline": (C.c_int, [C.c_int, _I32, C.POINTER(ChunkTiming), _D, _I32, C.POINTER(SimSpan), _I32,
                                         _PI32, _PD]),
     "moe_simulate_graph": (C.c_int, [C.POINTER(SimTask), _I32, _PI32, _PD, _PD, _PD]),
+    "moe_build_pipeline": (C.c_int, [C.c_int, _I32, _P, C.c_double, _I32, _P, _P, _P, _I32, _P, _I32, _P]),
+    "moe_check_specs": (C.c_int, [C.c_int, _P, _P, _P, _P, _I64, _P, _P]),
 }
 
 _lib = None

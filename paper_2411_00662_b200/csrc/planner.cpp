@@ -460,3 +460,129 @@ extern "C" moe_status moe_simulate_graph(const moe_sim_task* tasks, int32_t coun
   *makespan = ms;
   return MOE_OK;
 }
+
+extern "C" moe_status moe_build_pipeline(int level, int32_t n, const moe_chunk_timing* timing, double expert_time,
+                                         int32_t phases, moe_sim_task* tasks, int32_t* kinds, int32_t* chunks,
+                                         int32_t capacity, int32_t* deps, int32_t dep_capacity, int32_t* count) {
+  if (!timing || !count) return fail(MOE_ERR_INVALID_ARGUMENT, "build_pipeline: null argument");
+  if (n < 1) return fail(MOE_ERR_INVALID_ARGUMENT, "build_pipeline: n must be >= 1");
+  if (phases != 1 && phases != 2) return fail(MOE_ERR_INVALID_ARGUMENT, "build_pipeline: phases must be 1 or 2");
+  if (level < MOE_BASELINE || level > MOE_O3) return fail(MOE_ERR_INVALID_ARGUMENT, "build_pipeline: bad level");
+  if (level == MOE_BASELINE || level == MOE_O1) n = 1;
+  std::vector<Task> g;
+  const std::vector<int> term = add_phase(g, level, n, *timing, 0, {});
+  if (phases == 2) {
+    g.push_back(Task{3, 0, 3, expert_time, term});
+    const int expert = int(g.size()) - 1;
+    add_phase(g, level, n, *timing, 1, {expert});
+  }
+  *count = int32_t(g.size());
+  if (!tasks) return MOE_OK;  // size query
+  if (int32_t(g.size()) > capacity) return fail(MOE_ERR_INVALID_ARGUMENT, "build_pipeline: task capacity too small");
+  int32_t at = 0;
+  for (size_t i = 0; i < g.size(); ++i) {
+    if (at + int32_t(g[i].deps.size()) > dep_capacity)
+      return fail(MOE_ERR_INVALID_ARGUMENT, "build_pipeline: dependency capacity too small");
+    tasks[i].stream = g[i].stream;
+    tasks[i].duration = g[i].dur;
+    tasks[i].dep_begin = at;
+    for (int d : g[i].deps) deps[at++] = d;
+    tasks[i].dep_end = at;
+    if (kinds) kinds[i] = g[i].kind;
+    if (chunks) chunks[i] = g[i].chunk;
+  }
+  return MOE_OK;
+}
+
+// config.hpp check()/validate(): field-domain and placement reports.  The
+// messages are data (one per violated rule), written '\n'-separated.
+namespace {
+
+struct Report {
+  std::string text;
+  int32_t count = 0;
+  void add(const std::string& m) {
+    text += m;
+    text += '\n';
+    ++count;
+  }
+};
+
+void model_rules(const moe_model_spec& m, Report& r) {
+  const struct { int64_t v; const char* name; } pos[] = {{m.b, "b"}, {m.s, "s"}, {m.h, "h"},
+                                                          {m.a, "a"}, {m.l, "l"}, {m.k, "k"}};
+  for (const auto& f : pos)
+    if (f.v <= 0) r.add(std::string("model: ") + f.name + " must be positive");
+  if (m.p1 < 0) r.add("model: p1 must be non-negative");
+  if (m.p2 < 0) r.add("model: p2 must be non-negative");
+  if (m.bpe != 1 && m.bpe != 2 && m.bpe != 4 && m.bpe != 8) r.add("model: bpe must be one of 1, 2, 4, 8");
+}
+
+void parallel_rules(const moe_parallel_spec& p, Report& r) {
+  const struct { int v; const char* name; } deg[] = {{p.d, "d"}, {p.p, "p"}, {p.t, "t"}, {p.e, "e"}, {p.cp, "cp"}};
+  for (const auto& f : deg)
+    if (f.v < 1) r.add(std::string("parallel: ") + f.name + " must be >= 1");
+}
+
+void cluster_rules(const moe_cluster_spec& c, Report& r) {
+  if (c.nodes < 1) r.add("cluster: nodes must be >= 1");
+  if (c.gpus_per_node < 1) r.add("cluster: gpus_per_node must be >= 1");
+  if (!(c.b1 > 0.0)) r.add("cluster: b1 must be positive");
+  if (!(c.b2 > 0.0)) r.add("cluster: b2 must be positive");
+  if (c.b2 < c.b1) r.add("cluster: b2 must be >= b1 (intra-node links are the fast ones)");
+  if (!(c.b3 > 0.0)) r.add("cluster: b3 must be positive");
+  if (!(c.peak_flops > 0.0)) r.add("cluster: peak_flops must be positive");
+  if (c.switch_capacity < 1) r.add("cluster: switch_capacity must be >= 1");
+}
+
+void placement_rules(const moe_parallel_spec& p, const moe_cluster_spec& c, Report& r) {
+  if (p.t < 1 || c.gpus_per_node % p.t != 0) {
+    r.add("t (" + std::to_string(p.t) + ") does not divide gpus_per_node (" + std::to_string(c.gpus_per_node) + ")");
+  } else {
+    const int64_t slots = int64_t(c.nodes) * (c.gpus_per_node / p.t);
+    if (p.e > slots)
+      r.add("e (" + std::to_string(p.e) + ") exceeds the " + std::to_string(slots) +
+            " tensor-group slots of the cluster");
+  }
+  const int64_t gpus = int64_t(c.nodes) * c.gpus_per_node;
+  const int64_t dense = int64_t(p.d) * p.p * p.t * p.cp;
+  if (dense > gpus)
+    r.add("d*p*t*cp (" + std::to_string(dense) + ") exceeds the " + std::to_string(gpus) + " GPUs of the cluster");
+}
+
+}  // namespace
+
+extern "C" moe_status moe_check_specs(int which, const moe_model_spec* m, const moe_parallel_spec* p,
+                                      const moe_cluster_spec* c, char* buf, int64_t capacity, int32_t* n_messages,
+                                      int64_t* bytes_needed) {
+  if (!n_messages) return fail(MOE_ERR_INVALID_ARGUMENT, "check_specs: null argument");
+  Report r;
+  switch (which) {
+    case MOE_CHECK_MODEL:
+      if (!m) return fail(MOE_ERR_INVALID_ARGUMENT, "check_specs: null model");
+      model_rules(*m, r);
+      break;
+    case MOE_CHECK_PARALLEL:
+      if (!p) return fail(MOE_ERR_INVALID_ARGUMENT, "check_specs: null parallel spec");
+      parallel_rules(*p, r);
+      break;
+    case MOE_CHECK_CLUSTER:
+      if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "check_specs: null cluster");
+      cluster_rules(*c, r);
+      break;
+    case MOE_CHECK_PLACEMENT:
+      if (!p || !c) return fail(MOE_ERR_INVALID_ARGUMENT, "check_specs: null parallel spec or cluster");
+      placement_rules(*p, *c, r);
+      break;
+    default:
+      return fail(MOE_ERR_INVALID_ARGUMENT, "check_specs: unknown report %d", which);
+  }
+  *n_messages = r.count;
+  if (bytes_needed) *bytes_needed = int64_t(r.text.size()) + 1;
+  if (buf && capacity > 0) {
+    const size_t w = std::min<size_t>(r.text.size(), size_t(capacity - 1));
+    std::copy(r.text.begin(), r.text.begin() + std::ptrdiff_t(w), buf);
+    buf[w] = '\0';
+  }
+  return MOE_OK;
+}

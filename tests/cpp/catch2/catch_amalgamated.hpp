@@ -1,5 +1,5 @@
 // Minimal Catch2-compatible test harness (TEST_CASE, REQUIRE, REQUIRE_FALSE,
-// REQUIRE_THROWS_AS, Catch::Approx) so the reference's unit tests compile and
+// REQUIRE_THROWS_AS, FAIL, Catch::Approx) so the reference's unit tests compile and
 // run against this repository's drop-in headers without the Catch2
 // amalgamation (absent in this image).  Test infrastructure only.
 #pragma once
@@ -38,6 +38,8 @@ inline void fail(const char* file, int line, const char* what) {
   ss << file << ":" << line << ": " << what;
   throw Failure(ss.str());
 }
+
+inline void fail(const char* file, int line, const std::string& what) { fail(file, line, what.c_str()); }
 
 }  // namespace catch_shim
 
@@ -85,6 +87,7 @@ class Approx {
   do {                                                                 \
     if (!(__VA_ARGS__)) catch_shim::fail(__FILE__, __LINE__, "REQUIRE(" #__VA_ARGS__ ")"); \
   } while (0)
+#define FAIL(...) catch_shim::fail(__FILE__, __LINE__, std::string("FAIL: ") + std::string(__VA_ARGS__))
 #define REQUIRE_FALSE(...)                                             \
   do {                                                                 \
     if ((__VA_ARGS__)) catch_shim::fail(__FILE__, __LINE__, "REQUIRE_FALSE(" #__VA_ARGS__ ")"); \
