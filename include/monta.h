@@ -168,6 +168,30 @@ moe_status moe_route_backward(const void* logits, int logit_dtype, int64_t T, in
                               void* stream);
 
 /* ------------------------------------------------------------------------
+ * 1d. Communication priorities (conflict.hpp:40-50,
+ * PAPER.md "Communication Conflict": EP > PP > CP > DP on the shared
+ * inter-node fabric).  On B200 every group's traffic is issued by kernels on
+ * CUDA streams (this library's exchange kernels for EP, NCCL kernels on the
+ * caller's streams for PP/CP/DP), so the resolution priority becomes the
+ * stream priority: the block scheduler starts a higher-priority stream's
+ * pending CTAs first whenever the groups' kernels contend for SMs.
+ * ------------------------------------------------------------------------ */
+#define MOE_COMM_TP_SP 0
+#define MOE_COMM_EP 1
+#define MOE_COMM_PP 2
+#define MOE_COMM_CP 3
+#define MOE_COMM_DP 4
+/* The reference's resolution priority (EP 3, PP 2, CP 1, DP 0, TP/SP -1). */
+int moe_comm_priority(int group);
+/* CUDA stream priority for a group on `device`: the groups' order spread over
+ * the device's range (EP = greatest, TP/SP = least; distinct levels when the
+ * range allows). */
+moe_status moe_comm_stream_priority(int group, int device, int* cuda_priority);
+/* A non-blocking stream on the current device with that priority. */
+moe_status moe_comm_stream_create(int group, void** stream);
+moe_status moe_comm_stream_destroy(void* stream);
+
+/* ------------------------------------------------------------------------
  * 1c. Expert compute between dispatch and combine (
  * the reference's expert task gated on the dispatch terminals,
  * pipesim.hpp:102 — the reference models it, it computes nothing).

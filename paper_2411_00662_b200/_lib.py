@@ -34,6 +34,8 @@ LEVEL_NAMES = {BASELINE: "Baseline", O1: "O1", O2: "O2", O3: "O3"}
 F32, BF16, F16, F64, I64 = 0, 1, 2, 3, 4
 # moe_landing
 LAND_FINAL, LAND_STAGED = 0, 1
+# communication groups (monta.h 1d; conflict.hpp CommGroup)
+COMM_TP_SP, COMM_EP, COMM_PP, COMM_CP, COMM_DP = 0, 1, 2, 3, 4
 # expert activations (moe_grouped_gemm)
 ACT_NONE, ACT_SWIGLU = 0, 1
 W13_BLOCK = 128
@@ -174,6 +176,10 @@ SIGNATURES = {
     "moe_route_backward": (C.c_int, [_P, C.c_int, _I64, _I32, _I32, _P, _P, _P, _P]),
     "moe_ctx_bind_experts": (C.c_int, [_P, C.c_int, _P, _P, _I64]),
     "moe_ctx_experts": (C.c_int, [_P, _P]),
+    "moe_comm_priority": (C.c_int, [C.c_int]),
+    "moe_comm_stream_priority": (C.c_int, [C.c_int, C.c_int, _P]),
+    "moe_comm_stream_create": (C.c_int, [C.c_int, _P]),
+    "moe_comm_stream_destroy": (C.c_int, [_P]),
     "moe_grouped_gemm": (C.c_int, [_P, _I64, _I64, _P, _P, _I32, _I64, _I64, _P, _I64, C.c_int, _P]),
     "moe_interleave_w13": (C.c_int, [_P, _P, _I32, _I64, _I64, _P, _P]),
     "moe_expert_ffn": (C.c_int, [_P, _I64, _I64, _P, _P, _P, _I32, _I64, _I64, _P, _P, _I64, _P]),

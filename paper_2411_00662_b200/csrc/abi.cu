@@ -47,6 +47,51 @@ extern "C" moe_status moe_host_free(void* ptr) {
   return MOE_OK;
 }
 
+// Communication priorities (monta.h 1d; conflict.hpp:40-50).
+extern "C" int moe_comm_priority(int group) {
+  switch (group) {
+    case MOE_COMM_EP: return 3;
+    case MOE_COMM_PP: return 2;
+    case MOE_COMM_CP: return 1;
+    case MOE_COMM_DP: return 0;
+    case MOE_COMM_TP_SP: return -1;
+  }
+  return -2;
+}
+
+extern "C" moe_status moe_comm_stream_priority(int group, int device, int* cuda_priority) {
+  if (!cuda_priority) return fail(MOE_ERR_INVALID_ARGUMENT, "comm_stream_priority: null output");
+  const int p = moe_comm_priority(group);
+  if (p < -1) return fail(MOE_ERR_INVALID_ARGUMENT, "comm_stream_priority: unknown group %d", group);
+  int least = 0, greatest = 0;
+  int prev = 0;
+  MONTA_CUDA(cudaGetDevice(&prev));
+  MONTA_CUDA(cudaSetDevice(device));
+  const cudaError_t e = cudaDeviceGetStreamPriorityRange(&least, &greatest);
+  cudaSetDevice(prev);
+  if (e != cudaSuccess) return cuda_fail(e, "cudaDeviceGetStreamPriorityRange");
+  // priorities -1..3 over [least, greatest] (numerically lower = higher priority)
+  const int span = least - greatest;
+  *cuda_priority = least - ((p + 1) * span + 2) / 4;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_comm_stream_create(int group, void** stream) {
+  if (!stream) return fail(MOE_ERR_INVALID_ARGUMENT, "comm_stream_create: null output");
+  int dev = 0, prio = 0;
+  MONTA_CUDA(cudaGetDevice(&dev));
+  if (moe_status st = moe_comm_stream_priority(group, dev, &prio)) return st;
+  cudaStream_t s = nullptr;
+  MONTA_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, prio));
+  *stream = s;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_comm_stream_destroy(void* stream) {
+  if (stream) MONTA_CUDA(cudaStreamDestroy(static_cast<cudaStream_t>(stream)));
+  return MOE_OK;
+}
+
 extern "C" moe_status moe_route_topk(const void* logits, int logit_dtype, int64_t T, int32_t E, int32_t k,
                                      int32_t* experts, void* probs, void* stream) {
   return route_topk(logits, logit_dtype, T, E, k, experts, probs, static_cast<cudaStream_t>(stream));

@@ -396,6 +396,9 @@ extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int
   }
   int lo = 0, hi = 0;
   cudaDeviceGetStreamPriorityRange(&lo, &hi);  // hi is the numerically smallest (highest) priority
+  // the AllToAll legs are EP traffic: the top of the EP > PP > CP > DP order
+  // (monta.h 1d), above any PP/CP/DP stream a caller makes with moe_comm_stream_create
+  moe_comm_stream_priority(MOE_COMM_EP, device, &hi);
   cudaStreamCreateWithPriority(&c->s_aa, cudaStreamNonBlocking, hi);
   cudaStreamCreateWithPriority(&c->s_ag, cudaStreamNonBlocking, lo);
   cudaStreamCreateWithPriority(&c->s_d2d, cudaStreamNonBlocking, lo);

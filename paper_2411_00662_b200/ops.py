@@ -226,3 +226,25 @@ def expert_ffn(x: torch.Tensor, w13: torch.Tensor, w2: torch.Tensor, expert_offs
                                      expert_offsets.contiguous().data_ptr(), L, h, F, workspace.data_ptr(),
                                      out.data_ptr(), out.stride(0), _stream()))
     return out
+
+
+# ---------------------------------------------------------------------------
+# Communication priorities (include/monta.h section 1d): EP > PP > CP > DP.
+
+def comm_priority(group: int) -> int:
+    """The reference's resolution priority of a communication group (conflict.hpp:40-50)."""
+    return int(_lib.load().moe_comm_priority(group))
+
+
+def comm_stream_priority(group: int, device: int | None = None) -> int:
+    """CUDA stream priority the library assigns to a group on `device`."""
+    dev = torch.cuda.current_device() if device is None else device
+    out = C.c_int()
+    check(_lib.load().moe_comm_stream_priority(group, dev, C.byref(out)))
+    return int(out.value)
+
+
+def comm_stream(group: int) -> torch.cuda.Stream:
+    """A torch stream carrying `group`'s priority (e.g. the stream a caller
+    issues its DP gradient all-reduce on, below this library's EP exchange)."""
+    return torch.cuda.Stream(priority=comm_stream_priority(group))
