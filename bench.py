@@ -406,6 +406,8 @@ def main():
     ap.add_argument("--landing", default="final", choices=["final", "staged"])
     ap.add_argument("--quick", action="store_true", help="skip naive/e2e/cpu extras (profiling runs)")
     ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
+    ap.add_argument("--aa-ctas", type=int, default=0,
+                    help="B1-throttled mode: cap the cross-node AllToAll legs at this many CTAs (0: off)")
     ap.add_argument("--no-persistent", action="store_true",
                     help="multi-GPU: one launch per (leg, chunk) instead of the persistent exchange kernels")
     args = ap.parse_args()
@@ -464,6 +466,8 @@ def main():
     layer.enable_graphs(not args.no_graphs)
     if args.no_persistent:
         layer.set_persistent(False)
+    if args.aa_ctas:
+        layer.set_aa_ctas(args.aa_ctas)
     cd = layer.cards[0]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + node)
     x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(PD)
@@ -774,6 +778,7 @@ def main():
             "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic (randn x, randn f32 gate logits)",
             "config": workload_config(e, t),
             "schedule": {"level": _lib.LEVEL_NAMES[level], "chunks": n, "landing": args.landing,
+                         "aa_ctas": args.aa_ctas or None,
                          "cuda_graphs": not args.no_graphs,
                          "planner": None if decision is None else
                          {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,

@@ -190,6 +190,18 @@ moe_status moe_comm_stream_priority(int group, int device, int* cuda_priority);
 /* A non-blocking stream on the current device with that priority. */
 moe_status moe_comm_stream_create(int group, void** stream);
 moe_status moe_comm_stream_destroy(void* stream);
+/* Stream priority orders CTA scheduling, not the shared links: measured on a
+ * B200 box, a concurrent DP all-reduce slows the EP layer the same at either
+ * priority.  The conflict resolution itself (resolve_by_priority,
+ * conflict.hpp:113-142: the lower-priority event slides right until it
+ * overlaps no EP event) is the gate: with the gate enabled every
+ * moe_ctx_forward marks the context EP-busy (stream-ordered, captured in its
+ * graph) from its first kernel to its last; moe_comm_gate_wait enqueues on a
+ * lower-priority group's stream a wait until the EP phase is idle — issue it
+ * before each chunk of DP/PP/CP traffic. */
+typedef struct moe_ctx moe_ctx;
+moe_status moe_ctx_enable_comm_gate(moe_ctx* ctx, int enable);
+moe_status moe_comm_gate_wait(moe_ctx* ctx, void* stream);
 
 /* ------------------------------------------------------------------------
  * 1c. Expert compute between dispatch and combine (
@@ -366,8 +378,12 @@ moe_status moe_ctx_enable_timing(moe_ctx* ctx, int enable);
  * lockstep across ranks.  Ignored while timing is enabled. */
 moe_status moe_ctx_enable_graphs(moe_ctx* ctx, int enable);
 moe_status moe_ctx_spans(moe_ctx* ctx, moe_span* spans, int32_t capacity, int32_t* n_spans);
-/* Cap the SMs used by the cross-group (AllToAll) copy kernels, emulating a
- * slow inter-node link ("B1-throttled" mode).  0 = no cap. */
+/* Cap the CTAs of the cross-group (AllToAll, dispatch and combine) copy
+ * kernels, emulating a slow inter-node link — the paper's B2/B1 >> 1 regime
+ * on one NVSwitch box.  While capped the context runs the
+ * per-leg launches (AllToAll on the high-priority stream, AllGather and
+ * reorder copies on their own at full width), so only the cross-node legs
+ * are throttled.  0 = no cap (persistent exchange kernels). */
 moe_status moe_ctx_set_aa_ctas(moe_ctx* ctx, int32_t ctas);
 /* Transport primitive (calibration / microbenchmarks, config 5): card-local
  * rows [0, sum) of this card's `recv` buffer are stored, rows_per_card[c]

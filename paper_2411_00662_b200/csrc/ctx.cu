@@ -109,6 +109,9 @@ struct moe_ctx {
   bool debug = false;          // record front-kernel phase timestamps
   bool use_graphs = false;
   bool use_xchg = true;  // persistent role-specialised exchange kernels (multi-GPU)
+  // EP-busy gate (monta.h 1d): nonzero while a forward's EP traffic is in flight
+  int32_t* ep_busy = nullptr;
+  bool gate = false;
   struct GraphEntry {
     int level, n, landing;
     const void *hx, *hl;
@@ -439,6 +442,7 @@ extern "C" moe_status moe_ctx_destroy(moe_ctx* c) {
     cudaFree(cd.slab);
     if (cd.ffn_ws) cudaFree(cd.ffn_ws);
   }
+  if (c->ep_busy) cudaFree(c->ep_busy);
   for (auto& sp : c->spans) {
     cudaEventDestroy(sp.a);
     cudaEventDestroy(sp.b);
@@ -932,7 +936,7 @@ moe_status dispatch_tail_wait(moe_ctx* c, Card& cd, int level, int n, int landin
 // The persistent dispatch runs (and declines nothing later) when the rows
 // take 4+-byte vectors and 16+ CTAs are co-resident (four roles of >= 4).
 bool xchg_eligible(moe_ctx* c, int level) {
-  if (!c->use_xchg || is_virtual(c)) return false;
+  if (!c->use_xchg || c->aa_ctas > 0 || is_virtual(c)) return false;
   const bool dedup = level != MOE_BASELINE && c->d.t > 1;
   const int vec = copy_vec(c, dedup);
   return vec >= 4 && xchg_max_ctas(vec) >= 16;
@@ -1367,7 +1371,7 @@ moe_status combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
   // un-permute writes only local HBM: a separate launch of the top-k item
   // kernel (3-4 CTAs per SM) beats the persistent kernel's register-capped
   // un-permute, so only chunked or deduplicated combines go persistent.
-  if (c->use_xchg && (n > 1 || dedup)) {
+  if (c->use_xchg && c->aa_ctas == 0 && (n > 1 || dedup)) {
     bool done = false;
     if (moe_status st = launch_combine_persistent(c, cd, level, n, s, &done)) return st;
     if (done) return MOE_OK;
@@ -1520,12 +1524,14 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
     c->span_used = 0;
     record_timing(c->ev_base, s);
   }
+  if (c->gate) MONTA_CUDA(cudaMemsetAsync(c->ep_busy, 1, 4, s));  // EP phase begins
   c->in_forward = true;
   moe_status st = dispatch_impl(c, level, n, landing, s, true);
   c->in_forward = false;
   if (st != MOE_OK) return st;
   if (moe_status st1 = experts_impl(c, s)) return st1;
   if (moe_status st2 = combine_impl(c, level, n, s)) return st2;
+  if (c->gate) MONTA_CUDA(cudaMemsetAsync(c->ep_busy, 0, 4, s));  // EP phase over: gated DP traffic may go
   if (ho)
     for (size_t i = 0; i < c->local.size(); ++i)
       MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(ho) + i * obytes, c->local[i].v.out, obytes,
@@ -1585,6 +1591,48 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
 }
 
 }  // namespace
+
+namespace monta {
+// A lower-priority group's stream waits here until the context's EP phase is
+// idle (resolve_by_priority, conflict.hpp:113-142: the lower-priority event
+// slides right until it overlaps no EP event).
+__global__ void k_comm_gate(const volatile int32_t* busy, int32_t* err) {
+  if (threadIdx.x != 0) return;
+  const unsigned long long t0 = globaltimer();
+  while (*busy != 0) {
+    if (globaltimer() - t0 > kWaitTimeoutNs) {
+      atomicExch(err, int32_t(MOE_ERR_TIMEOUT));
+      return;
+    }
+    __nanosleep(256);
+  }
+}
+}  // namespace monta
+
+extern "C" moe_status moe_ctx_enable_comm_gate(moe_ctx* c, int enable) {
+  if (moe_status st = check_ready(c)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  if (enable && !c->ep_busy) {
+    MONTA_CUDA(cudaMalloc(&c->ep_busy, 16));
+    MONTA_CUDA(cudaMemset(c->ep_busy, 0, 16));
+  }
+  if (c->gate != (enable != 0)) {  // captured steps differ by the gate's memset nodes
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+  }
+  c->gate = enable != 0;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_comm_gate_wait(moe_ctx* c, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (!c->gate) return fail(MOE_ERR_INVALID_ARGUMENT, "comm_gate_wait: gate not enabled (moe_ctx_enable_comm_gate)");
+  MONTA_CUDA(cudaSetDevice(c->device));
+  k_comm_gate<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(c->ep_busy, c->local[0].err);
+  MONTA_CHECK_LAUNCH("comm_gate_wait");
+  return MOE_OK;
+}
 
 extern "C" moe_status moe_ctx_forward(moe_ctx* c, int level, int32_t n, int landing, void* stream) {
   if (moe_status st = check_ready(c)) return st;

@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--config", default="mixtral")
     ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--dp-mib", type=int, default=512)
+    ap.add_argument("--gap-cycles", type=int, default=400000, help="non-MoE compute between layers (~200 us)")
     args = ap.parse_args()
     world, rank, local = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -46,38 +47,66 @@ def main():
     ep = ops.comm_stream(_lib.COMM_EP)
     bucket = torch.ones(args.dp_mib << 18, dtype=torch.float32, device=f"cuda:{local}")
 
+    chunks = 16  # the DP bucket all-reduced in chunks (what the gate schedules around)
+    pieces = bucket.chunk(chunks)
+
     def run(mode):
         dp = None
+        layer.enable_comm_gate(mode == "gated")
         if mode == "equal":
             dp = torch.cuda.Stream(priority=ops.comm_stream_priority(_lib.COMM_EP))
-        elif mode == "mapped":
+        elif mode in ("mapped", "gated"):
             dp = ops.comm_stream(_lib.COMM_DP)
         for _ in range(3):
             layer.forward(level, 1, 0, ep)
         torch.cuda.synchronize()
         dist.barrier()
+        d0, d1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         if dp is not None:  # keep the DP all-reduces running through the whole timed window
             dp.wait_stream(torch.cuda.current_stream())
+            d0.record(dp)
             with torch.cuda.stream(dp):
                 for _ in range(args.steps * 2):
-                    dist.all_reduce(bucket)
+                    for p in pieces:
+                        if mode == "gated":
+                            layer.comm_gate_wait(dp)  # DP yields to EP (resolve_by_priority)
+                        dist.all_reduce(p)
+            d1.record(dp)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
         for a, b in evs:
             a.record(ep)
             layer.forward(level, 1, 0, ep)
             b.record(ep)
+            torch.cuda._sleep(args.gap_cycles)  # the step's non-MoE compute between MoE layers
         torch.cuda.synchronize()
         us = sorted(a.elapsed_time(b) * 1e3 for a, b in evs)
         med = torch.tensor([us[len(us) // 2]], dtype=torch.float64, device=f"cuda:{local}")
         dist.all_reduce(med, op=dist.ReduceOp.MAX)
-        return float(med.item())
+        dp_us = d0.elapsed_time(d1) * 1e3 / (args.steps * 2) if dp is not None else None
+        return float(med.item()), dp_us
+
+    def dp_alone():
+        dp = ops.comm_stream(_lib.COMM_DP)
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(dp)
+        with torch.cuda.stream(dp):
+            for p in pieces:
+                dist.all_reduce(p)
+        b.record(dp)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) * 1e3
 
     out = {"config": args.config, "topology": f"{e}x{t}", "level": _lib.LEVEL_NAMES[level], "dp_bucket_mib": args.dp_mib,
            "stream_priorities": {n: ops.comm_stream_priority(gr) for n, gr in
                                  (("EP", _lib.COMM_EP), ("PP", _lib.COMM_PP), ("CP", _lib.COMM_CP),
                                   ("DP", _lib.COMM_DP), ("TP_SP", _lib.COMM_TP_SP))}}
-    for mode in ("alone", "equal", "mapped", "alone"):
-        out.setdefault("layer_us_median", {}).setdefault(mode, []).append(run(mode))
+    for mode in ("alone", "equal", "mapped", "gated", "alone"):
+        lay, dp_us = run(mode)
+        out.setdefault("layer_us_median", {}).setdefault(mode, []).append(lay)
+        if dp_us is not None:
+            out.setdefault("dp_bucket_us_during", {})[mode] = dp_us
+    out["dp_bucket_allreduce_us_alone"] = dp_alone()
     if rank == 0:
         print(json.dumps(out), flush=True)
     layer.close()

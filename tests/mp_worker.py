@@ -21,6 +21,15 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2411_00662_b200.layer import MoeLayer  # noqa: E402
 
 
+def expert_weights(E, F, h, seed=777):
+    """Deterministic SwiGLU expert weights (CPU), shared with the parent test."""
+    g = torch.Generator().manual_seed(seed)
+    wg = (torch.randn(E, F, h, generator=g) / h ** 0.5).to(torch.bfloat16)
+    wu = (torch.randn(E, F, h, generator=g) / h ** 0.5).to(torch.bfloat16)
+    w2 = (torch.randn(E, h, F, generator=g) / F ** 0.5).to(torch.bfloat16)
+    return wg, wu, w2
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", required=True)
@@ -36,6 +45,7 @@ def main():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--graphs", type=int, default=0)
     ap.add_argument("--persistent", type=int, default=1)
+    ap.add_argument("--ffn", type=int, default=0)  # > 0: SwiGLU experts of this size bound on every card
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -62,6 +72,13 @@ def main():
     logits = torch.randn(a.T, a.E, generator=g)
     cd.x.copy_(x.cuda())
     cd.logits.copy_(logits.cuda())
+    if a.ffn:
+        from paper_2411_00662_b200 import ops
+        wg, wu, w2 = expert_weights(a.E, a.ffn, a.h)
+        L = a.E // a.e
+        sl = slice(node * L, (node + 1) * L)
+        w13 = ops.interleave_w13(wg[sl].cuda(), wu[sl].cuda())
+        layer.bind_experts(cd.card, w13, w2[sl].contiguous().cuda())
     results = {}
     for spec in a.runs.split(","):
         level, n, landing = (int(v) for v in spec.split(":"))

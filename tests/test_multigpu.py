@@ -30,14 +30,14 @@ def _port():
 
 
 def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0, persistent=1,
-            per_gpu=1):
+            per_gpu=1, ffn=0):
     world = e * t
     if torch.cuda.device_count() * per_gpu < world:
         pytest.skip(f"needs {world // per_gpu} GPUs, have {torch.cuda.device_count()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--out", str(tmp), "--groups", str(e), "--tp", str(t), "--experts", str(E), "--topk", str(k), "--tokens", str(T),
-           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs), "--persistent", str(persistent)]
+           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs), "--persistent", str(persistent), "--ffn", str(ffn)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=240 * per_gpu)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
@@ -139,3 +139,45 @@ def test_eight_gpus_2x4(cuda, tmp_path):
 def test_eight_gpus_4x2_finegrained(cuda, tmp_path):
     runs = "0:1:0,1:1:0,3:2:1"
     _check(_launch(tmp_path, 4, 2, E=16, k=4, runs=runs, T=512, h=512), 4, 2, 16, runs)
+
+
+def _check_experts(ranks, e, t, E, F, runs):
+    """Layer with SwiGLU experts between dispatch and combine over NVLink: out =
+    sum_s p_s * FFN_{x_s}(x) per token against an fp32 torch FFN (intermediate
+    and expert rows rounded to bf16 like the kernels), per element."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from mp_worker import expert_weights
+    wg, wu, w2 = (w.cuda() for w in expert_weights(E, F, ranks[0]["x"].shape[-1] // 2))
+    T = ranks[0]["experts"].shape[0]
+    for r in range(e * t):
+        x = torch.from_numpy(ranks[r]["x"].reshape(T, -1)).view(torch.bfloat16).cuda()
+        ex = torch.from_numpy(ranks[r]["experts"]).long().cuda()
+        pr = torch.from_numpy(ranks[r]["probs"]).float().cuda()
+        ref = torch.zeros(T, x.shape[1], device="cuda")
+        mag = torch.zeros_like(ref)
+        for s in range(ex.shape[1]):
+            for xe in range(E):
+                m = ex[:, s] == xe
+                if not bool(m.any()):
+                    continue
+                gt = x[m].float() @ wg[xe].float().T
+                ut = x[m].float() @ wu[xe].float().T
+                hm = (torch.nn.functional.silu(gt) * ut).to(torch.bfloat16).float()
+                y = (hm @ w2[xe].float().T).to(torch.bfloat16).float()
+                ref[m] += pr[m, s:s + 1] * y
+                mag[m] += pr[m, s:s + 1] * 2.0 ** -7 * (y.abs() + hm.abs() @ w2[xe].float().abs().T)
+        for spec in runs.split(","):
+            level, n, landing = (int(v) for v in spec.split(":"))
+            got = torch.from_numpy(ranks[r][f"out_{level}_{n}_{landing}"]).cuda()
+            bad = (got - ref).abs() > 2.0 ** -8 * ref.abs() + mag + 1e-6
+            assert not bool(bad.any()), (spec, r, int(bad.sum()))
+
+
+def test_two_gpus_ep2_with_experts(cuda, tmp_path):
+    runs = "0:1:0"
+    _check_experts(_launch(tmp_path, 2, 1, runs=runs, ffn=128), 2, 1, 8, 128, runs)
+
+
+def test_four_gpus_2x2_with_experts(cuda, tmp_path):
+    runs = "0:1:0,1:1:0,2:2:1,3:4:0"
+    _check_experts(_launch(tmp_path, 2, 2, runs=runs, ffn=256, graphs=1), 2, 2, 8, 256, runs)
