@@ -38,7 +38,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
-os.environ["NCCL_DEBUG"] = "WARN"  # keep stdout to the one JSON line
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL logs (its version line too) off stdout: one JSON line
 
 # BASELINE.json configs as workloads (--config); the default, configs[1], is the metric's workload and the
 # others are reported the same way for completeness.  Topology (e x t) per GPU count.
@@ -453,8 +454,13 @@ def main():
                                 P.EfficiencyCurve.constant(0.8))
             ov = P.OverheadModel(8e-6, 4e-6)
         model = P.ModelSpec(b=1, s=T * k, h=h, k=k, bpe=ELEM)  # routed rows: s_eff = T*k
+        # the reference's selection (separate inter-/intra-node links), reported as is
         decision = P.select_strategy(model, P.ParallelSpec(t=t, e=e), P.b200_cluster(e, t), curves, ov, n_cap=16)
-        level, n = int(decision.level), decision.n
+        # the B200 variant: on one NVSwitch box both legs leave through the same
+        # NVLink egress (not so when the AllToAll is throttled: B1-emulated mode)
+        decision_b200 = P.select_strategy_b200(model, P.ParallelSpec(t=t, e=e), P.b200_cluster(e, t), curves, ov,
+                                               n_cap=16, shared_egress=not args.aa_ctas)
+        level, n = int(decision_b200.level), decision_b200.n
         while T % n:
             n -= 1
     landing = LAND_STAGED if args.landing == "staged" else LAND_FINAL
@@ -514,23 +520,22 @@ def main():
     def step(lv=None, nn=None, ld=None):  # defaults: the (possibly re-chosen) level, n, landing
         layer.forward(level if lv is None else lv, n if nn is None else nn, landing if ld is None else ld, stream)
 
-    # The planner's model assumes the AllToAll and AllGather legs own separate
-    # links (inter- vs intra-node); on one NVSwitch box they share each GPU's
-    # ports, so a chunked proposal is checked in place against O1 (a short
-    # trial of each, max over ranks) and the faster one runs.  The reference's
-    # selection itself is unchanged (decision is reported as is).
+    # The schedule runs as the library decides it: the B200 planner variant's
+    # choice and the reference's (when they differ) are timed in place by
+    # moe_ctx_autotune (max over ranks, inside the C ABI) and the faster runs.
     autotune = None
-    if decision is not None and args.level == "auto" and (level, n) != (O1, 1):
-        def trial(lv, nn):
-            for _ in range(3):
-                step(lv, nn)
-            layer.sync()
-            return timed(lambda: step(lv, nn), 5)[0] * 1e3 / 5
-        t_plan, t_o1 = trial(level, n), trial(O1, 1)
-        autotune = {"planner": [_lib.LEVEL_NAMES[level], n, t_plan], "O1": ["O1", 1, t_o1]}
-        if t_o1 < t_plan:
-            level, n = O1, 1
-        autotune["chosen"] = [_lib.LEVEL_NAMES[level], n]
+    if decision is not None and args.level == "auto":
+        rn = decision.n
+        while T % rn:
+            rn -= 1
+        cands = [(level, n, landing)]
+        if (int(decision.level), rn) != (level, n):
+            cands.append((int(decision.level), rn, landing))
+        if len(cands) > 1:
+            best, times = layer.autotune(cands, steps=5, stream=stream)
+            autotune = {"candidates": [[_lib.LEVEL_NAMES[c[0]], c[1], us] for c, us in zip(cands, times)],
+                        "chosen": [_lib.LEVEL_NAMES[cands[best][0]], cands[best][1]]}
+            level, n = cands[best][0], cands[best][1]
 
     for _ in range(args.warmup):
         step()
@@ -781,8 +786,14 @@ def main():
                          "aa_ctas": args.aa_ctas or None,
                          "cuda_graphs": not args.no_graphs,
                          "planner": None if decision is None else
-                         {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
-                          "t_pred_us": decision.t_pred * 1e6, "in_place_check_us": autotune}},
+                         {"reference": {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,
+                                        "t_pred_us": decision.t_pred * 1e6},
+                          "b200_shared_egress": {"level": _lib.LEVEL_NAMES[int(decision_b200.level)],
+                                                 "n": decision_b200.n, "t_pred_us": decision_b200.t_pred * 1e6,
+                                                 "alternatives": [[_lib.LEVEL_NAMES[int(a.level)], a.n,
+                                                                   a.t_pred * 1e6]
+                                                                  for a in decision_b200.alternatives]},
+                          "autotune_us": autotune}},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "clocks": clk.summary(), "stages": stages, "roles_busy_us": roles, "exposed_alltoall_us": exp_aa,
             "naive": naive,

@@ -337,6 +337,18 @@ moe_status moe_ctx_dispatch(moe_ctx* ctx, int level, int32_t n_chunks, int landi
 moe_status moe_ctx_combine(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
 /* route + dispatch + (bound experts) + combine. */
 moe_status moe_ctx_forward(moe_ctx* ctx, int level, int32_t n_chunks, int landing, void* stream);
+/* Measured schedule choice (the planner's candidates checked in place):
+ * each candidate runs `steps` timed forwards through this context; times
+ * (us/layer, written back into .us) are max-reduced over the ranks of a
+ * multi-GPU context through peer memory, so all ranks return the same
+ * *best (index of the fastest; ties keep the earlier).  Every rank must call
+ * it with the same candidates. */
+typedef struct moe_schedule {
+  int32_t level, n_chunks, landing;
+  double us;
+} moe_schedule;
+moe_status moe_ctx_autotune(moe_ctx* ctx, moe_schedule* candidates, int32_t count, int32_t steps,
+                            void* stream, int32_t* best);
 /* End-to-end from HOST buffers: H2D of x/logits for every local card
  * (node-major [local cards][T][...]), forward, D2H of `out`.  Host buffers
  * should be pinned for async copies.  A lone card (1x1 context) with
@@ -491,6 +503,16 @@ moe_status moe_asymptotic_speedup(int32_t t, int32_t e, double b1, double b2, do
 moe_status moe_select_strategy(const moe_model_spec* m, const moe_parallel_spec* par,
                                const moe_cluster_spec* cl, const moe_curve_set* curves,
                                const moe_overhead* ov, int32_t n_cap, moe_strategy_decision* out);
+/* B200 variant of select_strategy.  shared_egress == 0: exactly
+ * moe_select_strategy (the reference's separate inter-/intra-node links).
+ * shared_egress != 0 (every card on one NVSwitch domain, no AllToAll cap):
+ * the AllToAll and AllGather of a chunk serialise on the same NVLink
+ * egress, so O2/O3 score n (aa + ag) + d2d [+ O2's copy backlog] — same
+ * candidates, gates, search and tie order as the reference. */
+moe_status moe_select_strategy_b200(const moe_model_spec* m, const moe_parallel_spec* par,
+                                    const moe_cluster_spec* cl, const moe_curve_set* curves,
+                                    const moe_overhead* ov, int32_t n_cap, int32_t shared_egress,
+                                    moe_strategy_decision* out);
 moe_status moe_estimate_performance(const moe_strategy_decision* d, const moe_model_spec* m,
                                     const moe_parallel_spec* par, const moe_cluster_spec* cl,
                                     int32_t moe_layer_count, double non_comm_time,

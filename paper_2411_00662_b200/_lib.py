@@ -149,6 +149,10 @@ class SimSpan(C.Structure):
                 ("end", C.c_double)]
 
 
+class Schedule(C.Structure):
+    _fields_ = [("level", C.c_int32), ("n_chunks", C.c_int32), ("landing", C.c_int32), ("us", C.c_double)]
+
+
 class SimTask(C.Structure):
     _fields_ = [("stream", C.c_int32), ("duration", C.c_double), ("dep_begin", C.c_int32), ("dep_end", C.c_int32)]
 
@@ -227,6 +231,10 @@ SIGNATURES = {
     "moe_asymptotic_speedup": (C.c_int, [_I32, _I32, _D, _D, _D, _D, _PD]),
     "moe_select_strategy": (C.c_int, [C.POINTER(ModelSpec), C.POINTER(ParallelSpec), C.POINTER(ClusterSpec),
                                       C.POINTER(CurveSet), C.POINTER(Overhead), _I32, C.POINTER(StrategyDecision)]),
+    "moe_select_strategy_b200": (C.c_int, [C.POINTER(ModelSpec), C.POINTER(ParallelSpec), C.POINTER(ClusterSpec),
+                                           C.POINTER(CurveSet), C.POINTER(Overhead), _I32, _I32,
+                                           C.POINTER(StrategyDecision)]),
+    "moe_ctx_autotune": (C.c_int, [_P, _P, _I32, _I32, _P, _P]),
     "moe_estimate_performance": (C.c_int, [C.POINTER(StrategyDecision), C.POINTER(ModelSpec),
                                            C.POINTER(ParallelSpec), C.POINTER(ClusterSpec), _I32, _D,
                                            C.POINTER(PerfReport)]),

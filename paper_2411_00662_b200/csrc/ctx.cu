@@ -30,6 +30,8 @@ namespace {
 constexpr size_t kAlign = 256;
 inline size_t align_up(size_t v) { return (v + kAlign - 1) / kAlign * kAlign; }
 
+constexpr int kMaxTune = 32;  // autotune candidates per call
+
 struct PeerPtrs {
   char* slab = nullptr;
   char* recv = nullptr;
@@ -47,7 +49,7 @@ struct PeerPtrs {
 struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
-  size_t lists, local_delta, recv_rows, recv_offs, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
+  size_t lists, local_delta, recv_rows, recv_offs, tune, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
       ready, xchg_counters, xchg_flags, xtrace, aa_table, total;
 };
 
@@ -112,6 +114,7 @@ struct moe_ctx {
   // EP-busy gate (monta.h 1d): nonzero while a forward's EP traffic is in flight
   int32_t* ep_busy = nullptr;
   bool gate = false;
+  uint64_t tune_epoch = 0;
   struct GraphEntry {
     int level, n, landing;
     const void *hx, *hl;
@@ -175,6 +178,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.local_delta = take(size_t(E) * 4);
   s.recv_rows = take(8);
   s.recv_offs = take(size_t(c->L + 1) * 4);
+  s.tune = take(size_t(kMaxCards) * kMaxTune * 8);  // [sender][candidate] us (autotune)
   s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
   s.epoch = take(8);
   s.front_done = take(16);
@@ -256,6 +260,7 @@ void set_peer(moe_ctx* c, int card, char* slab) {
 
 inline int card_of(const moe_ctx* c, int node, int rho) { return node * c->d.t + rho; }
 inline int sig_chunk(const moe_ctx* c, int ps, int j) { return kSigChunkBase + ps * c->d.max_chunks + j; }
+inline int sig_tune(const moe_ctx* c) { return c->n_flag_sigs - 1; }
 
 // Flag word on `owner` that `sender` writes for signal `sig`.
 inline uint64_t* flag_at(moe_ctx* c, int owner, int sig, int sender) {
@@ -368,7 +373,7 @@ extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int
   c->R = desc->tokens * desc->top_k;
   c->row_bytes = desc->hidden * int64_t(c->xb);
   c->recv_cap = int64_t(desc->e) * desc->tokens * std::min<int64_t>(desc->top_k, c->L);
-  c->n_flag_sigs = kSigChunkBase + kNumPhaseSignals * desc->max_chunks;
+  c->n_flag_sigs = kSigChunkBase + kNumPhaseSignals * desc->max_chunks + 1;  // + the autotune signal
   c->lay = make_layout(c);
   const int first = world_size == 1 ? 0 : rank;
   const int nlocal = world_size == 1 ? cards : 1;
@@ -1641,6 +1646,76 @@ extern "C" moe_status moe_ctx_forward(moe_ctx* c, int level, int32_t n, int land
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (c->use_graphs) return forward_graph(c, level, n, landing, nullptr, nullptr, nullptr, s);
   return forward_impl(c, level, n, landing, nullptr, nullptr, nullptr, s);
+}
+
+// In-place schedule selection: every candidate (level, n, landing) runs
+// `steps` timed forwards through this context (after two warm-ups); on a
+// multi-GPU context the per-candidate times are max-reduced over the ranks
+// through the peers' slabs (stores + epoch flags), so every rank picks the
+// same schedule.  The reference's select_strategy stays exact; this is the
+// measured decision (SURVEY §8(a) planner row on one NVSwitch box).
+extern "C" moe_status moe_ctx_autotune(moe_ctx* c, moe_schedule* cand, int32_t count, int32_t steps, void* stream,
+                                       int32_t* best) {
+  if (moe_status st = check_ready(c)) return st;
+  if (!cand || !best || count < 1 || count > kMaxTune || steps < 1)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "autotune: need 1..%d candidates, steps >= 1, outputs", kMaxTune);
+  for (int i = 0; i < count; ++i)
+    if (moe_status st = validate_dispatch(c, cand[i].level, cand[i].n_chunks, cand[i].landing)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaEvent_t e0, e1;
+  MONTA_CUDA(cudaEventCreate(&e0));
+  MONTA_CUDA(cudaEventCreate(&e1));
+  std::vector<double> local(size_t(kMaxTune), 0.0);
+  moe_status st = MOE_OK;
+  for (int i = 0; i < count && st == MOE_OK; ++i) {
+    for (int w = 0; w < 2 + steps && st == MOE_OK; ++w) {
+      if (w == 2) cudaEventRecord(e0, s);
+      st = moe_ctx_forward(c, cand[i].level, cand[i].n_chunks, cand[i].landing, stream);
+    }
+    cudaEventRecord(e1, s);
+    if (cudaEventSynchronize(e1) != cudaSuccess) st = cuda_fail(cudaGetLastError(), "autotune");
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    local[size_t(i)] = double(ms) * 1e3 / steps;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (st != MOE_OK) return st;
+  if (moe_status s2 = moe_ctx_sync(c)) return s2;
+  std::vector<double> worst(local.begin(), local.begin() + count);
+  if (!is_virtual(c)) {
+    Card& cd = c->local[0];
+    const uint64_t epoch = ++c->tune_epoch;
+    for (int q = 0; q < c->cards; ++q)  // my times into every card's [me] row (mine included)
+      if (c->peer[q].slab)
+        MONTA_CUDA(cudaMemcpyAsync(c->peer[q].slab + c->lay.tune + size_t(cd.id) * kMaxTune * 8, local.data(),
+                                   size_t(count) * 8, cudaMemcpyHostToDevice, s));
+    SignalList sg = no_signal();
+    sg.epoch = epoch;
+    WaitList w = no_wait();
+    w.epoch = epoch;
+    for (int q = 0; q < c->cards; ++q)
+      if (q != cd.id && c->peer[q].slab) {
+        sg.flags[sg.n++] = flag_at(c, q, sig_tune(c), cd.id);
+        w.flags[w.n++] = flag_at(c, cd.id, sig_tune(c), q);
+      }
+    MONTA_CUDA(launch_signal(sg, s));
+    MONTA_CUDA(launch_wait(w, cd.err, s));
+    std::vector<double> all(size_t(c->cards) * kMaxTune);
+    MONTA_CUDA(cudaMemcpyAsync(all.data(), cd.slab + c->lay.tune, all.size() * 8, cudaMemcpyDeviceToHost, s));
+    MONTA_CUDA(cudaStreamSynchronize(s));
+    if (moe_status s3 = moe_ctx_sync(c)) return s3;
+    for (int q = 0; q < c->cards; ++q)
+      for (int i = 0; i < count; ++i) worst[size_t(i)] = std::max(worst[size_t(i)], all[size_t(q) * kMaxTune + i]);
+  }
+  int b = 0;
+  for (int i = 0; i < count; ++i) {
+    cand[i].us = worst[size_t(i)];
+    if (worst[size_t(i)] < worst[size_t(b)]) b = i;  // ties keep the earlier candidate
+  }
+  *best = b;
+  return MOE_OK;
 }
 
 extern "C" moe_status moe_ctx_forward_host(moe_ctx* c, int level, int32_t n, int landing, const void* host_x,

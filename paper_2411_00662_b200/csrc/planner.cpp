@@ -240,6 +240,45 @@ extern "C" moe_status moe_select_strategy(const moe_model_spec* m, const moe_par
   return MOE_OK;
 }
 
+// B200 variant (one NVSwitch box): the AllToAll and the AllGather leave each
+// GPU through the same NVLink ports, so a chunk's AllGather cannot overlap
+// the next chunk's AllToAll — the two legs serialise on the egress; only the
+// HBM reorder copies overlap the links (the last one stays exposed; under O2
+// a copy longer than the next AllToAll holds back the next gather).
+double score_shared_o2(double aa, double ag, double d2d, int n) {
+  return n * (aa + ag) + d2d + (n - 1) * std::max(0.0, d2d - aa);
+}
+double score_shared_o3(double aa, double ag, double d2d, int n) { return n * (aa + ag) + d2d; }
+
+extern "C" moe_status moe_select_strategy_b200(const moe_model_spec* m, const moe_parallel_spec* par,
+                                               const moe_cluster_spec* cl, const moe_curve_set* curves,
+                                               const moe_overhead* ov, int32_t n_cap, int32_t shared_egress,
+                                               moe_strategy_decision* out) {
+  if (!shared_egress) return moe_select_strategy(m, par, cl, curves, ov, n_cap, out);
+  if (!m || !par || !cl || !curves || !out) return fail(MOE_ERR_INVALID_ARGUMENT, "select_strategy: null argument");
+  if (par->t == 1) return moe_select_strategy(m, par, cl, curves, ov, n_cap, out);  // baseline only
+  const double volume = volume_of(m);
+  moe_strategy_decision d{};
+  double t1;
+  if (moe_status st = moe_o1_time(volume, par->t, par->e, cl->b1, cl->b2, curves, ov, &t1)) return st;
+  d.alternatives[d.n_alternatives++] = moe_strategy_alt{MOE_O1, t1, 1};
+  if (par->e >= 2) {
+    moe_chunk_search_result r2, r3;
+    if (moe_status st = search(m, par, cl, curves, ov, n_cap, score_shared_o2, &r2)) return st;
+    d.alternatives[d.n_alternatives++] = moe_strategy_alt{MOE_O2, r2.t_pred, r2.n_opt};
+    if (moe_status st = search(m, par, cl, curves, ov, n_cap, score_shared_o3, &r3)) return st;
+    d.alternatives[d.n_alternatives++] = moe_strategy_alt{MOE_O3, r3.t_pred, r3.n_opt};
+  }
+  int best = 0;
+  for (int i = 1; i < d.n_alternatives; ++i)
+    if (d.alternatives[i].t_pred < d.alternatives[best].t_pred) best = i;
+  d.level = d.alternatives[best].level;
+  d.n = d.alternatives[best].n;
+  d.t_pred = d.alternatives[best].t_pred;
+  *out = d;
+  return MOE_OK;
+}
+
 extern "C" moe_status moe_estimate_performance(const moe_strategy_decision* d, const moe_model_spec* m,
                                                const moe_parallel_spec* par, const moe_cluster_spec* cl,
                                                int32_t moe_layer_count, double non_comm_time,

@@ -177,6 +177,15 @@ class MoeLayer:
         self._experts[card] = (w13, w2)  # keep the weights alive while bound
         check(self.lib.moe_ctx_bind_experts(self._ctx, card, w13.data_ptr(), w2.data_ptr(), w13.shape[1] // 2))
 
+    def autotune(self, candidates, steps: int = 5, stream=None):
+        """moe_ctx_autotune: time each (level, n, landing) in place (max over ranks);
+        returns (index of the fastest, [us/layer per candidate])."""
+        arr = (_lib.Schedule * len(candidates))(*[_lib.Schedule(int(lv), int(n), int(ld), 0.0)
+                                                   for lv, n, ld in candidates])
+        best = C.c_int32()
+        check(self.lib.moe_ctx_autotune(self._ctx, arr, len(candidates), steps, _stream_ptr(stream), C.byref(best)))
+        return int(best.value), [arr[i].us for i in range(len(candidates))]
+
     def enable_comm_gate(self, enable: bool = True) -> None:
         """Mark the context EP-busy during every forward (monta.h 1d)."""
         check(self.lib.moe_ctx_enable_comm_gate(self._ctx, int(enable)))

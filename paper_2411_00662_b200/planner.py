@@ -262,6 +262,20 @@ def select_strategy(model: ModelSpec, par: ParallelSpec, cluster: ClusterSpec, c
     return StrategyDecision(StrategyLevel(d.level), d.n, d.t_pred, alts)
 
 
+def select_strategy_b200(model: ModelSpec, par: ParallelSpec, cluster: ClusterSpec, curves: CurveSet,
+                         ov: OverheadModel = OverheadModel(), n_cap: int = 64,
+                         shared_egress: bool = True) -> StrategyDecision:
+    """B200 variant (monta.h): AllToAll and AllGather serialise on one NVSwitch
+    box's shared NVLink egress; shared_egress=False is select_strategy."""
+    d = _lib.StrategyDecision()
+    check(_L().moe_select_strategy_b200(C.byref(model._c()), C.byref(par._c()), C.byref(cluster._c()),
+                                        C.byref(curves._c()), C.byref(ov._c()), n_cap, int(shared_egress),
+                                        C.byref(d)))
+    alts = [StrategyAlternative(StrategyLevel(d.alternatives[i].level), d.alternatives[i].t_pred,
+                                d.alternatives[i].n) for i in range(d.n_alternatives)]
+    return StrategyDecision(StrategyLevel(d.level), d.n, d.t_pred, alts)
+
+
 def estimate_performance(decision: StrategyDecision, model: ModelSpec, par: ParallelSpec, cluster: ClusterSpec,
                          moe_layer_count: int, non_comm_time: float) -> PerfReport:
     d = _lib.StrategyDecision()

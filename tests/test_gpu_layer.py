@@ -394,3 +394,23 @@ def test_top1_wide_rows(cuda, e, t, level):
     """Top-1 routing over rows of >= 2048 columns per slice takes the 4 KiB-item
     top-1 un-permute (the 2x70B config's shape class)."""
     _run(e, t, 2 * e, 1, 300, 2048 * t, torch.bfloat16, level, 1 if level != O3 else 2, LAND_FINAL, seed=7 + e + t)
+
+
+def test_autotune_picks_a_measured_candidate(cuda):
+    """moe_ctx_autotune times every candidate in place and returns the fastest
+    (times written back); invalid candidates are rejected before any run."""
+    layer = MoeLayer(2, 2, 8, 2, 512, 256, dtype=torch.bfloat16, max_chunks=8)
+    try:
+        for cd in layer.cards:
+            cd.logits.normal_()
+            cd.x.normal_()
+        cands = [(O1, 1, LAND_FINAL), (O2, 4, LAND_FINAL), (O3, 2, LAND_STAGED), (BASELINE, 1, LAND_FINAL)]
+        best, times = layer.autotune(cands, steps=3)
+        assert 0 <= best < len(cands) and all(t > 0 for t in times)
+        assert times[best] == min(times)
+        with pytest.raises(ValueError):
+            layer.autotune([(O1, 3, LAND_FINAL)])  # O1 is unchunked
+        layer.forward(*cands[best])
+        layer.sync()
+    finally:
+        layer.close()

@@ -315,3 +315,32 @@ def test_planner_matches_reference_golden_fixtures():
             r = fn(m, par, cl, cs, ov, n_cap)
             assert (r.n_opt, r.feasible) == (int(d[p + key][0]), bool(d[p + key][2]))
             assert r.t_pred == pytest.approx(float(d[p + key][1]), rel=1e-12)
+
+
+def test_b200_shared_egress_variant():
+    """moe_select_strategy_b200: with shared_egress off it is the reference's
+    select_strategy; on, chunked levels score n*(aa+ag) + d2d (+ O2's copy
+    backlog) — the AllToAll and the AllGather serialise on one NVSwitch box's
+    egress — through the same gates and tie order."""
+    rng = random.Random(5)
+    for _ in range(200):
+        curves = CurveSet(EfficiencyCurve([CurvePoint(1e5, rng.uniform(0.05, 1)), CurvePoint(1e8, rng.uniform(0.05, 1))]),
+                          EfficiencyCurve([CurvePoint(1e5, rng.uniform(0.05, 1)), CurvePoint(1e8, rng.uniform(0.05, 1))]),
+                          EfficiencyCurve.constant(rng.uniform(0.3, 1)))
+        model = ModelSpec(b=1, s=rng.randint(1, 65536), h=4096, bpe=2)
+        par = ParallelSpec(t=rng.choice([1, 2, 4, 8]), e=rng.choice([1, 2, 4]))
+        cl = ClusterSpec(nodes=2, gpus_per_node=8, b1=rng.uniform(1e10, 8e11), b2=8e11, b3=7e12, peak_flops=1e15)
+        ov = P.OverheadModel(rng.choice([0.0, 1e-5]), rng.choice([0.0, 5e-6]))
+        ref = P.select_strategy(model, par, cl, curves, ov, n_cap=16)
+        off = P.select_strategy_b200(model, par, cl, curves, ov, n_cap=16, shared_egress=False)
+        assert (off.level, off.n, off.t_pred) == (ref.level, ref.n, ref.t_pred)
+        on = P.select_strategy_b200(model, par, cl, curves, ov, n_cap=16, shared_egress=True)
+        assert on.t_pred == min(a.t_pred for a in on.alternatives)
+        if par.t >= 2:
+            o1 = P.o1_time(P.traffic_volume(model), par.t, par.e, cl.b1, cl.b2, curves, ov)
+            assert on.alternatives[0].t_pred == pytest.approx(o1, rel=1e-12)
+            for a in on.alternatives[1:]:
+                # no overlap across the shared egress: a chunked level never beats n = 1 of itself
+                assert a.t_pred >= min(x.t_pred for x in on.alternatives) - 1e-18
+        else:
+            assert (on.level, on.n) == (ref.level, ref.n)
