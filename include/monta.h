@@ -358,6 +358,15 @@ moe_status moe_ctx_autotune(moe_ctx* ctx, moe_schedule* candidates, int32_t coun
 moe_status moe_ctx_forward_host(moe_ctx* ctx, int level, int32_t n_chunks, int landing,
                                 const void* host_x, const void* host_logits, void* host_out,
                                 void* stream);
+/* Routing checks (the reference's CorruptRoutingError, dataplane.hpp:18-20):
+ * when enabled, every dispatch first poisons the receive tags, and
+ * moe_ctx_forward (or moe_ctx_verify after moe_ctx_dispatch) checks every
+ * landed row's tags {source card, position, expert} against the receiving
+ * node's reference layout (expert-major, sources ascending, positions
+ * ascending) on the device; a lost, duplicated or misplaced row raises
+ * MOE_ERR_CORRUPT_ROUTING at the next moe_ctx_sync. */
+moe_status moe_ctx_enable_checks(moe_ctx* ctx, int enable);
+moe_status moe_ctx_verify(moe_ctx* ctx, void* stream);
 /* Rows in card's recv buffer after the last dispatch (synchronises). */
 moe_status moe_ctx_recv_rows(moe_ctx* ctx, int card, int64_t* rows);
 /* Synchronise the context's streams and report device-side errors

@@ -115,6 +115,7 @@ struct moe_ctx {
   int32_t* ep_busy = nullptr;
   bool gate = false;
   uint64_t tune_epoch = 0;
+  bool checks = false;  // poison + verify the landed rows' tags every dispatch (moe_ctx_enable_checks)
   struct GraphEntry {
     int level, n, landing;
     const void *hx, *hl;
@@ -1105,6 +1106,8 @@ moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t
     c->span_used = 0;
     record_timing(c->ev_base, s);
   }
+  if (c->checks)  // poisoned tags: a row that never lands fails verify_dispatch
+    for (auto& cd : c->local) MONTA_CUDA(cudaMemsetAsync(cd.v.recv_tags, 0xff, size_t(c->recv_cap) * 16, s));
   if (moe_status st = do_front(c, route, level, n, landing, s)) return st;
 
   if (is_virtual(c)) {
@@ -1480,6 +1483,20 @@ moe_status forward_host_pipelined(moe_ctx* c, int level, int landing, const void
   return MOE_OK;
 }
 
+// Routing check of the last dispatch (checks enabled): every landed row's
+// tags against the receiving node's reference layout (verify.cu).
+moe_status verify_dispatch(moe_ctx* c, cudaStream_t s) {
+  if (!c->checks) return MOE_OK;
+  if (!is_virtual(c))
+    if (moe_status st = dispatch_tail_wait(c, c->local[0], c->last_level, c->last_n, MOE_LAND_FINAL, s)) return st;
+  for (auto& cd : c->local) {
+    MONTA_CUDA(launch_verify_recv(cd.v.recv_tags, cd.recv_rows, cd.v.recv_expert_offsets, c->L, cd.node, c->d.e,
+                                  c->d.t, c->d.tokens, c->recv_cap, cd.err, s));
+    ++c->launches;
+  }
+  return MOE_OK;
+}
+
 // Bound experts between dispatch and combine.  Multi-GPU:
 // the persistent dispatch returns before the peers' rows have landed, so the
 // experts first wait for every incoming chunk (the flags the combine would
@@ -1534,6 +1551,7 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
   moe_status st = dispatch_impl(c, level, n, landing, s, true);
   c->in_forward = false;
   if (st != MOE_OK) return st;
+  if (moe_status st0 = verify_dispatch(c, s)) return st0;
   if (moe_status st1 = experts_impl(c, s)) return st1;
   if (moe_status st2 = combine_impl(c, level, n, s)) return st2;
   if (c->gate) MONTA_CUDA(cudaMemsetAsync(c->ep_busy, 0, 4, s));  // EP phase over: gated DP traffic may go
@@ -1613,6 +1631,24 @@ __global__ void k_comm_gate(const volatile int32_t* busy, int32_t* err) {
   }
 }
 }  // namespace monta
+
+extern "C" moe_status moe_ctx_enable_checks(moe_ctx* c, int enable) {
+  if (moe_status st = check_ready(c)) return st;
+  if (c->checks != (enable != 0)) {
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+  }
+  c->checks = enable != 0;
+  return MOE_OK;
+}
+
+extern "C" moe_status moe_ctx_verify(moe_ctx* c, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (!c->checks) return fail(MOE_ERR_INVALID_ARGUMENT, "verify: checks not enabled (moe_ctx_enable_checks)");
+  MONTA_CUDA(cudaSetDevice(c->device));
+  return verify_dispatch(c, static_cast<cudaStream_t>(stream));
+}
 
 extern "C" moe_status moe_ctx_enable_comm_gate(moe_ctx* c, int enable) {
   if (moe_status st = check_ready(c)) return st;
@@ -1760,6 +1796,8 @@ extern "C" moe_status moe_ctx_sync(moe_ctx* c) {
       if (e == MOE_ERR_TIMEOUT) return fail(MOE_ERR_TIMEOUT, "card %d: cross-GPU flag wait timed out", cd.id);
       if (e == MOE_ERR_INVALID_ARGUMENT)
         return fail(MOE_ERR_INVALID_ARGUMENT, "card %d: expert id out of range in the routing", cd.id);
+      if (e == MOE_ERR_CORRUPT_ROUTING)
+        return fail(MOE_ERR_CORRUPT_ROUTING, "card %d: a dispatched row is missing or out of place (tag check)", cd.id);
       return fail(moe_status(e), "card %d: device error %d", cd.id, e);
     }
   }

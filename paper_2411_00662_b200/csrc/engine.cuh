@@ -192,6 +192,8 @@ struct PlanArgs {
 };
 size_t plan_scratch_ints(int e, int E, int max_chunks);
 moe_status configure_grouped_gemm();  // experts.cu
+cudaError_t launch_verify_recv(const int32_t* tags, const int64_t* recv_rows, const int32_t* offs, int L, int node,
+                               int e, int t, int64_t T, int64_t cap, int32_t* err, cudaStream_t s);  // verify.cu
 bool plan_fits_smem(int e, int E, int n);
 moe_status configure_plan();
 cudaError_t launch_plan_with_scratch(const PlanArgs& a, int32_t* scratch, cudaStream_t s);

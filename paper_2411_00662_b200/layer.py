@@ -186,6 +186,13 @@ class MoeLayer:
         check(self.lib.moe_ctx_autotune(self._ctx, arr, len(candidates), steps, _stream_ptr(stream), C.byref(best)))
         return int(best.value), [arr[i].us for i in range(len(candidates))]
 
+    def enable_checks(self, enable: bool = True) -> None:
+        """Poison + verify the landed rows' tags every dispatch (CorruptRoutingError on failure)."""
+        check(self.lib.moe_ctx_enable_checks(self._ctx, int(enable)))
+
+    def verify(self, stream=None) -> None:
+        check(self.lib.moe_ctx_verify(self._ctx, _stream_ptr(stream)))
+
     def enable_comm_gate(self, enable: bool = True) -> None:
         """Mark the context EP-busy during every forward (monta.h 1d)."""
         check(self.lib.moe_ctx_enable_comm_gate(self._ctx, int(enable)))

@@ -414,3 +414,45 @@ def test_autotune_picks_a_measured_candidate(cuda):
         layer.sync()
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("e,t,E,k,level,n,landing", [
+    (2, 2, 8, 2, O1, 1, LAND_FINAL), (2, 2, 8, 2, O2, 4, LAND_STAGED), (4, 2, 160, 6, O3, 2, LAND_FINAL),
+    (1, 1, 160, 6, BASELINE, 1, LAND_FINAL), (2, 1, 4, 2, BASELINE, 1, LAND_FINAL)])
+def test_routing_checks_pass_and_catch_corruption(cuda, e, t, E, k, level, n, landing):
+    """moe_ctx_enable_checks: a clean layer passes the device tag check on every
+    step; a landed row moved out of place (or lost) raises CorruptRoutingError
+    (the reference's exception, dataplane.hpp:18-20) at the next sync."""
+    layer = MoeLayer(e, t, E, k, 256, 128, dtype=torch.bfloat16, max_chunks=max(n, 1))
+    try:
+        layer.enable_checks(True)
+        for cd in layer.cards:
+            cd.logits.normal_()
+            cd.x.normal_()
+        for _ in range(2):
+            layer.forward(level, n, landing)
+            layer.sync()
+        layer.dispatch(level, n, landing)
+        layer.verify()
+        layer.sync()
+        cd = layer.cards[-1]
+        rows = layer.recv_rows(cd.card)
+        assert rows >= 2
+        tags = cd.recv_tags[:rows].clone()
+        cd.recv_tags[0].copy_(tags[1])            # two rows swapped: out of order
+        cd.recv_tags[1].copy_(tags[0])
+        layer.verify()
+        with pytest.raises(_lib.CorruptRoutingError):
+            layer.sync()
+        cd.recv_tags[:rows].copy_(tags)
+        cd.recv_tags[rows - 1].fill_(-1)          # a row that never landed
+        layer.verify()
+        with pytest.raises(_lib.CorruptRoutingError):
+            layer.sync()
+        cd.recv_tags[:rows].copy_(tags)
+        layer.verify()
+        layer.sync()
+        layer.combine(level, n)
+        layer.sync()
+    finally:
+        layer.close()
