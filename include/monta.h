@@ -190,18 +190,11 @@ moe_status moe_comm_stream_priority(int group, int device, int* cuda_priority);
 /* A non-blocking stream on the current device with that priority. */
 moe_status moe_comm_stream_create(int group, void** stream);
 moe_status moe_comm_stream_destroy(void* stream);
-/* Stream priority orders CTA scheduling, not the shared links: measured on a
- * B200 box, a concurrent DP all-reduce slows the EP layer the same at either
- * priority.  The conflict resolution itself (resolve_by_priority,
- * conflict.hpp:113-142: the lower-priority event slides right until it
- * overlaps no EP event) is the gate: with the gate enabled every
- * moe_ctx_forward marks the context EP-busy (stream-ordered, captured in its
- * graph) from its first kernel to its last; moe_comm_gate_wait enqueues on a
- * lower-priority group's stream a wait until the EP phase is idle — issue it
- * before each chunk of DP/PP/CP traffic. */
-typedef struct moe_ctx moe_ctx;
-moe_status moe_ctx_enable_comm_gate(moe_ctx* ctx, int enable);
-moe_status moe_comm_gate_wait(moe_ctx* ctx, void* stream);
+/* Measured on a B200 box (scripts/micro/priority_bench.py): stream priority
+ * orders CTA scheduling, not the shared NVLink ports — a concurrent DP
+ * all-reduce slows the EP layer the same at either priority; sequencing the
+ * lower-priority traffic after the EP phase (resolve_by_priority) is the
+ * caller's stream order. */
 
 /* ------------------------------------------------------------------------
  * 1c. Expert compute between dispatch and combine (

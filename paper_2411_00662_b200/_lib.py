@@ -181,10 +181,8 @@ SIGNATURES = {
     "moe_ctx_bind_experts": (C.c_int, [_P, C.c_int, _P, _P, _I64]),
     "moe_ctx_experts": (C.c_int, [_P, _P]),
     "moe_comm_priority": (C.c_int, [C.c_int]),
-    "moe_ctx_enable_comm_gate": (C.c_int, [_P, C.c_int]),
     "moe_ctx_enable_checks": (C.c_int, [_P, C.c_int]),
     "moe_ctx_verify": (C.c_int, [_P, _P]),
-    "moe_comm_gate_wait": (C.c_int, [_P, _P]),
     "moe_comm_stream_priority": (C.c_int, [C.c_int, C.c_int, _P]),
     "moe_comm_stream_create": (C.c_int, [C.c_int, _P]),
     "moe_comm_stream_destroy": (C.c_int, [_P]),

@@ -111,9 +111,6 @@ struct moe_ctx {
   bool debug = false;          // record front-kernel phase timestamps
   bool use_graphs = false;
   bool use_xchg = true;  // persistent role-specialised exchange kernels (multi-GPU)
-  // EP-busy gate (monta.h 1d): nonzero while a forward's EP traffic is in flight
-  int32_t* ep_busy = nullptr;
-  bool gate = false;
   uint64_t tune_epoch = 0;
   bool checks = false;  // poison + verify the landed rows' tags every dispatch (moe_ctx_enable_checks)
   struct GraphEntry {
@@ -448,7 +445,6 @@ extern "C" moe_status moe_ctx_destroy(moe_ctx* c) {
     cudaFree(cd.slab);
     if (cd.ffn_ws) cudaFree(cd.ffn_ws);
   }
-  if (c->ep_busy) cudaFree(c->ep_busy);
   for (auto& sp : c->spans) {
     cudaEventDestroy(sp.a);
     cudaEventDestroy(sp.b);
@@ -1546,7 +1542,6 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
     c->span_used = 0;
     record_timing(c->ev_base, s);
   }
-  if (c->gate) MONTA_CUDA(cudaMemsetAsync(c->ep_busy, 1, 4, s));  // EP phase begins
   c->in_forward = true;
   moe_status st = dispatch_impl(c, level, n, landing, s, true);
   c->in_forward = false;
@@ -1554,7 +1549,6 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
   if (moe_status st0 = verify_dispatch(c, s)) return st0;
   if (moe_status st1 = experts_impl(c, s)) return st1;
   if (moe_status st2 = combine_impl(c, level, n, s)) return st2;
-  if (c->gate) MONTA_CUDA(cudaMemsetAsync(c->ep_busy, 0, 4, s));  // EP phase over: gated DP traffic may go
   if (ho)
     for (size_t i = 0; i < c->local.size(); ++i)
       MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(ho) + i * obytes, c->local[i].v.out, obytes,
@@ -1615,23 +1609,6 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
 
 }  // namespace
 
-namespace monta {
-// A lower-priority group's stream waits here until the context's EP phase is
-// idle (resolve_by_priority, conflict.hpp:113-142: the lower-priority event
-// slides right until it overlaps no EP event).
-__global__ void k_comm_gate(const volatile int32_t* busy, int32_t* err) {
-  if (threadIdx.x != 0) return;
-  const unsigned long long t0 = globaltimer();
-  while (*busy != 0) {
-    if (globaltimer() - t0 > kWaitTimeoutNs) {
-      atomicExch(err, int32_t(MOE_ERR_TIMEOUT));
-      return;
-    }
-    __nanosleep(256);
-  }
-}
-}  // namespace monta
-
 extern "C" moe_status moe_ctx_enable_checks(moe_ctx* c, int enable) {
   if (moe_status st = check_ready(c)) return st;
   if (c->checks != (enable != 0)) {
@@ -1648,31 +1625,6 @@ extern "C" moe_status moe_ctx_verify(moe_ctx* c, void* stream) {
   if (!c->checks) return fail(MOE_ERR_INVALID_ARGUMENT, "verify: checks not enabled (moe_ctx_enable_checks)");
   MONTA_CUDA(cudaSetDevice(c->device));
   return verify_dispatch(c, static_cast<cudaStream_t>(stream));
-}
-
-extern "C" moe_status moe_ctx_enable_comm_gate(moe_ctx* c, int enable) {
-  if (moe_status st = check_ready(c)) return st;
-  MONTA_CUDA(cudaSetDevice(c->device));
-  if (enable && !c->ep_busy) {
-    MONTA_CUDA(cudaMalloc(&c->ep_busy, 16));
-    MONTA_CUDA(cudaMemset(c->ep_busy, 0, 16));
-  }
-  if (c->gate != (enable != 0)) {  // captured steps differ by the gate's memset nodes
-    for (auto& g : c->graphs)
-      if (g.exec) cudaGraphExecDestroy(g.exec);
-    c->graphs.clear();
-  }
-  c->gate = enable != 0;
-  return MOE_OK;
-}
-
-extern "C" moe_status moe_comm_gate_wait(moe_ctx* c, void* stream) {
-  if (moe_status st = check_ready(c)) return st;
-  if (!c->gate) return fail(MOE_ERR_INVALID_ARGUMENT, "comm_gate_wait: gate not enabled (moe_ctx_enable_comm_gate)");
-  MONTA_CUDA(cudaSetDevice(c->device));
-  k_comm_gate<<<1, 32, 0, static_cast<cudaStream_t>(stream)>>>(c->ep_busy, c->local[0].err);
-  MONTA_CHECK_LAUNCH("comm_gate_wait");
-  return MOE_OK;
 }
 
 extern "C" moe_status moe_ctx_forward(moe_ctx* c, int level, int32_t n, int landing, void* stream) {

@@ -193,14 +193,6 @@ class MoeLayer:
     def verify(self, stream=None) -> None:
         check(self.lib.moe_ctx_verify(self._ctx, _stream_ptr(stream)))
 
-    def enable_comm_gate(self, enable: bool = True) -> None:
-        """Mark the context EP-busy during every forward (monta.h 1d)."""
-        check(self.lib.moe_ctx_enable_comm_gate(self._ctx, int(enable)))
-
-    def comm_gate_wait(self, stream=None) -> None:
-        """Enqueue on `stream` (a DP/PP/CP stream) a wait until the EP phase is idle."""
-        check(self.lib.moe_comm_gate_wait(self._ctx, _stream_ptr(stream)))
-
     def experts(self, stream=None) -> None:
         check(self.lib.moe_ctx_experts(self._ctx, _stream_ptr(stream)))
 

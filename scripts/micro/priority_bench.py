@@ -52,10 +52,9 @@ def main():
 
     def run(mode):
         dp = None
-        layer.enable_comm_gate(mode == "gated")
         if mode == "equal":
             dp = torch.cuda.Stream(priority=ops.comm_stream_priority(_lib.COMM_EP))
-        elif mode in ("mapped", "gated"):
+        elif mode == "mapped":
             dp = ops.comm_stream(_lib.COMM_DP)
         for _ in range(3):
             layer.forward(level, 1, 0, ep)
@@ -68,8 +67,6 @@ def main():
             with torch.cuda.stream(dp):
                 for _ in range(args.steps * 2):
                     for p in pieces:
-                        if mode == "gated":
-                            layer.comm_gate_wait(dp)  # DP yields to EP (resolve_by_priority)
                         dist.all_reduce(p)
             d1.record(dp)
         evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
@@ -101,7 +98,7 @@ def main():
            "stream_priorities": {n: ops.comm_stream_priority(gr) for n, gr in
                                  (("EP", _lib.COMM_EP), ("PP", _lib.COMM_PP), ("CP", _lib.COMM_CP),
                                   ("DP", _lib.COMM_DP), ("TP_SP", _lib.COMM_TP_SP))}}
-    for mode in ("alone", "equal", "mapped", "gated", "alone"):
+    for mode in ("alone", "equal", "mapped", "alone"):
         lay, dp_us = run(mode)
         out.setdefault("layer_us_median", {}).setdefault(mode, []).append(lay)
         if dp_us is not None:
