@@ -95,36 +95,57 @@ __device__ __forceinline__ void sum_hists(const int32_t* hist, int rows, int E, 
   const int N = (tot ? rows : b_pre) * E;
   const double inv_tpc = 1.0 / double(tpc);
   int row = threadIdx.x / E, x = threadIdx.x - (threadIdx.x / E) * E;
-  if (dr == 0 && (cnt == nullptr || (n == 1 && tpc >= rows))) {
-    // common case: every thread keeps one expert x; sum in registers, fold
-    // the lanes of a warp that share x, then one shared atomic per (warp, x)
-    // (per-value atomics were 64-way conflicts on E addresses: ~1 us)
+  if (dq >= 1 && (cnt == nullptr || tpc >= 1)) {
+    // common case: the first dq*E threads each keep one expert x (the rest
+    // idle, so E need not divide the block); sum in registers (16 loads in
+    // flight per thread), fold the lanes of a warp that share x, then one
+    // shared atomic per (warp, x) (per-value atomics were 64-way conflicts on
+    // E addresses: ~1 us; the per-element path for E = 160 cost ~5 us)
+    // Chunk counts (cnt): tiles are chunk-aligned, chunk j = row / tpc; the
+    // running count flushes with one atomic when the thread's row crosses a
+    // chunk boundary (no division in the loop).
+    constexpr int kF = 16;
+    const int span = dq * E;
     int st = 0, sp = 0;
-    for (int base = threadIdx.x; base < N; base += kB * bd) {
-      int v[kB];
-#pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        const int i = base + u * bd;
-        v[u] = i < N ? __ldcg(hist + i) : 0;
+    int cj = 0, crun = 0, cnext = tpc;
+    if (int(threadIdx.x) < span) {
+      if (cnt) {
+        cj = row / tpc;
+        cnext = (cj + 1) * tpc;
       }
+      for (int base = threadIdx.x; base < N; base += kF * span) {
+        int v[kF];
 #pragma unroll
-      for (int u = 0; u < kB; ++u) {
-        st += v[u];
-        sp += row < b_pre ? v[u] : 0;
-        row += dq;
+        for (int u = 0; u < kF; ++u) {
+          const int i = base + u * span;
+          v[u] = i < N ? __ldcg(hist + i) : 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kF; ++u) {
+          st += v[u];
+          sp += row < b_pre ? v[u] : 0;
+          if (cnt) {
+            if (row >= cnext) {
+              if (crun && cj < n) atomicAdd(cnt + cj * E + x, crun);
+              cj = row / tpc;
+              cnext = (cj + 1) * tpc;
+              crun = 0;
+            }
+            crun += v[u];
+          }
+          row += dq;
+        }
       }
+      if (cnt && crun && cj < n) atomicAdd(cnt + cj * E + x, crun);
     }
-    if (32 % E == 0) {
+    if (dr == 0 && 32 % E == 0) {  // every lane active: fold lanes sharing x
       for (int off = 16; off >= E; off >>= 1) {
         st += __shfl_xor_sync(0xffffffffu, st, off);
         sp += __shfl_xor_sync(0xffffffffu, sp, off);
       }
       if ((threadIdx.x & 31) >= E) st = sp = 0;
     }
-    if (st) {
-      if (tot) atomicAdd(tot + x, st);
-      if (cnt) atomicAdd(cnt + x, st);  // one chunk holding every tile
-    }
+    if (st && tot) atomicAdd(tot + x, st);
     if (sp && pre) atomicAdd(pre + x, sp);
     return;
   }
@@ -502,7 +523,11 @@ moe_status launch_e(const FrontArgs* a, int E, cudaStream_t s, bool configure) {
   if (E <= 16) return launch_t<T, 16, 1>(a, s, configure);
   if (E <= 32) return launch_t<T, 32, 1>(a, s, configure);
   if (E <= 64) return launch_t<T, 32, 2>(a, s, configure);
+  if (E <= 96) return launch_t<T, 32, 3>(a, s, configure);
   if (E <= 128) return launch_t<T, 32, 4>(a, s, configure);
+  if (E <= 160) return launch_t<T, 32, 5>(a, s, configure);
+  if (E <= 192) return launch_t<T, 32, 6>(a, s, configure);
+  if (E <= 224) return launch_t<T, 32, 7>(a, s, configure);
   if (E <= 256) return launch_t<T, 32, 8>(a, s, configure);
   if (E <= 512) return launch_t<T, 32, 16>(a, s, configure);
   return launch_t<T, 32, 32>(a, s, configure);

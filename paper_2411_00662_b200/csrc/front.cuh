@@ -60,33 +60,33 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
   }
 #pragma unroll
   for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(gmask, sum, off, G);
-  unsigned taken = 0;
-  int my_sel = -1;
-  T my_soft = T(0);
   if constexpr (sizeof(T) == 4) {
-    // fp32 scores: a lane's best candidate is an order-preserving 32-bit key;
-    // the group argmax is one max-reduction (redux.sync for whole warps, a
-    // packed 64-bit {key, ~index} shuffle tree for sub-warp groups) — ties go
-    // to the lower expert index in both
-    for (int s = 0; s < k; ++s) {
-      unsigned key = 0u;  // 0: no candidate (every real score maps above it)
-      unsigned bi = 0xffffffffu;
+    // fp32 scores: each entry's order-preserving 32-bit key is computed once
+    // (-0.0 canonicalised to +0.0 first: the reference compares values,
+    // scores[l] > scores[r] at dataplane.hpp:97-98, for which the two zeros
+    // tie and the lower index wins); a taken entry's key drops to 0 (every
+    // real score maps above it).  Per round: the lane's best key (strict >
+    // keeps its lower index on ties), then the group argmax — one redux.sync
+    // max/min pair for whole warps, a packed 64-bit {key, ~index} shuffle tree
+    // for sub-warp groups; ties go to the lower expert index in both.
+    unsigned u[PER];
 #pragma unroll
-      for (int m = 0; m < PER; ++m) {
-        const int x = sub + m * G;
-        if (x < E && !((taken >> m) & 1u)) {
-          // -0.0 is canonicalised to +0.0 first: the reference compares
-          // values (scores[l] > scores[r], dataplane.hpp:97-98), for which
-          // the two zeros tie and the lower index wins
-          unsigned b = __float_as_uint(float(v[m]));
-          b = (b == 0x80000000u) ? 0u : b;
-          const unsigned u = (b & 0x80000000u) ? ~b : (b | 0x80000000u);
-          if (u > key) {  // x ascends within the lane: strict > keeps the lower index on ties
-            key = u;
-            bi = unsigned(x);
-          }
+    for (int m = 0; m < PER; ++m) {
+      const int x = sub + m * G;
+      unsigned b = __float_as_uint(float(v[m]));
+      b = (b == 0x80000000u) ? 0u : b;
+      u[m] = x < E ? ((b & 0x80000000u) ? ~b : (b | 0x80000000u)) : 0u;
+    }
+    unsigned sel = 0;  // bit m: entry m (expert sub + m*G) selected
+    for (int s = 0; s < k; ++s) {
+      unsigned key = 0u, bm = 0u;
+#pragma unroll
+      for (int m = 0; m < PER; ++m)
+        if (u[m] > key) {
+          key = u[m];
+          bm = unsigned(m);
         }
-      }
+      const unsigned bi = key ? unsigned(sub) + bm * G : 0xffffffffu;
       unsigned wi;
       if constexpr (G == 32) {
         const unsigned mk = __reduce_max_sync(0xffffffffu, key);
@@ -100,18 +100,36 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
         }
         wi = 0xffffffffu - unsigned(pk & 0xffffffffull);
       }
-      T mine = T(0);
+      if (wi != 0xffffffffu && int(wi % G) == sub) {
+        const unsigned mw = wi / G;
 #pragma unroll
-      for (int m = 0; m < PER; ++m)
-        if (unsigned(sub + m * G) == wi) mine = ex[m];
-      const T bs = __shfl_sync(gmask, mine, (lane / G) * G + int(wi % G), kWarp);
-      if (int(wi % G) == sub) taken |= 1u << (wi / G);
-      if (sub == s) {
-        my_sel = int(wi);
-        my_soft = bs / sum;
+        for (int m = 0; m < PER; ++m)
+          if (unsigned(m) == mw) u[m] = 0u;
+        sel |= 1u << mw;
       }
     }
+    // experts leave in ascending order: entry (lane, m)'s slot is the number
+    // of selected entries of the group with a smaller index (ballots by m)
+    const int gshift = (lane / G) * G;
+    const unsigned lt = (1u << sub) - 1u;
+    int before = 0;
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const unsigned bal = __ballot_sync(0xffffffffu, (sel >> m) & 1u);
+      const unsigned gb = G == 32 ? bal : ((bal >> gshift) & ((1u << G) - 1u));
+      if (active && ((sel >> m) & 1u)) {
+        const int slot = before + __popc(gb & lt);
+        const int x = sub + m * G;
+        experts[token * k + slot] = x;
+        probs[token * k + slot] = ex[m] / sum;
+        if (s_exp) s_exp[(token - s_base) * k + slot] = x;  // the tile's mirror in shared memory
+      }
+      before += __popc(gb);
+    }
   } else {
+    unsigned taken = 0;
+    int my_sel = -1;
+    T my_soft = T(0);
     for (int s = 0; s < k; ++s) {
       T bv = neg_inf<T>();
       int bi = int(kNone);
@@ -145,16 +163,16 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
         my_soft = bs / sum;
       }
     }
-  }
-  int rank = 0;
-  for (int s = 0; s < k; ++s) {
-    const int other = __shfl_sync(gmask, my_sel, (lane / G) * G + s, kWarp);
-    if (other < my_sel) ++rank;
-  }
-  if (active && sub < k) {
-    experts[token * k + rank] = my_sel;
-    probs[token * k + rank] = my_soft;
-    if (s_exp) s_exp[(token - s_base) * k + rank] = my_sel;  // the tile's mirror in shared memory
+    int rank = 0;
+    for (int s = 0; s < k; ++s) {
+      const int other = __shfl_sync(gmask, my_sel, (lane / G) * G + s, kWarp);
+      if (other < my_sel) ++rank;
+    }
+    if (active && sub < k) {
+      experts[token * k + rank] = my_sel;
+      probs[token * k + rank] = my_soft;
+      if (s_exp) s_exp[(token - s_base) * k + rank] = my_sel;  // the tile's mirror in shared memory
+    }
   }
 }
 

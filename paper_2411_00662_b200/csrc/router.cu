@@ -33,7 +33,11 @@ cudaError_t route_dispatch(const T* logits, int64_t tokens, int E, int k, int32_
   if (E <= 16) return launch<T, 16, 1>(logits, tokens, E, k, experts, probs, s);
   if (E <= 32) return launch<T, 32, 1>(logits, tokens, E, k, experts, probs, s);
   if (E <= 64) return launch<T, 32, 2>(logits, tokens, E, k, experts, probs, s);
+  if (E <= 96) return launch<T, 32, 3>(logits, tokens, E, k, experts, probs, s);
   if (E <= 128) return launch<T, 32, 4>(logits, tokens, E, k, experts, probs, s);
+  if (E <= 160) return launch<T, 32, 5>(logits, tokens, E, k, experts, probs, s);
+  if (E <= 192) return launch<T, 32, 6>(logits, tokens, E, k, experts, probs, s);
+  if (E <= 224) return launch<T, 32, 7>(logits, tokens, E, k, experts, probs, s);
   if (E <= 256) return launch<T, 32, 8>(logits, tokens, E, k, experts, probs, s);
   if (E <= 512) return launch<T, 32, 16>(logits, tokens, E, k, experts, probs, s);
   return launch<T, 32, 32>(logits, tokens, E, k, experts, probs, s);
