@@ -401,9 +401,10 @@ def test_autotune_picks_a_measured_candidate(cuda):
     (times written back); invalid candidates are rejected before any run."""
     layer = MoeLayer(2, 2, 8, 2, 512, 256, dtype=torch.bfloat16, max_chunks=8)
     try:
+        x, logits = _inputs(2, 512, 256, 8, torch.bfloat16, 5)
         for cd in layer.cards:
-            cd.logits.normal_()
-            cd.x.normal_()
+            cd.x.copy_(x[cd.node])
+            cd.logits.copy_(logits[cd.node])
         cands = [(O1, 1, LAND_FINAL), (O2, 4, LAND_FINAL), (O3, 2, LAND_STAGED), (BASELINE, 1, LAND_FINAL)]
         best, times = layer.autotune(cands, steps=3)
         assert 0 <= best < len(cands) and all(t > 0 for t in times)
@@ -426,15 +427,28 @@ def test_routing_checks_pass_and_catch_corruption(cuda, e, t, E, k, level, n, la
     layer = MoeLayer(e, t, E, k, 256, 128, dtype=torch.bfloat16, max_chunks=max(n, 1))
     try:
         layer.enable_checks(True)
-        for cd in layer.cards:
-            cd.logits.normal_()
-            cd.x.normal_()
+        g = torch.Generator(device="cuda").manual_seed(e * 10 + t)
+        xs = [torch.randn(256, 128, generator=g, device="cuda").to(torch.bfloat16) for _ in range(e)]
+        ls = [torch.randn(256, E, generator=g, device="cuda") for _ in range(e)]
+        for cd in layer.cards:  # a node's TP ranks hold the same batch (the dedup relies on it)
+            cd.logits.copy_(ls[cd.node])
+            cd.x.copy_(xs[cd.node])
         for _ in range(2):
             layer.forward(level, n, landing)
             layer.sync()
         layer.dispatch(level, n, landing)
         layer.verify()
         layer.sync()
+        if t > 1:  # TP ranks routing differently (inconsistent replicas) is caught too
+            layer.cards[1].logits.copy_(torch.randn(256, E, generator=g, device="cuda"))
+            layer.forward(level, n, landing)
+            with pytest.raises(_lib.CorruptRoutingError):
+                layer.sync()
+            layer.cards[1].logits.copy_(ls[layer.cards[1].node])
+            layer.forward(level, n, landing)
+            layer.sync()
+            layer.dispatch(level, n, landing)
+            layer.sync()
         cd = layer.cards[-1]
         rows = layer.recv_rows(cd.card)
         assert rows >= 2
