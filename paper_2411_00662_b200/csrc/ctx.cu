@@ -1739,21 +1739,28 @@ extern "C" moe_status moe_ctx_sync(moe_ctx* c) {
   if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "sync: null ctx");
   MONTA_CUDA(cudaSetDevice(c->device));
   MONTA_CUDA(cudaDeviceSynchronize());
+  // every card's error word is read and cleared; the first error is reported
+  int32_t e = 0;
+  int first = -1;
   for (auto& cd : c->local) {
-    int32_t e = 0;
-    MONTA_CUDA(cudaMemcpy(&e, cd.err, 4, cudaMemcpyDeviceToHost));
-    if (e != 0) {
+    int32_t ec = 0;
+    MONTA_CUDA(cudaMemcpy(&ec, cd.err, 4, cudaMemcpyDeviceToHost));
+    if (ec != 0) {
       const int32_t zero = 0;
       cudaMemcpy(cd.err, &zero, 4, cudaMemcpyHostToDevice);
-      if (e == MOE_ERR_TIMEOUT) return fail(MOE_ERR_TIMEOUT, "card %d: cross-GPU flag wait timed out", cd.id);
-      if (e == MOE_ERR_INVALID_ARGUMENT)
-        return fail(MOE_ERR_INVALID_ARGUMENT, "card %d: expert id out of range in the routing", cd.id);
-      if (e == MOE_ERR_CORRUPT_ROUTING)
-        return fail(MOE_ERR_CORRUPT_ROUTING, "card %d: a dispatched row is missing or out of place (tag check)", cd.id);
-      return fail(moe_status(e), "card %d: device error %d", cd.id, e);
+      if (first < 0) {
+        first = cd.id;
+        e = ec;
+      }
     }
   }
-  return MOE_OK;
+  if (first < 0) return MOE_OK;
+  if (e == MOE_ERR_TIMEOUT) return fail(MOE_ERR_TIMEOUT, "card %d: cross-GPU flag wait timed out", first);
+  if (e == MOE_ERR_INVALID_ARGUMENT)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "card %d: expert id out of range in the routing", first);
+  if (e == MOE_ERR_CORRUPT_ROUTING)
+    return fail(MOE_ERR_CORRUPT_ROUTING, "card %d: a dispatched row is missing or out of place (tag check)", first);
+  return fail(moe_status(e), "card %d: device error %d", first, e);
 }
 
 extern "C" moe_status moe_ctx_enable_timing(moe_ctx* c, int enable) {
