@@ -69,7 +69,7 @@ struct Card {
   unsigned long long* dbg = nullptr;  // front-kernel phase timestamps (debug)
   int32_t* tile_hist = nullptr;       // [n_tiles][E]
   int32_t* tile_base = nullptr;       // [n_tiles][E]
-  int32_t* counts_acc = nullptr;      // [max_chunks][E]
+  int32_t* counts_acc = nullptr;      // [2][max_chunks][E] (epoch parity)
   unsigned* arrive = nullptr;         // front grid barrier
   unsigned long long* ready = nullptr;
   unsigned* xchg_counters = nullptr;  // [4][max_chunks] persistent-exchange chunk counters
@@ -184,7 +184,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   const int64_t tiles = (T + front_router_tokens(int(E)) - 1) / front_router_tokens(int(E));
   s.tile_hist = take(size_t(tiles) * E * 4);
   s.tile_base = take(size_t(tiles) * E * 4);
-  s.counts_acc = take(size_t(d.max_chunks) * E * 4);
+  s.counts_acc = take(size_t(2) * d.max_chunks * E * 4);
   s.arrive = take(16);
   s.ready = take(16);
   s.xchg_counters = take(size_t(8) * d.max_chunks * 17 * 4);  // [dispatch 4 + combine 2 legs][chunk][1 + 16 groups]

@@ -224,7 +224,8 @@ struct FrontArgs {
   int32_t aligned;      // (T / n) % tile_tokens == 0: chunk counts from tile histograms
   int32_t* tile_hist;   // [n_tiles][E]
   int32_t* tile_base;   // [n_tiles][E]
-  int32_t* counts_acc;  // [n][E] atomically accumulated when !aligned (zero between launches)
+  int32_t* counts_acc;  // [2][max_chunks][E] chunk counts accumulated by the tile CTAs; buffer epoch & 1
+                        // is this launch's, the other is zeroed for the next
   unsigned int* arrive; // grid-barrier arrival counter (zero between launches)
   unsigned long long* ready;  // grid-barrier release flag (= epoch)
   uint64_t* epoch_dev;  // bumped once per dispatch

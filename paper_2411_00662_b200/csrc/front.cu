@@ -207,17 +207,25 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
   int* offs = W;            // [E+1]
   int* ctot = W + E + 1;    // [33]
   int* cnt = ctot + 33;     // [n][E]
+  (void)ct;
+  (void)nt;
+  // chunk counts: the tile CTAs accumulated them (one atomic per tile and
+  // expert) into this launch's parity buffer; the other buffer is zeroed for
+  // the next launch (every reader of it finished in the previous one)
+  const int32_t* acc = a.counts_acc + size_t(epoch & 1ull) * a.max_chunks * E;
+  int32_t* other = a.counts_acc + size_t((epoch + 1ull) & 1ull) * a.max_chunks * E;
   #pragma unroll 1
-  for (int i = tid; i < E + 1 + 33 + n * E; i += blockDim.x) W[i] = 0;
+  for (int q = tid; q < n * E; q += blockDim.x) {
+    cnt[q] = __ldcg(acc + q);
+    other[q] = 0;
+  }
   __syncthreads();
-  const int tpc = ct > 0 ? int(ct / a.tile_tokens) : 0;  // tiles per chunk (aligned)
-  sum_hists(a.tile_hist, nt, E, offs, nullptr, 0, a.aligned && tpc > 0 ? cnt : nullptr, tpc > 0 ? tpc : 1, n);
-  if (!a.aligned)
-    #pragma unroll 1
-    for (int q = tid; q < n * E; q += blockDim.x) {
-      cnt[q] = __ldcg(a.counts_acc + q);
-      a.counts_acc[q] = 0;
-    }
+  #pragma unroll 1
+  for (int x = tid; x < E; x += blockDim.x) {
+    int sum = 0;
+    for (int j = 0; j < n; ++j) sum += cnt[j * E + x];
+    offs[x] = sum;
+  }
   __syncthreads();
   // count exchange: this node's [n][E] block of every EP peer's table, as
   // 8-byte {count | epoch << 32} words — each word is single-copy atomic, so a
@@ -334,6 +342,8 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const __grid_constant__
         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
     }
   }
+  // this launch's chunk-count buffer (epoch parity; control_tail zeroes the other)
+  int32_t* cacc = a.counts_acc + size_t((*a.epoch_dev + 1ull) & 1ull) * a.max_chunks * E;
   // ---------------- phase 1: route + tile histograms (tile CTAs)
   if (!control) {
     for (int b = blockIdx.x; b < nt; b += tile_ctas) {
@@ -363,15 +373,17 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const __grid_constant__
         if (!a.aligned) {
           const int64_t j = (i0 + q / k) / ct;
           if (j - j0 < 2) atomicAdd(hc + (j - j0) * E + x, 1);
-          else atomicAdd(a.counts_acc + j * E + x, 1);
+          else atomicAdd(cacc + j * E + x, 1);
         }
       }
       __syncthreads();
       for (int x = tid; x < E; x += blockDim.x) {
         a.tile_hist[int64_t(b) * E + x] = h[x];
         if (!a.aligned) {
-          if (hc[x]) atomicAdd(a.counts_acc + j0 * E + x, hc[x]);
-          if (hc[E + x]) atomicAdd(a.counts_acc + (j0 + 1) * E + x, hc[E + x]);
+          if (hc[x]) atomicAdd(cacc + j0 * E + x, hc[x]);
+          if (hc[E + x]) atomicAdd(cacc + (j0 + 1) * E + x, hc[E + x]);
+        } else if (h[x]) {
+          atomicAdd(cacc + j0 * E + x, h[x]);  // the tile lies inside chunk j0
         }
       }
       __syncthreads();
@@ -417,7 +429,13 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const __grid_constant__
     for (int b = blockIdx.x; b < nt; b += tile_ctas) {
       for (int i = tid; i < (have_tot ? E : 2 * E + 1); i += blockDim.x) (have_tot ? pre : W)[i] = 0;
       __syncthreads();
-      sum_hists(a.tile_hist, nt, E, have_tot ? nullptr : offs, pre, b, nullptr, 1, 0);
+      if (!have_tot)  // expert totals: column sums of the n x E chunk counts (not every tile histogram)
+        for (int x = tid; x < E; x += blockDim.x) {
+          int sum = 0;
+          for (int j = 0; j < n; ++j) sum += __ldcg(cacc + j * E + x);
+          offs[x] = sum;
+        }
+      sum_hists(a.tile_hist, nt, E, nullptr, pre, b, nullptr, 1, 0);
       __syncthreads();
       if (!have_tot) block_exscan(offs, E, ctot);
       have_tot = true;
