@@ -239,6 +239,10 @@ struct FrontArgs {
   unsigned long long* dbg;  // optional phase timestamps [8] (globaltimer ns)
 };
 constexpr int kFrontThreads = 512;
+// Front CTA size: wide expert sets (a whole warp per token, >= 3 scores per
+// lane: E > 64) route 32 tokens per pass with 1024 threads — half the
+// dependent top-k rounds per warp of a 512-thread CTA on the same tiles.
+__host__ __device__ constexpr int front_threads(int G, int PER) { return (G == 32 && PER >= 3) ? 1024 : kFrontThreads; }
 moe_status launch_front(const FrontArgs& a, int logit_dtype, cudaStream_t s);
 // Set the front kernel's shared-memory attribute ahead of graph capture.
 moe_status configure_front(int E, int logit_dtype);

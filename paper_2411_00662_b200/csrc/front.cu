@@ -313,7 +313,7 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
 }
 
 template <class T, int G, int PER>
-__global__ void __launch_bounds__(kFrontThreads) k_front(const __grid_constant__ FrontArgs a) {
+__global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_constant__ FrontArgs a) {
   extern __shared__ int smem[];
   __shared__ unsigned long long s_epoch;
   __shared__ PlanArgs s_plan;
@@ -354,7 +354,7 @@ __global__ void __launch_bounds__(kFrontThreads) k_front(const __grid_constant__
       int* hc = W + E;  // [2][E] chunk parts (unaligned only)
       for (int i = tid; i < 3 * E; i += blockDim.x) W[i] = 0;
       if (a.route) {
-        for (int64_t r0 = i0; r0 < i1; r0 += kFrontThreads / G)
+        for (int64_t r0 = i0; r0 < i1; r0 += front_threads(G, PER) / G)
           route_tokens<T, G, PER>(static_cast<const T*>(a.logits), i1, E, k, a.experts, static_cast<T*>(a.probs),
                                   r0 + tid / G, single ? s_exp : nullptr, i0);
       } else if (single) {
@@ -518,7 +518,8 @@ moe_status launch_t(const FrontArgs* a, cudaStream_t s, bool configure) {
     if (ci.fn == (const void*)k_front<T, G, PER> && ci.device == dev && ci.smem == smem_max) max_blocks = ci.blocks;
   if (max_blocks < 0) {
     int per_sm = 0, sms = 0;
-    MONTA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_front<T, G, PER>, kFrontThreads, smem_max));
+    MONTA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_front<T, G, PER>, front_threads(G, PER),
+                                                             smem_max));
     MONTA_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
     max_blocks = std::max(2, per_sm * sms);
     cache.push_back(CoopInfo{(const void*)k_front<T, G, PER>, dev, smem_max, max_blocks});
@@ -527,7 +528,7 @@ moe_status launch_t(const FrontArgs* a, cudaStream_t s, bool configure) {
   const int grid = tile_ctas + 1;
   const size_t smem = std::min(smem_max, front_smem_bytes(a, tile_ctas));
   void* args[] = {const_cast<FrontArgs*>(a)};
-  MONTA_CUDA(cudaLaunchCooperativeKernel((const void*)k_front<T, G, PER>, dim3(grid), dim3(kFrontThreads), args, smem,
+  MONTA_CUDA(cudaLaunchCooperativeKernel((const void*)k_front<T, G, PER>, dim3(grid), dim3(front_threads(G, PER)), args, smem,
                                          s));
   return MOE_OK;
 }
@@ -556,7 +557,8 @@ moe_status launch_e(const FrontArgs* a, int E, cudaStream_t s, bool configure) {
 int front_router_tokens(int E) {
   int g = 1;
   while (g < E && g < 32) g <<= 1;
-  return kFrontThreads / g;
+  const int per = g < 32 ? 1 : (E + 31) / 32;
+  return front_threads(g, per) / g;
 }
 
 // Index tile: a multiple of the router's tokens per CTA, grown (while it
