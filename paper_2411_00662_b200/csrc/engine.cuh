@@ -209,7 +209,6 @@ inline size_t index_smem_ints(int nwarps, int E, int n, bool count_in_smem) {
 struct FrontArgs {
   const void* logits;   // [T, E] (route != 0)
   int32_t route;
-  int32_t stage_lg;     // route from the tile's logits staged in shared memory (set by launch_front)
   int64_t T;
   int32_t E, k, n;
   int32_t* experts;     // [T, k]

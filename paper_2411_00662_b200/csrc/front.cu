@@ -178,14 +178,12 @@ __device__ __forceinline__ void sum_hists(const int32_t* hist, int rows, int E, 
 
 // Shared-memory layout (ints) of one front CTA.
 struct FrontSmem {
-  int lg_ints;    // the tile's gate logits staged for the router [tile_tokens * E] (16-byte multiple), else 0
   int exp_ints;   // tile experts mirror [tile_tokens * k] (one tile per CTA), else 0
   int work_ints;  // phase-dependent work area
 };
 __host__ __device__ inline FrontSmem front_smem_layout(int tile_tokens, int k, int E, int n, bool single,
-                                                       size_t plan_ints, int logit_bytes = 0) {
+                                                       size_t plan_ints) {
   FrontSmem l;
-  l.lg_ints = int(((size_t(tile_tokens) * E * logit_bytes + 15) / 16) * 4);
   l.exp_ints = single ? tile_tokens * k : 0;
   const int groups = (tile_tokens * k + 31) / 32;
   size_t w = size_t(3) * E;                                            // phase 1: h[E] | hc[2][E]
@@ -325,13 +323,24 @@ __global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_co
   const int tile_ctas = gridDim.x - 1;
   const bool control = blockIdx.x == tile_ctas;
   const bool single = nt <= tile_ctas;  // at most one tile per CTA: experts stay in shared memory
-  const FrontSmem L = front_smem_layout(a.tile_tokens, k, E, n, single, 0, a.stage_lg ? int(sizeof(T)) : 0);
-  T* s_lg = reinterpret_cast<T*>(smem);  // 16-byte aligned (dynamic shared memory base)
-  int* s_exp = smem + L.lg_ints;
-  int* W = s_exp + L.exp_ints;
+  const FrontSmem L = front_smem_layout(a.tile_tokens, k, E, n, single, 0);
+  int* s_exp = smem;
+  int* W = smem + L.exp_ints;
   if (tid == 0) {
     s_epoch = *a.epoch_dev + 1;  // read before this CTA arrives: the bump happens after every arrival
     if (a.dbg && blockIdx.x == 0) a.dbg[0] = globaltimer();
+    // the CTA's tiles of gate logits are contiguous: one bulk L2 prefetch up
+    // front, so the router's passes over a wide tile (E = 160: four passes)
+    // do not each wait for HBM
+    if (a.route && !control && blockIdx.x < nt) {
+      const size_t lb = sizeof(T) * size_t(E);
+      const int64_t i0 = int64_t(blockIdx.x) * a.tile_tokens;
+      const int64_t i1 = i0 + a.tile_tokens < a.T ? i0 + a.tile_tokens : a.T;
+      const uint32_t bytes = uint32_t(size_t(i1 - i0) * lb) & ~15u;
+      const char* src = static_cast<const char*>(a.logits) + size_t(i0) * lb;
+      if (bytes >= 16 && (reinterpret_cast<uintptr_t>(src) & 15) == 0 && bytes <= (1u << 20))
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
+    }
   }
   // this launch's chunk-count buffer (epoch parity; control_tail zeroes the other)
   int32_t* cacc = a.counts_acc + size_t((*a.epoch_dev + 1ull) & 1ull) * a.max_chunks * E;
@@ -344,33 +353,14 @@ __global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_co
       int* h = W;       // [E]
       int* hc = W + E;  // [2][E] chunk parts (unaligned only)
       for (int i = tid; i < 3 * E; i += blockDim.x) W[i] = 0;
-      if (a.route && !a.stage_lg) {
+      if (a.route) {
         for (int64_t r0 = i0; r0 < i1; r0 += front_threads(G, PER) / G)
           route_tokens<T, G, PER>(static_cast<const T*>(a.logits), i1, E, k, a.experts, static_cast<T*>(a.probs),
                                   r0 + tid / G, single ? s_exp : nullptr, i0);
-      } else if (a.route) {
-        // the tile's logits (contiguous) staged in shared memory by the whole
-        // CTA in one pass — every load in flight at once — so the router's
-        // dependent rounds never wait on HBM
-        const int64_t nel = (i1 - i0) * E;
-        const T* src = static_cast<const T*>(a.logits) + i0 * E;
-        if ((reinterpret_cast<uintptr_t>(src) & 15) == 0 && (nel * int64_t(sizeof(T))) % 16 == 0) {
-          const int64_t nv = nel * int64_t(sizeof(T)) / 16;
-#pragma unroll 4
-          for (int64_t v = tid; v < nv; v += blockDim.x)
-            reinterpret_cast<int4*>(s_lg)[v] = ld_stream(reinterpret_cast<const int4*>(src) + v);
-        } else {
-          for (int64_t q = tid; q < nel; q += blockDim.x) s_lg[q] = src[q];
-        }
-        __syncthreads();
-        for (int64_t r0 = 0; r0 < i1 - i0; r0 += front_threads(G, PER) / G)
-          route_tokens<T, G, PER>(s_lg, i1 - i0, E, k, a.experts + i0 * k, static_cast<T*>(a.probs) + i0 * k,
-                                  r0 + tid / G, single ? s_exp : nullptr, 0);
       } else if (single) {
         for (int q = tid; q < np; q += blockDim.x) s_exp[q] = a.experts[i0 * k + q];
       }
       __syncthreads();  // the tile's experts visible; histogram zeroed
-      if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[13] = globaltimer();
       const int64_t j0 = i0 / ct;
       for (int q = tid; q < np; q += blockDim.x) {
         const int x = single ? s_exp[q] : a.experts[i0 * k + q];
@@ -406,7 +396,6 @@ __global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_co
   }
   // ---------------- grid barrier: every CTA arrives; the last one releases
   __shared__ int s_last;
-  if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[14] = globaltimer();
   if (tid == 0) {
     __threadfence();
     const unsigned prev = atomicAdd(a.arrive, 1u);
@@ -497,11 +486,11 @@ __global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_co
   control_tail(a, s_plan, W, s_epoch);
 }
 
-size_t front_smem_bytes(const FrontArgs* a, int tile_ctas, int logit_bytes) {
+size_t front_smem_bytes(const FrontArgs* a, int tile_ctas) {
   const bool single = a->n_tiles <= tile_ctas;
   const size_t plan = a->do_plan && a->plan_in_smem ? plan_smem_ints(a->plan.e, a->plan.E, a->plan.n) : 0;
-  const FrontSmem l = front_smem_layout(a->tile_tokens, a->k, a->E, a->n, single, plan, a->stage_lg ? logit_bytes : 0);
-  return (size_t(l.lg_ints) + size_t(l.exp_ints) + size_t(l.work_ints)) * 4;
+  const FrontSmem l = front_smem_layout(a->tile_tokens, a->k, a->E, a->n, single, plan);
+  return (size_t(l.exp_ints) + size_t(l.work_ints)) * 4;
 }
 
 struct CoopInfo {
@@ -522,7 +511,7 @@ moe_status launch_t(const FrontArgs* a, cudaStream_t s, bool configure) {
   static std::vector<CoopInfo> cache;
   int dev = 0;
   cudaGetDevice(&dev);
-  const size_t smem_max = front_smem_bytes(a, a->n_tiles, int(sizeof(T)));  // the one-tile-per-CTA layout is the larger
+  const size_t smem_max = front_smem_bytes(a, a->n_tiles);  // the one-tile-per-CTA layout is the larger
   if (smem_max > size_t(kFrontSmemMax)) return fail(MOE_ERR_UNSUPPORTED, "front: too many experts (%d)", a->E);
   int max_blocks = -1;
   for (const auto& ci : cache)
@@ -537,7 +526,7 @@ moe_status launch_t(const FrontArgs* a, cudaStream_t s, bool configure) {
   }
   const int tile_ctas = std::max(1, std::min(a->n_tiles, max_blocks - 1));
   const int grid = tile_ctas + 1;
-  const size_t smem = std::min(smem_max, front_smem_bytes(a, tile_ctas, int(sizeof(T))));
+  const size_t smem = std::min(smem_max, front_smem_bytes(a, tile_ctas));
   void* args[] = {const_cast<FrontArgs*>(a)};
   MONTA_CUDA(cudaLaunchCooperativeKernel((const void*)k_front<T, G, PER>, dim3(grid), dim3(front_threads(G, PER)), args, smem,
                                          s));
@@ -587,15 +576,7 @@ moe_status launch_front(const FrontArgs& a, int logit_dtype, cudaStream_t s) {
     if (moe_status st = check_route_args(a.T, a.E, a.k)) return st;
   if (a.tile_tokens % front_router_tokens(a.E) != 0) return fail(MOE_ERR_INVALID_ARGUMENT, "front: bad tile size");
   FrontArgs f = a;
-  const int lb = logit_dtype == MOE_F64 ? 8 : 4;
-  f.stage_lg = 0;
-  if (f.route) {  // stage the logits when the staged layout fits (plan spilled to global first)
-    f.stage_lg = 1;
-    if (front_smem_bytes(&f, f.n_tiles, lb) > size_t(kFrontSmemMax)) f.plan_in_smem = 0;
-    if (front_smem_bytes(&f, f.n_tiles, lb) > size_t(kFrontSmemMax)) f.stage_lg = 0;
-  }
-  if (f.plan_in_smem && front_smem_bytes(&f, f.n_tiles, logit_dtype == MOE_F64 ? 8 : 4) > size_t(kFrontSmemMax))
-    f.plan_in_smem = 0;
+  if (f.plan_in_smem && front_smem_bytes(&f, f.n_tiles) > size_t(kFrontSmemMax)) f.plan_in_smem = 0;
   if (logit_dtype == MOE_F64) return launch_e<double>(&f, f.E, s, false);
   return launch_e<float>(&f, f.E, s, false);
 }
