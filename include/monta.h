@@ -281,6 +281,8 @@ typedef struct moe_card_view {
   int64_t recv_cap;        /* e*T*min(k, L)                                       */
   int32_t* recv_expert_offsets; /* [L + 1] row offsets of this node's local experts in
                                  * recv after a FINAL-landing dispatch (expert-major) */
+  void* grad_probs;        /* [T, k] logit dtype: moe_ctx_backward's d loss / d probs   */
+  void* grad_logits;       /* [T, E] logit dtype: moe_ctx_backward's d loss / d logits  */
 } moe_card_view;
 
 moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int rank, int world_size,
@@ -351,6 +353,25 @@ moe_status moe_ctx_autotune(moe_ctx* ctx, moe_schedule* candidates, int32_t coun
 moe_status moe_ctx_forward_host(moe_ctx* ctx, int level, int32_t n_chunks, int landing,
                                 const void* host_x, const void* host_logits, void* host_out,
                                 void* stream);
+/* Layer backward on the device (the reference has no backward; these are
+ * the adjoints of combine_unpermute / dispatch routed through the forward's
+ * own exchanges).  After a forward with the same
+ * level and n (the routing must still be in the context):
+ *   moe_ctx_backward_combine: d loss / d out is read from each card's x
+ *     buffer (payload dtype; equal on a node's TP cards); it is dispatched
+ *     with the forward's plan into each card's `pre` buffer (recv — the
+ *     forward's rows / expert outputs — is left intact), then on every expert
+ *     card pre[r] := p_r * g[r] (d loss / d expert output), and the partial
+ *     <g[r], y[r]> of each TP card's column slice goes to every TP card of
+ *     the source node, summed there in fixed order into grad_probs [T, k];
+ *     grad_logits [T, E] follows (softmax adjoint).  No host round trip.
+ *   moe_ctx_backward_dispatch: d loss / d x into `out` — the forward combine
+ *     with unit weights over the gradient rows in `pre` (grad_y, or the
+ *     expert-input gradient a caller's expert backward wrote there).
+ *   moe_ctx_backward: both (identity experts). */
+moe_status moe_ctx_backward_combine(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
+moe_status moe_ctx_backward_dispatch(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
+moe_status moe_ctx_backward(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
 /* Routing checks (the reference's CorruptRoutingError, dataplane.hpp:18-20):
  * when enabled, every dispatch first poisons the receive tags, and
  * moe_ctx_forward (or moe_ctx_verify after moe_ctx_dispatch) checks every

@@ -85,7 +85,8 @@ class CardView(C.Structure):
     _fields_ = [(n, C.c_void_p) for n in (
         "x", "logits", "token_ids", "experts", "probs", "perm_src", "expert_of", "slot_pos", "counts",
         "expert_offsets", "permuted", "recv", "recv_tags", "pre", "pre_tags", "expert_out", "comb", "out")] + [
-        ("rows_permuted", C.c_int64), ("recv_cap", C.c_int64), ("recv_expert_offsets", C.c_void_p)]
+        ("rows_permuted", C.c_int64), ("recv_cap", C.c_int64), ("recv_expert_offsets", C.c_void_p),
+        ("grad_probs", C.c_void_p), ("grad_logits", C.c_void_p)]
 
 
 class Span(C.Structure):
@@ -182,6 +183,9 @@ SIGNATURES = {
     "moe_ctx_experts": (C.c_int, [_P, _P]),
     "moe_comm_priority": (C.c_int, [C.c_int]),
     "moe_ctx_enable_checks": (C.c_int, [_P, C.c_int]),
+    "moe_ctx_backward_combine": (C.c_int, [_P, C.c_int, _I32, _P]),
+    "moe_ctx_backward_dispatch": (C.c_int, [_P, C.c_int, _I32, _P]),
+    "moe_ctx_backward": (C.c_int, [_P, C.c_int, _I32, _P]),
     "moe_ctx_verify": (C.c_int, [_P, _P]),
     "moe_comm_stream_priority": (C.c_int, [C.c_int, C.c_int, _P]),
     "moe_comm_stream_create": (C.c_int, [C.c_int, _P]),

@@ -42,6 +42,9 @@ struct PeerPtrs {
   char* out = nullptr;
   uint64_t* count_table = nullptr;  // [e][max_chunks][E] of {count | epoch << 32}
   uint64_t* flags = nullptr;
+  int32_t* experts = nullptr;       // routing (layer backward reads it by row tag)
+  void* probs = nullptr;
+  void* parts = nullptr;            // [T][k][t] grad-prob partials (layer backward)
 };
 
 // Byte offsets of every buffer inside a card's slab.  Identical on every
@@ -49,7 +52,8 @@ struct PeerPtrs {
 struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
-  size_t lists, local_delta, recv_rows, recv_offs, tune, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
+  size_t lists, local_delta, recv_rows, recv_offs, tune, prow, rowpos, rowslot, dot, parts, gprobs, glogits, ones,
+      scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
       ready, xchg_counters, xchg_flags, xtrace, aa_table, total;
 };
 
@@ -77,6 +81,13 @@ struct Card {
   unsigned long long* xtrace = nullptr;  // [2 kernels][4 roles][max_chunks][2] role trace (ns)
   int32_t* aa_table = nullptr;        // [4 + max_chunks][E] token-side AA destinations
   unsigned* front_done = nullptr;  // CTA election counter of the front kernel
+  // layer backward scratch (moe_ctx_backward)
+  void* prow = nullptr;
+  int32_t* rowpos = nullptr;
+  int32_t* rowslot = nullptr;
+  void* dot = nullptr;
+  void* parts = nullptr;
+  void* ones = nullptr;
   // bound expert FFN (moe_ctx_bind_experts)
   const void* w13 = nullptr;
   const void* w2 = nullptr;
@@ -113,6 +124,7 @@ struct moe_ctx {
   bool use_xchg = true;  // persistent role-specialised exchange kernels (multi-GPU)
   uint64_t tune_epoch = 0;
   bool checks = false;  // poison + verify the landed rows' tags every dispatch (moe_ctx_enable_checks)
+  bool unit_probs = false;  // combine with unit weights (the layer backward's dispatch adjoint)
   struct GraphEntry {
     int level, n, landing;
     const void *hx, *hl;
@@ -177,6 +189,16 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.recv_rows = take(8);
   s.recv_offs = take(size_t(c->L + 1) * 4);
   s.tune = take(size_t(kMaxCards) * kMaxTune * 8);  // [sender][candidate] us (autotune)
+  // layer backward (moe_ctx_backward): per landed row weight / position / slot / partial dot,
+  // the grad-prob partials [T][k][t], grad_probs [T, k], grad_logits [T, E], unit weights [T, k]
+  s.prow = take(size_t(c->recv_cap) * c->lb);
+  s.rowpos = take(size_t(c->recv_cap) * 4);
+  s.rowslot = take(size_t(c->recv_cap) * 4);
+  s.dot = take(size_t(c->recv_cap) * c->lb);
+  s.parts = take(size_t(T) * k * d.t * c->lb);
+  s.gprobs = take(size_t(T) * k * c->lb);
+  s.glogits = take(size_t(T) * E * c->lb);
+  s.ones = take(size_t(T) * k * c->lb);
   s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
   s.epoch = take(8);
   s.front_done = take(16);
@@ -220,6 +242,8 @@ void bind_card(moe_ctx* c, Card& cd) {
   v.rows_permuted = c->R;
   v.recv_cap = c->recv_cap;
   v.recv_expert_offsets = reinterpret_cast<int32_t*>(b + s.recv_offs);
+  v.grad_probs = b + s.gprobs;
+  v.grad_logits = b + s.glogits;
   cd.count_table = reinterpret_cast<uint64_t*>(b + s.count_table);
   cd.flags = reinterpret_cast<uint64_t*>(b + s.flags);
   cd.err = reinterpret_cast<int32_t*>(b + s.err);
@@ -234,6 +258,12 @@ void bind_card(moe_ctx* c, Card& cd) {
   cd.tile_hist = reinterpret_cast<int32_t*>(b + s.tile_hist);
   cd.tile_base = reinterpret_cast<int32_t*>(b + s.tile_base);
   cd.counts_acc = reinterpret_cast<int32_t*>(b + s.counts_acc);
+  cd.prow = b + s.prow;
+  cd.rowpos = reinterpret_cast<int32_t*>(b + s.rowpos);
+  cd.rowslot = reinterpret_cast<int32_t*>(b + s.rowslot);
+  cd.dot = b + s.dot;
+  cd.parts = b + s.parts;
+  cd.ones = b + s.ones;
   cd.arrive = reinterpret_cast<unsigned*>(b + s.arrive);
   cd.ready = reinterpret_cast<unsigned long long*>(b + s.ready);
   cd.xchg_counters = reinterpret_cast<unsigned*>(b + s.xchg_counters);
@@ -254,11 +284,15 @@ void set_peer(moe_ctx* c, int card, char* slab) {
   p.out = slab + s.out;
   p.count_table = reinterpret_cast<uint64_t*>(slab + s.count_table);
   p.flags = reinterpret_cast<uint64_t*>(slab + s.flags);
+  p.experts = reinterpret_cast<int32_t*>(slab + s.experts);
+  p.probs = slab + s.probs;
+  p.parts = slab + s.parts;
 }
 
 inline int card_of(const moe_ctx* c, int node, int rho) { return node * c->d.t + rho; }
 inline int sig_chunk(const moe_ctx* c, int ps, int j) { return kSigChunkBase + ps * c->d.max_chunks + j; }
-inline int sig_tune(const moe_ctx* c) { return c->n_flag_sigs - 1; }
+inline int sig_tune(const moe_ctx* c) { return c->n_flag_sigs - 2; }
+inline int sig_bwd(const moe_ctx* c) { return c->n_flag_sigs - 1; }
 
 // Flag word on `owner` that `sender` writes for signal `sig`.
 inline uint64_t* flag_at(moe_ctx* c, int owner, int sig, int sender) {
@@ -371,7 +405,7 @@ extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int
   c->R = desc->tokens * desc->top_k;
   c->row_bytes = desc->hidden * int64_t(c->xb);
   c->recv_cap = int64_t(desc->e) * desc->tokens * std::min<int64_t>(desc->top_k, c->L);
-  c->n_flag_sigs = kSigChunkBase + kNumPhaseSignals * desc->max_chunks + 1;  // + the autotune signal
+  c->n_flag_sigs = kSigChunkBase + kNumPhaseSignals * desc->max_chunks + 2;  // + autotune, layer-backward signals
   c->lay = make_layout(c);
   const int first = world_size == 1 ? 0 : rank;
   const int nlocal = world_size == 1 ? cards : 1;
@@ -388,6 +422,7 @@ extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int
     }
     cudaMemset(cd.slab, 0, c->lay.total);
     bind_card(c, cd);
+    launch_fill_ones(desc->logit_dtype, cd.ones, desc->tokens * desc->top_k, nullptr);
     c->local.push_back(cd);
     set_peer(c, cd.id, cd.slab);
   }
@@ -1208,7 +1243,7 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
   a.y_stride = c->row_bytes;
   a.slot_pos = cd.v.slot_pos;
   a.experts = cd.v.experts;
-  a.probs = cd.v.probs;
+  a.probs = c->unit_probs ? cd.ones : cd.v.probs;
   a.k = d.top_k;
   const int64_t ct = d.tokens / n;
   a.tok_begin = int64_t(j) * ct;
@@ -1268,7 +1303,7 @@ moe_status launch_combine_persistent(moe_ctx* c, Card& cd, int level, int n, cud
   u.y_stride = c->row_bytes;
   u.slot_pos = cd.v.slot_pos;
   u.experts = cd.v.experts;
-  u.probs = cd.v.probs;
+  u.probs = c->unit_probs ? cd.ones : cd.v.probs;
   u.k = d.top_k;
   u.col_begin = dedup ? int64_t(cd.rho) * (d.hidden / d.t) : 0;
   u.cols = dedup ? d.hidden / d.t : d.hidden;
@@ -1704,6 +1739,132 @@ extern "C" moe_status moe_ctx_autotune(moe_ctx* c, moe_schedule* cand, int32_t c
   }
   *best = b;
   return MOE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Layer backward on the device (the reference has none).
+namespace {
+
+// recv <-> pre in every local view and every peer pointer: the gradient
+// dispatch lands in the `pre` memory (FINAL landing never stages), so the
+// forward's dispatched rows / expert outputs in recv stay intact.
+void swap_recv_pre(moe_ctx* c) {
+  for (auto& cd : c->local) {
+    const bool eo = cd.v.expert_out == cd.v.recv;
+    std::swap(cd.v.recv, cd.v.pre);
+    std::swap(cd.v.recv_tags, cd.v.pre_tags);
+    if (eo) cd.v.expert_out = cd.v.recv;
+  }
+  for (int q = 0; q < c->cards; ++q) {
+    std::swap(c->peer[q].recv, c->peer[q].pre);
+    std::swap(c->peer[q].recv_tags, c->peer[q].pre_tags);
+  }
+}
+
+BwdPeers bwd_peers(moe_ctx* c) {
+  BwdPeers pe{};
+  for (int q = 0; q < c->cards; ++q) {
+    pe.experts[q] = c->peer[q].experts;
+    pe.probs[q] = c->peer[q].probs;
+    pe.parts[q] = c->peer[q].parts;
+  }
+  return pe;
+}
+
+// combine adjoint: grad_out (each card's x buffer) -> the forward's dispatch
+// (same level / n, FINAL landing into `pre`) -> per landed row g:
+// grad_y = p * g in place in `pre`, partial <g, y> over the card's column
+// slice -> every TP card of the source node -> grad_probs -> grad_logits.
+moe_status backward_combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  if (d.dtype == MOE_I64) return fail(MOE_ERR_INVALID_ARGUMENT, "backward: integer payloads have no gradient");
+  swap_recv_pre(c);
+  moe_status st = dispatch_impl(c, level, n, MOE_LAND_FINAL, s, false);
+  if (st == MOE_OK && !is_virtual(c)) st = dispatch_tail_wait(c, c->local[0], level, n, MOE_LAND_FINAL, s);
+  swap_recv_pre(c);
+  if (st != MOE_OK) return st;
+  const BwdPeers pe = bwd_peers(c);
+  const int64_t h = d.hidden, w = d.hidden / d.t;
+  const size_t es = c->xb;
+  const int ydt = d.dtype, pdt = d.logit_dtype;
+  for (auto& cd : c->local) {
+    MONTA_CUDA(launch_row_meta(pdt, cd.v.pre_tags, cd.recv_rows, c->recv_cap, d.t, cd.rho, d.top_k, pe, cd.prow,
+                               cd.rowpos, cd.rowslot, cd.err, s));
+    // partial dot over this card's column slice first (needs g), then grad_y = p * g in place
+    const size_t off = size_t(cd.rho) * size_t(w) * es;
+    if (moe_status s1 = moe_combine_backward(static_cast<char*>(cd.v.pre) + off, ydt, h,
+                                             static_cast<const char*>(cd.v.expert_out) + off, ydt, h, w, cd.rowpos,
+                                             cd.prow, pdt, c->recv_cap, 1, nullptr, h, cd.dot, s))
+      return s1;
+    if (moe_status s2 = moe_combine_backward(cd.v.pre, ydt, h, nullptr, ydt, h, h, cd.rowpos, cd.prow, pdt,
+                                             c->recv_cap, 1, cd.v.pre, h, nullptr, s))
+      return s2;
+    MONTA_CUDA(launch_scatter_parts(pdt, cd.v.pre_tags, cd.recv_rows, c->recv_cap, d.t, cd.rho, d.top_k,
+                                    cd.rowslot, cd.dot, pe, s));
+    c->launches += 4;
+  }
+  if (!is_virtual(c)) {  // every card's partials landed (stores into this card) before the sums
+    Card& cd = c->local[0];
+    SignalList sg = no_signal();
+    sg.epoch_ptr = cd.epoch_dev;
+    WaitList wl = no_wait();
+    wl.epoch_ptr = cd.epoch_dev;
+    for (int q = 0; q < c->cards; ++q)
+      if (q != cd.id) {
+        sg.flags[sg.n++] = flag_at(c, q, sig_bwd(c), cd.id);
+        wl.flags[wl.n++] = flag_at(c, cd.id, sig_bwd(c), q);
+      }
+    MONTA_CUDA(launch_signal(sg, s));
+    MONTA_CUDA(launch_wait(wl, cd.err, s));
+    c->launches += 2;
+  }
+  for (auto& cd : c->local) {
+    MONTA_CUDA(launch_sum_parts(pdt, cd.parts, cd.v.experts, d.tokens * d.top_k, d.t, cd.v.grad_probs, s));
+    if (moe_status s3 = moe_route_backward(cd.v.logits, pdt, d.tokens, d.num_experts, d.top_k, cd.v.experts,
+                                           cd.v.grad_probs, cd.v.grad_logits, s))
+      return s3;
+    c->launches += 2;
+  }
+  return MOE_OK;
+}
+
+// dispatch adjoint: grad_x = the forward combine with unit weights over the
+// gradient rows in `pre` (grad_y, or the caller's expert-input gradient).
+moe_status backward_dispatch_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
+  std::vector<void*> saved;
+  for (auto& cd : c->local) {
+    saved.push_back(cd.v.expert_out);
+    cd.v.expert_out = cd.v.pre;
+  }
+  c->unit_probs = true;
+  const moe_status st = combine_impl(c, level, n, s);
+  c->unit_probs = false;
+  for (size_t i = 0; i < c->local.size(); ++i) c->local[i].v.expert_out = saved[i];
+  return st;
+}
+
+}  // namespace
+
+extern "C" moe_status moe_ctx_backward_combine(moe_ctx* c, int level, int32_t n, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (moe_status st = validate_dispatch(c, level, n, MOE_LAND_FINAL)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  return backward_combine_impl(c, level, n, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" moe_status moe_ctx_backward_dispatch(moe_ctx* c, int level, int32_t n, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  return backward_dispatch_impl(c, level, n, static_cast<cudaStream_t>(stream));
+}
+
+extern "C" moe_status moe_ctx_backward(moe_ctx* c, int level, int32_t n, void* stream) {
+  if (moe_status st = check_ready(c)) return st;
+  if (moe_status st = validate_dispatch(c, level, n, MOE_LAND_FINAL)) return st;
+  MONTA_CUDA(cudaSetDevice(c->device));
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (moe_status st = backward_combine_impl(c, level, n, s)) return st;
+  return backward_dispatch_impl(c, level, n, s);
 }
 
 extern "C" moe_status moe_ctx_forward_host(moe_ctx* c, int level, int32_t n, int landing, const void* host_x,

@@ -192,6 +192,21 @@ struct PlanArgs {
 };
 size_t plan_scratch_ints(int e, int E, int max_chunks);
 moe_status configure_grouped_gemm();  // experts.cu
+// layer backward (layer_bwd.cu): every card's routing and grad-prob partials by card id
+struct BwdPeers {
+  const int32_t* experts[kMaxCards];
+  const void* probs[kMaxCards];
+  void* parts[kMaxCards];
+};
+cudaError_t launch_row_meta(int logit_dtype, const int32_t* tags, const int64_t* recv_rows, int64_t cap, int t,
+                            int rho, int k, const BwdPeers& pe, void* prow, int32_t* rowpos, int32_t* rowslot,
+                            int32_t* err, cudaStream_t s);
+cudaError_t launch_scatter_parts(int logit_dtype, const int32_t* tags, const int64_t* recv_rows, int64_t cap, int t,
+                                 int rho, int k, const int32_t* rowslot, const void* dot, const BwdPeers& pe,
+                                 cudaStream_t s);
+cudaError_t launch_sum_parts(int logit_dtype, const void* parts, const int32_t* experts, int64_t Tk, int t,
+                             void* gprobs, cudaStream_t s);
+cudaError_t launch_fill_ones(int logit_dtype, void* p, int64_t n, cudaStream_t s);
 cudaError_t launch_verify_recv(const int32_t* tags, const int64_t* recv_rows, const int32_t* offs, int L, int node,
                                int e, int t, int64_t T, int64_t cap, int32_t* err, cudaStream_t s);  // verify.cu
 bool plan_fits_smem(int e, int E, int n);

@@ -70,6 +70,8 @@ class CardTensors:
     comb: torch.Tensor
     out: torch.Tensor
     recv_expert_offsets: torch.Tensor
+    grad_probs: torch.Tensor
+    grad_logits: torch.Tensor
 
 
 def _stream_ptr(stream) -> int:
@@ -120,7 +122,9 @@ class MoeLayer:
             recv_tags=mk(v.recv_tags, (cap, 4), i32), pre=mk(v.pre, (cap, h), self.dtype),
             pre_tags=mk(v.pre_tags, (cap, 4), i32), comb=mk(v.comb, (R, h), self.dtype),
             out=mk(v.out, (T, h), self.out_dtype),
-            recv_expert_offsets=mk(v.recv_expert_offsets, (self.L + 1,), i32))
+            recv_expert_offsets=mk(v.recv_expert_offsets, (self.L + 1,), i32),
+            grad_probs=mk(v.grad_probs, (T, k), self.logit_dtype),
+            grad_logits=mk(v.grad_logits, (T, E), self.logit_dtype))
 
     def card(self, c: int) -> CardTensors:
         return self._cards[c]
@@ -185,6 +189,19 @@ class MoeLayer:
         best = C.c_int32()
         check(self.lib.moe_ctx_autotune(self._ctx, arr, len(candidates), steps, _stream_ptr(stream), C.byref(best)))
         return int(best.value), [arr[i].us for i in range(len(candidates))]
+
+    # ------------------------------------------------------------ backward
+    def backward_combine(self, level: int = O1, n: int = 1, stream=None) -> None:
+        """d loss/d out read from each card's x; leaves d loss/d expert-output in
+        each card's pre rows and grad_probs / grad_logits in the card views."""
+        check(self.lib.moe_ctx_backward_combine(self._ctx, level, n, _stream_ptr(stream)))
+
+    def backward_dispatch(self, level: int = O1, n: int = 1, stream=None) -> None:
+        """d loss/d x into each card's out, from the gradient rows in pre."""
+        check(self.lib.moe_ctx_backward_dispatch(self._ctx, level, n, _stream_ptr(stream)))
+
+    def backward(self, level: int = O1, n: int = 1, stream=None) -> None:
+        check(self.lib.moe_ctx_backward(self._ctx, level, n, _stream_ptr(stream)))
 
     def enable_checks(self, enable: bool = True) -> None:
         """Poison + verify the landed rows' tags every dispatch (CorruptRoutingError on failure)."""

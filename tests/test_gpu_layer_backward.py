@@ -90,3 +90,87 @@ def test_layer_backward_closed_form(cuda, e, t, E, k, level, n, landing):
             assert torch.equal(cd.probs.double().cpu(), probs[cd.node])
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("e,t,E,k,level,n", [
+    (2, 2, 8, 2, O1, 1), (2, 2, 8, 2, O2, 2), (2, 2, 8, 2, BASELINE, 1), (2, 1, 8, 2, BASELINE, 1),
+    (1, 2, 4, 2, O1, 1), (4, 2, 16, 6, O2, 2), (2, 4, 2, 1, O1, 1), (1, 1, 160, 6, BASELINE, 1)])
+def test_ctx_backward_device_side(cuda, e, t, E, k, level, n):
+    """moe_ctx_backward_combine / _dispatch (the whole layer backward inside the
+    context, no host round trip) against the closed forms of the composed test
+    above: grad_y bit-exact, grad_probs 1e-5 of fp64, grad_logits 1e-4, grad_x 1e-2."""
+    T, h = 128, 256
+    dt = torch.bfloat16
+    gen = torch.Generator().manual_seed(e * 10 + t + level + 7)
+    x = torch.randn(e, T, h, generator=gen).to(dt)
+    logits = torch.randn(e, T, E, generator=gen)
+    gout = torch.randn(e, T, h, generator=gen).to(dt)
+    c = torch.linspace(0.5, 2.0, E, dtype=torch.float64)
+    d = torch.linspace(-1.0, 1.0, E, dtype=torch.float64)
+    layer = MoeLayer(e, t, E, k, T, h, dtype=dt, logit_dtype=torch.float32, max_chunks=max(n, 1), device=0)
+    try:
+        for cd in layer.cards:
+            cd.x.copy_(x[cd.node])
+            cd.logits.copy_(logits[cd.node])
+        layer.route()
+        layer.dispatch(level, n)
+        layer.sync()
+        for cd in layer.cards:  # experts in place: y = c_x * row (bf16)
+            rows = layer.recv_rows(cd.card)
+            xe = cd.recv_tags[:rows, 3].long()
+            cd.recv[:rows].copy_((cd.recv[:rows].double() * c.to(cuda)[xe][:, None]).to(dt))
+        layer.combine(level, n)
+        layer.sync()
+        experts = {cd.node: cd.experts.long().cpu() for cd in layer.cards}
+        probs = {cd.node: cd.probs.double().cpu() for cd in layer.cards}
+        for cd in layer.cards:
+            cd.x.copy_(gout[cd.node])
+        layer.backward_combine(level, n)
+        layer.sync()
+        ex_all = torch.stack([experts[g_] for g_ in range(e)])
+        pr_all = torch.stack([probs[g_] for g_ in range(e)])
+        for cd in layer.cards:
+            g, xx = gout[cd.node].double(), x[cd.node].double()
+            ex = experts[cd.node]
+            yx = (xx[:, None, :] * c[ex][:, :, None]).to(dt).double()
+            want = (g[:, None, :] * yx).sum(-1)
+            mag = (g[:, None, :] * yx).abs().sum(-1)
+            gp = cd.grad_probs.double().cpu()
+            assert ((gp - want).abs() / mag).max().item() < 1e-5, cd.card
+            P = torch.softmax(logits[cd.node].double(), -1)
+            G = torch.zeros(T, E, dtype=torch.float64)
+            G.scatter_(1, ex, want)
+            want_z = P * (G - (G * P).sum(-1, keepdim=True))
+            assert torch.allclose(cd.grad_logits.double().cpu(), want_z, rtol=1e-4, atol=1e-5), cd.card
+            rows = layer.recv_rows(cd.card)
+            if rows:
+                tags = cd.recv_tags[:rows].long().cpu()
+                src_node, pos, xe = tags[:, 1] // t, tags[:, 2], tags[:, 3]
+                slot = (ex_all[src_node, pos] == xe[:, None]).int().argmax(dim=1)
+                p_r = pr_all[src_node, pos, slot]
+                want_gy = (p_r[:, None].float() * gout[src_node, pos].float()).to(dt)
+                assert torch.equal(cd.pre[:rows].cpu(), want_gy), cd.card
+                # the caller's expert backward: d loss / d expert input = d_x * g_tok (replaces grad_y)
+                cd.pre[:rows].copy_((gout[src_node, pos].double() * d[xe][:, None]).to(dt).to(cuda))
+        layer.backward_dispatch(level, n)
+        layer.sync()
+        for cd in layer.cards:
+            ex = experts[cd.node]
+            want = (gout[cd.node].double()[:, None, :] * d[ex][:, :, None]).to(dt).double().sum(1)
+            err = ((cd.out.double().cpu() - want).abs().max() / want.abs().max()).item()
+            assert err < 1e-2, (cd.card, err)
+        # identity experts end to end: grad_x = g * sum(p)
+        for cd in layer.cards:
+            cd.x.copy_(x[cd.node])
+        layer.forward(level, n)
+        layer.sync()
+        for cd in layer.cards:
+            cd.x.copy_(gout[cd.node])
+        layer.backward(level, n)
+        layer.sync()
+        for cd in layer.cards:
+            want = gout[cd.node].double() * probs[cd.node].sum(1, keepdim=True)
+            err = ((cd.out.double().cpu() - want).abs().max() / want.abs().max()).item()
+            assert err < 1e-2, (cd.card, err)
+    finally:
+        layer.close()
