@@ -83,9 +83,24 @@ def main():
         LB.dispatch_backward(layer, grad_rows, level, a.chunks)
 
     bwd_us = timed(bwd)
+
+    def bwd_ctx():  # the whole backward inside the context (moe_ctx_backward): no host round trip
+        cd.x.copy_(gout)
+        layer.backward(level, a.chunks)
+
+    ctx_us = timed(bwd_ctx)
+    layer.enable_graphs(True)
+
+    def fwd_graph():
+        cd.x.copy_(x)
+        layer.forward(level, a.chunks, LAND_FINAL)
+
+    fwdg_us = timed(fwd_graph)
+    layer.enable_graphs(False)
     if rank == 0:
         print(json.dumps({"workload": "mixtral-8x7b-moe-layer", "topology": f"{e}x{t}", "level": level,
                           "chunks": a.chunks, "forward_us": fwd_us, "backward_us": bwd_us,
+                          "ctx_backward_us": ctx_us, "forward_route_graph_us": fwdg_us,
                           "note": "host-timed regions include the Python orchestration, the syncs inside "
                                   "combine_backward/dispatch_backward and the metadata all-gathers; no CUDA "
                                   "graphs; max over ranks"}), flush=True)

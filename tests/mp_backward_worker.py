@@ -71,6 +71,31 @@ def main():
             if not torch.equal(cd.probs.double().cpu(), pr):
                 print(f"rank {rank} {spec}: probs not restored", flush=True)
                 ok = False
+            # the same closed forms through the context's device-side backward
+            # (moe_ctx_backward_combine / _dispatch: no host round trip)
+            if landing == 0:
+                cd.x.copy_(x[cd.node])
+                layer.dispatch(level, n, landing)
+                layer.sync()
+                cd.recv[:rows].copy_(y[cd.card])       # the scaling experts, in place
+                layer.combine(level, n)
+                cd.x.copy_(gout[cd.node])
+                layer.backward_combine(level, n)
+                layer.sync()
+                want_p = (g[:, None, :] * yx).sum(-1)
+                err = ((cd.grad_probs.double().cpu() - want_p).abs() / (g[:, None, :] * yx).abs().sum(-1)).max().item()
+                if not err < 1e-5:
+                    print(f"rank {rank} {spec}: ctx grad_probs rel err {err}", flush=True)
+                    ok = False
+                tags = cd.recv_tags[:rows].long()
+                cd.pre[:rows].copy_((gout.to(dev)[tags[:, 1] // t, tags[:, 2]].double()
+                                     * d.to(dev)[tags[:, 3]][:, None]).to(dt))
+                layer.backward_dispatch(level, n)
+                layer.sync()
+                err = ((cd.out.double().cpu() - want).abs().max() / want.abs().max()).item()
+                if not err < 1e-2:
+                    print(f"rank {rank} {spec}: ctx grad_x rel err {err}", flush=True)
+                    ok = False
     finally:
         layer.close()
         dist.barrier()
