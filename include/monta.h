@@ -372,6 +372,19 @@ moe_status moe_ctx_forward_host(moe_ctx* ctx, int level, int32_t n_chunks, int l
 moe_status moe_ctx_backward_combine(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
 moe_status moe_ctx_backward_dispatch(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
 moe_status moe_ctx_backward(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
+/* Dispatch wire format of the cross-node (AllToAll) legs (SURVEY.md §8(f)
+ * item 3).  MOE_WIRE_BF16 (default): rows move bit-exactly.  MOE_WIRE_FP8:
+ * the sender quantises each 128-element block of a cross-node row slice to
+ * e4m3 with one fp32 scale (amax / 448, round to nearest, saturating) and
+ * stores bytes + scales into the receiver's pre / scale buffers — half the
+ * AllToAll bytes; the receiver decodes them into recv before the intra-node
+ * AllGather forwards its slice (bf16).  Own-node rows stay bf16.  Lossy by
+ * design (one e4m3 rounding, <= 2^-4 relative per element); needs a bf16
+ * payload, hidden and hidden/t multiples of 128, top_k <= 16, FINAL landing;
+ * runs the per-leg launches.  The combine's return leg stays bf16. */
+#define MOE_WIRE_BF16 0
+#define MOE_WIRE_FP8 1
+moe_status moe_ctx_set_wire(moe_ctx* ctx, int wire);
 /* Routing checks (the reference's CorruptRoutingError, dataplane.hpp:18-20):
  * when enabled, every dispatch first poisons the receive tags, and
  * moe_ctx_forward (or moe_ctx_verify after moe_ctx_dispatch) checks every

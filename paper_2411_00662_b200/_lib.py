@@ -38,6 +38,8 @@ LAND_FINAL, LAND_STAGED = 0, 1
 COMM_TP_SP, COMM_EP, COMM_PP, COMM_CP, COMM_DP = 0, 1, 2, 3, 4
 # expert activations (moe_grouped_gemm)
 ACT_NONE, ACT_SWIGLU = 0, 1
+# dispatch wire formats (moe_ctx_set_wire)
+WIRE_BF16, WIRE_FP8 = 0, 1
 W13_BLOCK = 128
 # moe_stage
 STAGES = ["route", "index", "aa", "ag", "d2d", "caa", "unpermute", "total", "experts"]
@@ -183,6 +185,7 @@ SIGNATURES = {
     "moe_ctx_experts": (C.c_int, [_P, _P]),
     "moe_comm_priority": (C.c_int, [C.c_int]),
     "moe_ctx_enable_checks": (C.c_int, [_P, C.c_int]),
+    "moe_ctx_set_wire": (C.c_int, [_P, C.c_int]),
     "moe_ctx_backward_combine": (C.c_int, [_P, C.c_int, _I32, _P]),
     "moe_ctx_backward_dispatch": (C.c_int, [_P, C.c_int, _I32, _P]),
     "moe_ctx_backward": (C.c_int, [_P, C.c_int, _I32, _P]),

@@ -18,6 +18,10 @@
 // what keep enough loads in flight: the gather micro-benchmark
 // (scripts/micro/gather_bench.cu) gains ~10% from 16 to 32 warps per SM at
 // equal bytes in flight.
+#include <cuda_fp8.h>
+
+#include <algorithm>
+
 #include "copy.cuh"
 
 namespace monta {
@@ -43,6 +47,8 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
     const int64_t v0 = (it % pieces) * kPieceVec;
     // lane s < k: destination of slot s (row pointer, byte window [off, end))
     char* dp = nullptr;
+    char* qp = nullptr;   // fp8 wire: e4m3 row on the receiver (cross-node legs)
+    float* sp = nullptr;  //           its per-128-element scales
     int off = 0, end = 0;
     if (lane < k) {
       const int64_t q = i * k + lane;
@@ -55,6 +61,10 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
         off = __ldg(a.table + 2 * E + x);
         end = off + __ldg(a.table + 3 * E + x);
         dp = a.dst[card] + row * a.dst_stride;
+        if (a.fp8 && card / a.t != a.node) {
+          qp = a.dst_pre[card] + row * a.dst_stride;
+          sp = a.dst_scale[card] + row * a.blocks_per_row;
+        }
         if (v0 == 0 && a.dst_tags[card])
           *reinterpret_cast<int4*>(a.dst_tags[card] + 4 * row) = make_int4(__ldg(a.token_ids + i), a.source_card,
                                                                              int(i), x);
@@ -72,6 +82,43 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
       char* d = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dp), s));
       const int o = __shfl_sync(0xffffffffu, off, s), e = __shfl_sync(0xffffffffu, end, s);
       if (!d || e <= piece_lo || o >= piece_hi) continue;  // warp-uniform
+      if constexpr (V == 16) {
+        char* q = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(qp), s));
+        if (q) {  // warp-uniform: the fp8 wire for this cross-node leg
+          float* sc = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), s));
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int64_t v = v0 + u * 32 + lane;  // 16 lanes x 8 bf16 = one 128-element block
+            const int64_t byte = v * V;
+            const bool in = v < nvec && byte >= o && byte < e;
+            const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&r[u]);
+            float f[8];
+            float amax = 0.f;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              f[j] = in ? __bfloat162float(hv[j]) : 0.f;
+              amax = fmaxf(amax, fabsf(f[j]));
+            }
+#pragma unroll
+            for (int m = 8; m > 0; m >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, m));
+            const float scale = amax > 0.f ? amax / 448.f : 1.f;
+            if (in) {
+              uint32_t w[2];
+#pragma unroll
+              for (int j = 0; j < 2; ++j) {
+                const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
+                    make_float2(f[4 * j] / scale, f[4 * j + 1] / scale), __NV_SATFINITE, __NV_E4M3);
+                const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
+                    make_float2(f[4 * j + 2] / scale, f[4 * j + 3] / scale), __NV_SATFINITE, __NV_E4M3);
+                w[j] = uint32_t(lo) | (uint32_t(hi) << 16);
+              }
+              *reinterpret_cast<uint2*>(q + v * 8) = make_uint2(w[0], w[1]);
+              if ((lane & 15) == 0) sc[v / 16] = scale;
+            }
+          }
+          continue;
+        }
+      }
       Vec* dv = reinterpret_cast<Vec*>(d);
 #pragma unroll
       for (int u = 0; u < U; ++u) {
@@ -84,7 +131,50 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
   cta_signal(a.sig);
 }
 
+// fp8 wire receive: thread per 8 columns of a row that came cross-node.
+__global__ void __launch_bounds__(256) k_wire_dequant(char* __restrict__ recv, const int32_t* __restrict__ tags,
+                                                      const int64_t* __restrict__ recv_rows, const char* __restrict__ pre,
+                                                      const float* __restrict__ scales, int64_t row_bytes, int bpr,
+                                                      int node, int t, int64_t col0, int64_t width, int64_t p0,
+                                                      int64_t p1) {
+  const int64_t rows = *recv_rows;
+  const int64_t per_row = width / 8;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < rows * per_row;
+       q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t r = q / per_row, c = col0 + (q - r * per_row) * 8;
+    const int4 tg = reinterpret_cast<const int4*>(tags)[r];  // {token_id, source_card, source_position, expert}
+    if (tg.y / t == node || tg.z < p0 || tg.z >= p1) continue;
+    const uint2 b = *reinterpret_cast<const uint2*>(pre + r * row_bytes + c);
+    const float scale = scales[r * bpr + c / 128];
+    const uint32_t w[2] = {b.x, b.y};
+    __nv_bfloat162 o[4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2(__nv_fp8x2_storage_t(w[j] & 0xffffu), __NV_E4M3);
+      const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2(__nv_fp8x2_storage_t(w[j] >> 16), __NV_E4M3);
+      const float2 fl = __half22float2(__half2(lo)), fh = __half22float2(__half2(hi));
+      o[2 * j] = __floats2bfloat162_rn(fl.x * scale, fl.y * scale);
+      o[2 * j + 1] = __floats2bfloat162_rn(fh.x * scale, fh.y * scale);
+    }
+    *reinterpret_cast<uint4*>(recv + r * row_bytes + c * 2) = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_wire_dequant(char* recv, const int32_t* tags, const int64_t* recv_rows, int64_t cap,
+                                const char* pre, const float* scales, int64_t row_bytes, int blocks_per_row,
+                                int node, int t, int64_t col0, int64_t width, int64_t p0, int64_t p1,
+                                cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t work = cap * (width / 8);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, int64_t(sms) * 8)));
+  k_wire_dequant<<<grid, 256, 0, s>>>(recv, tags, recv_rows, pre, scales, row_bytes, blocks_per_row, node, t, col0,
+                                      width, p0, p1);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s) {
   if (a.k > kTokMaxK) return cudaErrorNotSupported;

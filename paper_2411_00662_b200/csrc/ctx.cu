@@ -45,6 +45,7 @@ struct PeerPtrs {
   int32_t* experts = nullptr;       // routing (layer backward reads it by row tag)
   void* probs = nullptr;
   void* parts = nullptr;            // [T][k][t] grad-prob partials (layer backward)
+  float* wscale = nullptr;          // [recv_cap][h / 128] fp8 wire scales
 };
 
 // Byte offsets of every buffer inside a card's slab.  Identical on every
@@ -53,7 +54,7 @@ struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
   size_t lists, local_delta, recv_rows, recv_offs, tune, prow, rowpos, rowslot, dot, parts, gprobs, glogits, ones,
-      scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
+      wscale, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
       ready, xchg_counters, xchg_flags, xtrace, aa_table, total;
 };
 
@@ -125,6 +126,7 @@ struct moe_ctx {
   uint64_t tune_epoch = 0;
   bool checks = false;  // poison + verify the landed rows' tags every dispatch (moe_ctx_enable_checks)
   bool unit_probs = false;  // combine with unit weights (the layer backward's dispatch adjoint)
+  int wire = MOE_WIRE_BF16;  // cross-node dispatch payload format (moe_ctx_set_wire)
   struct GraphEntry {
     int level, n, landing;
     const void *hx, *hl;
@@ -199,6 +201,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.gprobs = take(size_t(T) * k * c->lb);
   s.glogits = take(size_t(T) * E * c->lb);
   s.ones = take(size_t(T) * k * c->lb);
+  s.wscale = take(size_t(c->recv_cap) * std::max<int64_t>(1, h / 128) * 4);  // fp8 wire scales
   s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
   s.epoch = take(8);
   s.front_done = take(16);
@@ -287,6 +290,7 @@ void set_peer(moe_ctx* c, int card, char* slab) {
   p.experts = reinterpret_cast<int32_t*>(slab + s.experts);
   p.probs = slab + s.probs;
   p.parts = slab + s.parts;
+  p.wscale = reinterpret_cast<float*>(slab + s.wscale);
 }
 
 inline int card_of(const moe_ctx* c, int node, int rho) { return node * c->d.t + rho; }
@@ -793,7 +797,13 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
       if (!c->peer[q].slab) continue;
       t.dst[q] = t.staged ? c->peer[q].pre : c->peer[q].recv;
       t.dst_tags[q] = t.staged ? c->peer[q].pre_tags : c->peer[q].recv_tags;
+      t.dst_pre[q] = c->peer[q].pre;
+      t.dst_scale[q] = c->peer[q].wscale;
     }
+    t.fp8 = c->wire == MOE_WIRE_FP8 ? 1 : 0;
+    t.node = cd.node;
+    t.t = d.t;
+    t.blocks_per_row = int(std::max<int64_t>(1, d.hidden / 128));
     t.sig = no_signal();
     t.sig.epoch_ptr = cd.epoch_dev;
     t.sig.done = cd.done + kPsAA * d.max_chunks + j;
@@ -860,6 +870,23 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
 
 // One chunk of the intra-node AllGather (forward this rank's slice of the
 // rows that arrived from other nodes to every TP peer).
+// fp8 wire, receive side: the rows of chunk j (j < 0: every chunk) that came
+// from another node, this card's columns, e4m3 + scales (pre, wscale) -> bf16 recv.
+moe_status wire_dequant(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s) {
+  if (c->wire != MOE_WIRE_FP8 || c->d.e == 1) return MOE_OK;
+  const moe_layer_desc& d = c->d;
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  const int64_t w = dedup ? d.hidden / d.t : d.hidden;
+  const int64_t ct = d.tokens / std::max(1, c->last_n);
+  const int64_t p0 = j < 0 ? 0 : int64_t(j) * ct, p1 = j < 0 ? d.tokens : p0 + ct;
+  MONTA_CUDA(launch_wire_dequant(static_cast<char*>(cd.v.recv), cd.v.recv_tags, cd.recv_rows, c->recv_cap,
+                                 static_cast<const char*>(cd.v.pre), c->peer[cd.id].wscale, c->row_bytes,
+                                 int(std::max<int64_t>(1, d.hidden / 128)), cd.node, d.t,
+                                 dedup ? int64_t(cd.rho) * w : 0, w, p0, p1, s));
+  ++c->launches;
+  return MOE_OK;
+}
+
 moe_status launch_ag(moe_ctx* c, Card& cd, int j, int landing, cudaStream_t s, bool concurrent) {
   const moe_layer_desc& d = c->d;
   CopyArgs a{};
@@ -894,6 +921,8 @@ moe_status launch_ag(moe_ctx* c, Card& cd, int j, int landing, cudaStream_t s, b
   }
   a.err = cd.err;
   if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;
+  if (!is_virtual(c))  // this chunk's cross-node rows arrived (fp8 wire): decode before forwarding
+    if (moe_status st = wire_dequant(c, cd, MOE_O1, j, s)) return st;
   size_t sl;
   span_begin(c, MOE_STAGE_AG, j, s, &sl);
   MONTA_CUDA(launch_seg_copy(a, copy_vec(c, true), copy_grid(c, concurrent, false), s));
@@ -973,7 +1002,7 @@ moe_status dispatch_tail_wait(moe_ctx* c, Card& cd, int level, int n, int landin
 // The persistent dispatch runs (and declines nothing later) when the rows
 // take 4+-byte vectors and 16+ CTAs are co-resident (four roles of >= 4).
 bool xchg_eligible(moe_ctx* c, int level) {
-  if (!c->use_xchg || c->aa_ctas > 0 || is_virtual(c)) return false;
+  if (!c->use_xchg || c->aa_ctas > 0 || c->wire != MOE_WIRE_BF16 || is_virtual(c)) return false;
   const bool dedup = level != MOE_BASELINE && c->d.t > 1;
   const int vec = copy_vec(c, dedup);
   return vec >= 4 && xchg_max_ctas(vec) >= 16;
@@ -1096,6 +1125,8 @@ moe_status validate_dispatch(moe_ctx* c, int level, int n, int landing) {
     return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch_chunked: tensor group must evenly split the payload");
   if (landing != MOE_LAND_FINAL && landing != MOE_LAND_STAGED)
     return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch: bad landing mode");
+  if (c->wire == MOE_WIRE_FP8 && landing == MOE_LAND_STAGED && level != MOE_BASELINE)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "dispatch: the fp8 wire lands in pre: FINAL landing only");
   return MOE_OK;
 }
 
@@ -1145,6 +1176,8 @@ moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t
     for (int j = 0; j < n; ++j) {
       for (auto& cd : c->local)
         if (moe_status st = launch_aa(c, cd, level, j, landing, s, false)) return st;
+      for (auto& cd : c->local)
+        if (moe_status st = wire_dequant(c, cd, level, j, s)) return st;
       if (dedup)
         for (auto& cd : c->local)
           if (moe_status st = launch_ag(c, cd, j, landing, s, false)) return st;
@@ -1187,7 +1220,9 @@ moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t
   MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_aa, 0));
   MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_ag, 0));
   MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_d2d, 0));
-  return dispatch_tail_wait(c, cd, level, n, landing, s);
+  if (moe_status st = dispatch_tail_wait(c, cd, level, n, landing, s)) return st;
+  if (!dedup) return wire_dequant(c, cd, level, -1, s);  // (deduplicated: decoded per chunk before the AllGather)
+  return MOE_OK;
 }
 
 }  // namespace
@@ -1410,7 +1445,7 @@ moe_status combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
   // un-permute writes only local HBM: a separate launch of the top-k item
   // kernel (3-4 CTAs per SM) beats the persistent kernel's register-capped
   // un-permute, so only chunked or deduplicated combines go persistent.
-  if (c->use_xchg && c->aa_ctas == 0 && (n > 1 || dedup)) {
+  if (c->use_xchg && c->aa_ctas == 0 && c->wire == MOE_WIRE_BF16 && (n > 1 || dedup)) {
     bool done = false;
     if (moe_status st = launch_combine_persistent(c, cd, level, n, s, &done)) return st;
     if (done) return MOE_OK;
@@ -1643,6 +1678,22 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
 }
 
 }  // namespace
+
+extern "C" moe_status moe_ctx_set_wire(moe_ctx* c, int wire) {
+  if (moe_status st = check_ready(c)) return st;
+  if (wire != MOE_WIRE_BF16 && wire != MOE_WIRE_FP8) return fail(MOE_ERR_INVALID_ARGUMENT, "set_wire: unknown format %d", wire);
+  const moe_layer_desc& d = c->d;
+  if (wire == MOE_WIRE_FP8 && (d.dtype != MOE_BF16 || d.hidden % 128 || (d.hidden / d.t) % 128 || d.top_k > 16))
+    return fail(MOE_ERR_INVALID_ARGUMENT,
+                "set_wire: the fp8 wire needs a bf16 payload, hidden and hidden/t multiples of 128, top_k <= 16");
+  if (c->wire != wire) {
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+  }
+  c->wire = wire;
+  return MOE_OK;
+}
 
 extern "C" moe_status moe_ctx_enable_checks(moe_ctx* c, int enable) {
   if (moe_status st = check_ready(c)) return st;

@@ -112,10 +112,22 @@ struct TokArgs {
   int64_t dst_stride;
   char* dst[kMaxCards];
   int32_t* dst_tags[kMaxCards];
+  // fp8 wire (moe_ctx_set_wire): cross-node legs store e4m3 bytes + one fp32
+  // scale per 128 elements into the receiver's pre / wscale instead of bf16
+  int32_t fp8, node, t, blocks_per_row;
+  char* dst_pre[kMaxCards];
+  float* dst_scale[kMaxCards];
   SignalList sig;
   int32_t* err;
 };
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s);
+// fp8 wire receive side (aa.cu): rows of this card that came from another
+// node with source position in [p0, p1): columns [col0, col0 + width) of
+// recv (bf16) = dequant(pre (e4m3), wscale)
+cudaError_t launch_wire_dequant(char* recv, const int32_t* tags, const int64_t* recv_rows, int64_t cap,
+                                const char* pre, const float* scales, int64_t row_bytes, int blocks_per_row,
+                                int node, int t, int64_t col0, int64_t width, int64_t p0, int64_t p1,
+                                cudaStream_t s);
 
 // Persistent exchange (xchg.cu): the whole chunked dispatch of one card in
 // one cooperative launch.  CTA roles, in order: AA (cross-node legs), AAL

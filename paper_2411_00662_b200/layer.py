@@ -203,6 +203,10 @@ class MoeLayer:
     def backward(self, level: int = O1, n: int = 1, stream=None) -> None:
         check(self.lib.moe_ctx_backward(self._ctx, level, n, _stream_ptr(stream)))
 
+    def set_wire(self, wire: int) -> None:
+        """Cross-node dispatch payload format: _lib.WIRE_BF16 (exact) or _lib.WIRE_FP8."""
+        check(self.lib.moe_ctx_set_wire(self._ctx, wire))
+
     def enable_checks(self, enable: bool = True) -> None:
         """Poison + verify the landed rows' tags every dispatch (CorruptRoutingError on failure)."""
         check(self.lib.moe_ctx_enable_checks(self._ctx, int(enable)))
