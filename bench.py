@@ -409,6 +409,8 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--aa-ctas", type=int, default=0,
                     help="B1-throttled mode: cap the cross-node AllToAll legs at this many CTAs (0: off)")
+    ap.add_argument("--wire", default="bf16", choices=["bf16", "fp8"],
+                    help="cross-node dispatch payload (fp8: e4m3 + per-128 scales, lossy; SURVEY §8(f) item 3)")
     ap.add_argument("--no-persistent", action="store_true",
                     help="multi-GPU: one launch per (leg, chunk) instead of the persistent exchange kernels")
     args = ap.parse_args()
@@ -474,6 +476,8 @@ def main():
         layer.set_persistent(False)
     if args.aa_ctas:
         layer.set_aa_ctas(args.aa_ctas)
+    if args.wire == "fp8":
+        layer.set_wire(_lib.WIRE_FP8)
     cd = layer.cards[0]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + node)
     x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(PD)
@@ -619,7 +623,7 @@ def main():
     if not args.quick and t > 1:
         pipelined = []
         for lv, nn, ld in ((O2, 4, LAND_FINAL), (O3, 4, LAND_STAGED), (O2, 8, LAND_FINAL)):
-            if T % nn or nn > layer.max_chunks:
+            if T % nn or nn > layer.max_chunks or (ld == LAND_STAGED and args.wire == "fp8"):
                 continue
             for _ in range(3):
                 step(lv, nn, ld)
@@ -783,7 +787,7 @@ def main():
             "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic (randn x, randn f32 gate logits)",
             "config": workload_config(e, t),
             "schedule": {"level": _lib.LEVEL_NAMES[level], "chunks": n, "landing": args.landing,
-                         "aa_ctas": args.aa_ctas or None,
+                         "aa_ctas": args.aa_ctas or None, "wire": args.wire,
                          "cuda_graphs": not args.no_graphs,
                          "planner": None if decision is None else
                          {"reference": {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,

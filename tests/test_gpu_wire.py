@@ -57,10 +57,11 @@ def test_fp8_wire_rows_and_combine(cuda, e, t, E, k, level, n):
             want = torch.from_numpy(want_rows.copy()).view(torch.bfloat16).reshape(rows, h).clone()
             want[~own] = rt[src[~own], pos[~own]]  # crossed a node: the fp8 round trip
             assert torch.equal(got.view(torch.int16), want.view(torch.int16)), cd.card
-            if (~own).any():  # and that round trip is genuinely lossy but close
-                err = ((got[~own].float() - x[src[~own], pos[~own]].float()).abs()
-                       / x[src[~own], pos[~own]].float().abs().clamp_min(1e-30))
-                assert err.max() <= 2.0 ** -4 + 1e-6
+            if (~own).any():  # and that round trip is lossy but bounded: one e4m3 rounding
+                xs = x[src[~own], pos[~own]].float()
+                scale = xs.view(-1, h // 128, 128).abs().amax(-1, keepdim=True).expand(-1, -1, 128).reshape(xs.shape) / 448
+                bound = (2.0 ** -4 + 2.0 ** -8) * xs.abs() + scale * 2.0 ** -9
+                assert ((got[~own].float() - xs).abs() <= bound).all()
         layer.combine(level, n)
         layer.sync()
         for cd in layer.cards:

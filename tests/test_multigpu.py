@@ -181,3 +181,15 @@ def test_two_gpus_ep2_with_experts(cuda, tmp_path):
 def test_four_gpus_2x2_with_experts(cuda, tmp_path):
     runs = "0:1:0,1:1:0,2:2:1,3:4:0"
     _check_experts(_launch(tmp_path, 2, 2, runs=runs, ffn=256, graphs=1), 2, 2, 8, 256, runs)
+
+
+@pytest.mark.parametrize("e,t,runs", [(2, 1, "0:1"), (2, 2, "1:1,0:1,2:2,3:4")])
+def test_fp8_wire_multiprocess(cuda, e, t, runs):
+    world = e * t
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs, have {torch.cuda.device_count()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_wire_worker.py"),
+           "--groups", str(e), "--tp", str(t), "--runs", runs]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
