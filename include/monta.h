@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define MONTA_ABI_VERSION 1
+#define MONTA_ABI_VERSION 2
 
 typedef enum moe_status {
   MOE_OK = 0,

@@ -14,6 +14,8 @@ import pathlib
 PKG = pathlib.Path(__file__).resolve().parent
 LIB_PATH = PKG / "lib" / "libmonta.so"
 
+ABI_VERSION = 2  # include/monta.h MONTA_ABI_VERSION (the card view / structs this binding mirrors)
+
 # moe_status
 OK = 0
 ERR_INVALID_ARGUMENT = 1
@@ -270,6 +272,8 @@ def load(path: str | os.PathLike | None = None):
         except Exception as exc:  # pragma: no cover - depends on toolchain
             raise ImportError(f"libmonta.so missing at {p} and could not be built: {exc}") from exc
     lib = C.CDLL(str(p), mode=C.RTLD_GLOBAL)
+    if not os.environ.get("MONTA_LIB") and lib.moe_abi_version() != ABI_VERSION:
+        raise ImportError(f"{p}: ABI version {lib.moe_abi_version()}, this binding needs {ABI_VERSION} (rebuild)")
     for name, (res, args) in SIGNATURES.items():
         if os.environ.get("MONTA_LIB") and not hasattr(lib, name):
             continue  # A/B against an older build: symbols it predates stay unbound

@@ -19,7 +19,7 @@ def header_functions():
 
 def test_library_loads_and_reports_version():
     lib = _lib.load()
-    assert lib.moe_abi_version() == 1
+    assert lib.moe_abi_version() == 2  # 2: card view grew (recv_expert_offsets, grad_probs, grad_logits)
     assert lib.moe_dtype_size(_lib.BF16) == 2 and lib.moe_dtype_size(_lib.I64) == 8
 
 
