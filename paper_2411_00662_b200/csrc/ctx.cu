@@ -1511,7 +1511,7 @@ moe_status forward_host_pipelined(moe_ctx* c, int level, int landing, const void
                                   cudaStream_t s) {
   const moe_layer_desc& d = c->d;
   Card& cd = c->local[0];
-  int P = std::min(8, d.max_chunks);
+  int P = std::min(16, d.max_chunks);
   while (P > 1 && d.tokens % P) --P;
   const int64_t ct = d.tokens / P;
   const size_t xrow = size_t(c->row_bytes), orow = size_t(d.hidden) * c->ob;
