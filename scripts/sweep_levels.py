@@ -32,19 +32,25 @@ def main():
     ap.add_argument("--experts", type=int, default=8)
     ap.add_argument("--topk", type=int, default=2)
     ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--config", default=None, help="a bench.py workload name (overrides the shape flags)")
     a = ap.parse_args()
     world, rank = int(os.environ["WORLD_SIZE"]), int(os.environ["RANK"])
     local = int(os.environ.get("LOCAL_RANK", rank))
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    if a.config:
+        bench.select_workload(a.config)
+        a.tokens, a.hidden, a.experts, a.topk = (bench.CONFIG[x] for x in ("tokens_per_node", "hidden", "experts",
+                                                                            "top_k"))
     e, t = bench.topo_for(world)
     T, h, E, k = a.tokens, a.hidden, a.experts, a.topk
-    layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, max_chunks=16, device=local, rank=rank, world_size=world)
+    PD = bench.payload_dtype() if a.config else torch.bfloat16
+    layer = MoeLayer(e, t, E, k, T, h, dtype=PD, max_chunks=16, device=local, rank=rank, world_size=world)
     layer.connect()
     layer.enable_graphs(True)
     cd = layer.cards[0]
     g = torch.Generator(device=f"cuda:{local}").manual_seed(99 + cd.node)
-    cd.x.copy_(torch.randn(T, h, generator=g, device=f"cuda:{local}").to(torch.bfloat16))
+    cd.x.copy_(torch.randn(T, h, generator=g, device=f"cuda:{local}").to(PD))
     cd.logits.copy_(torch.randn(T, E, generator=g, device=f"cuda:{local}"))
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=f"cuda:{local}")
     bar = torch.zeros(1, device=f"cuda:{local}")
@@ -85,25 +91,36 @@ def main():
             busy, ex = bench.role_stats(layer.xchg_trace())
             exp.append(ex)
             roles = busy
+        disp = []
+        for _ in range(3):  # the dispatch exchange alone (the span of its kernel[s]), as the planner predicts it
+            flush.zero_()
+            dist.all_reduce(bar)
+            step()
+            disp.append(sum((b - a) * 1e3 for st, j, a, b in layer.spans() if st in ("aa", "ag", "d2d")))
         layer.enable_timing(False)
-        pred = None
+        pred, pred_b200 = None, None
         if curves is not None and lv != BASELINE:
-            m = P.ModelSpec(b=1, s=T * k, h=h, bpe=2)
+            m = P.ModelSpec(b=1, s=T * k, h=h, bpe=torch.empty((), dtype=PD).element_size())
             par = P.ParallelSpec(t=t, e=e)
             cl = P.b200_cluster(e, t)
             if lv == O1:
-                pred = P.o1_time(P.traffic_volume(m), t, e, cl.b1, cl.b2, curves, ov)
+                pred = pred_b200 = P.o1_time(P.traffic_volume(m), t, e, cl.b1, cl.b2, curves, ov)
             else:
                 vol = P.traffic_volume(m)
-                tm = (P.chunk_alltoall_time(vol, n, t, e, cl.b1, curves.alltoall, ov),
-                      P.chunk_allgather_time(vol, n, t, cl.b2, curves.allgather, ov),
-                      P.chunk_d2d_time(vol, n, cl.b3, curves.d2d, ov))
-                pred = (P.o2_score if lv == O2 else P.o3_score)(*tm, n)
+                aa, ag, dd = (P.chunk_alltoall_time(vol, n, t, e, cl.b1, curves.alltoall, ov),
+                              P.chunk_allgather_time(vol, n, t, cl.b2, curves.allgather, ov),
+                              P.chunk_d2d_time(vol, n, cl.b3, curves.d2d, ov))
+                pred = (P.o2_score if lv == O2 else P.o3_score)(aa, ag, dd, n)
+                # the B200 shared-egress score (moe_select_strategy_b200)
+                pred_b200 = n * (aa + ag) + dd + ((n - 1) * max(0.0, dd - aa) if lv == O2 else 0.0)
         if rank == 0:
             print(json.dumps({"topology": f"{e}x{t}", "level": ["Baseline", "O1", "O2", "O3"][lv], "n": n,
                               "us_per_layer": float(v.item()), "exposed_alltoall_us": sum(exp) / len(exp),
                               "roles_busy_us": {r: round(x, 1) for r, x in roles.items()},
-                              "planner_dispatch_pred_us": None if pred is None else pred * 1e6}), flush=True)
+                              "dispatch_exchange_us": sum(disp) / len(disp),
+                              "planner_dispatch_pred_us": None if pred is None else pred * 1e6,
+                              "b200_shared_egress_pred_us": None if pred_b200 is None else pred_b200 * 1e6}),
+                  flush=True)
     layer.close()
     dist.barrier()
     dist.destroy_process_group()
