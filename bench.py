@@ -39,6 +39,8 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 os.environ.setdefault("NCCL_DEBUG", "WARN")
+# the reference arm / cpu_baseline time the CPU port with every host thread
+os.environ.setdefault("OMP_NUM_THREADS", str(os.cpu_count() or 1))
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")  # NCCL logs (its version line too) off stdout: one JSON line
 
 # BASELINE.json configs as workloads (--config); the default, configs[1], is the metric's workload and the
@@ -223,6 +225,12 @@ def nvlink_legs(experts, e, t, E, T, h, node, dedup, recv_rows, busy):
 
 
 # ---------------------------------------------------------------------------
+def cpu_threads() -> int:
+    """Host threads the CPU port uses: OMP_NUM_THREADS, else every host thread
+    (bench.py sets it before the oracle library loads)."""
+    return int(os.environ.get("OMP_NUM_THREADS") or os.cpu_count() or 1)
+
+
 def cpu_port_layer(e, t, E, k, T, h, seed=0):
     """One full layer of the oracle port (oracle/moe_oracle.c: the C
     restatement of the reference data plane, E > e generalised) on the host,
@@ -259,10 +267,11 @@ def cpu_baseline_value(e, t, E, k, T, h, budget_s=10.0, max_reps=100):
 
 def run_reference(args):
     """--impl reference: the reference's CPU path on this host (rank 0 only).
-    The reference headers (oracle/_ref) cannot run this workload — with E = 8
-    experts on e < 8 nodes its dispatch drops records and its combine indexes
-    out of bounds (SURVEY.md §7 decision 1) — so the arm times the oracle port,
-    the C restatement of the same algorithm generalised to E > e."""
+    The reference headers (oracle/_ref) cannot run this workload — with more
+    experts than nodes (E = 160 on e <= 4) its dispatch drops records and its
+    combine indexes out of bounds (SURVEY.md §7 decision 1) — so the arm times
+    the oracle port, the C restatement of the same algorithm generalised to
+    E > e, on every host thread (OpenMP over tokens, experts and records)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
@@ -276,9 +285,9 @@ def run_reference(args):
             "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "weak",
             "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic", "impl": "reference",
             "config": workload_config(e, t),
-            "cpu_baseline": {"value": v, "unit": "us/layer", "cores": 1, "kind": "port",
+            "cpu_baseline": {"value": v, "unit": "us/layer", "cores": cpu_threads(), "kind": "port",
                              "sample": f"full layer ({T} tokens x {e} nodes) per step, {args.steps} steps; "
-                                       f"oracle/moe_oracle.c, 1 thread of {os.cpu_count()}"},
+                                       f"oracle/moe_oracle.c (OpenMP), {cpu_threads()} threads of {os.cpu_count()}"},
             "e2e": {"value": v, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -771,9 +780,10 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.quick:
         cpu_us, reps, secs = cpu_baseline_value(e, t, E, k, T, h)
-        cpu = {"value": cpu_us, "unit": "us/layer", "cores": 1, "kind": "port",
+        cpu = {"value": cpu_us, "unit": "us/layer", "cores": cpu_threads(), "kind": "port",
                "sample": f"{reps} full layers ({T} tokens, {secs:.1f} s CPU); oracle/moe_oracle.c "
-                         f"route+permute+dispatch+combine, 1 thread of {os.cpu_count()} host threads"}
+                         f"route+permute+dispatch+combine (OpenMP over tokens / experts / records), "
+                         f"{cpu_threads()} threads of {os.cpu_count()} host threads"}
 
     backward = None
     if world == 1 and not args.quick:

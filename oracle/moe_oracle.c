@@ -20,8 +20,14 @@
  *
  * Status codes match include/monta.h: 0 ok, 1 invalid argument, 2 corrupt
  * routing, 6 out of memory.
+ *
+ * Host threads (OpenMP, OMP_NUM_THREADS): the router, permute, monolithic
+ * dispatch and combine split their independent work (tokens, experts,
+ * records) across threads; every output position is computed exactly as the
+ * serial loops define it, so results do not depend on the thread count.
  */
 #include <math.h>
+#include <omp.h>
 #include <stdint.h>
 #include <stdlib.h>
 #include <string.h>
@@ -46,10 +52,18 @@ int oracle_route_topk(const double* scores, int64_t T, int E, int k, int32_t* ex
   if (T == 0) return OK;
   if (E < 1) return err(INVALID, "route_topk: empty gate score row");
   if (k > E) return err(INVALID, "route_topk: k exceeds the expert count");
+  int oom = 0;
+#pragma omp parallel
+  {
   double* soft = (double*)malloc(sizeof(double) * E);
   int* order = (int*)malloc(sizeof(int) * E);
-  if (!soft || !order) return err(OOM, "route_topk: oom");
+  if (!soft || !order) {
+#pragma omp atomic write
+    oom = 1;
+  }
+#pragma omp for schedule(static)
   for (int64_t i = 0; i < T; ++i) {
+    if (!soft || !order) continue;
     const double* s = scores + i * E;
     double peak = s[0];
     for (int x = 0; x < E; ++x) peak = s[x] > peak ? s[x] : peak;
@@ -84,6 +98,8 @@ int oracle_route_topk(const double* scores, int64_t T, int E, int k, int32_t* ex
   }
   free(soft);
   free(order);
+  }
+  if (oom) return err(OOM, "route_topk: oom");
   return OK;
 }
 
@@ -95,17 +111,41 @@ int oracle_permute(const int32_t* experts, int64_t T, int k, int32_t* perm_src, 
                    int32_t* inv, int32_t* inv_len) {
   int max_expert = -1;
   for (int64_t q = 0; q < T * k; ++q) max_expert = experts[q] > max_expert ? experts[q] : max_expert;
-  for (int64_t i = 0; i < T; ++i) inv_len[i] = 0;
-  int64_t r = 0;
-  for (int x = 0; x <= max_expert; ++x)
+  /* the serial definition: for x ascending, for token i, for slot s with
+   * experts[i,s] == x, append record (i); token i's inverse map lists its
+   * records in that order.  Record index = start[x] + rank among x's
+   * records; inverse slot = number of token i's entries appended before it
+   * (smaller expert, or equal expert at an earlier slot) — each computed
+   * independently, so experts split across threads. */
+  const int nx = max_expert + 1;
+  int64_t* start = (int64_t*)calloc((size_t)(nx > 0 ? nx : 1) + 1, sizeof(int64_t));
+  if (!start) return err(OOM, "permute: oom");
+  for (int64_t q = 0; q < T * k; ++q)
+    if (experts[q] >= 0) ++start[experts[q] + 1];
+  for (int x = 0; x < nx; ++x) start[x + 1] += start[x];
+  for (int64_t i = 0; i < T; ++i) {
+    int n = 0;
+    for (int s = 0; s < k; ++s) n += experts[i * k + s] >= 0 && experts[i * k + s] <= max_expert;
+    inv_len[i] = n;
+  }
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int x = 0; x < nx; ++x) {
+    int64_t r = start[x];
     for (int64_t i = 0; i < T; ++i)
       for (int s = 0; s < k; ++s) {
         if (experts[i * k + s] != x) continue;
-        inv[i * k + inv_len[i]++] = (int32_t)r;
+        int slot = 0;
+        for (int s2 = 0; s2 < k; ++s2) {
+          const int32_t y = experts[i * k + s2];
+          if (y >= 0 && (y < x || (y == x && s2 < s))) ++slot;
+        }
+        inv[i * k + slot] = (int32_t)r;
         perm_src[r] = (int32_t)i;
         expert_of[r] = x;
         ++r;
       }
+  }
+  free(start);
   return OK;
 }
 
@@ -141,19 +181,54 @@ int oracle_dispatch_monolithic(const oracle_batches* b, uint8_t* rows, int32_t* 
                                int64_t cap) {
   const int L = b->E / b->e;
   const int64_t R = b->T * b->k;
+  /* destination of record (g, r) with expert x*L + l on node x:
+   * base(x, l, g) + its rank among g's records of that expert (the serial
+   * order: for l, for g, for r); ranks from one pass per node g */
+  const int64_t nb = (int64_t)b->e * b->E;
+  int64_t* base = (int64_t*)calloc((size_t)(nb > 0 ? nb : 1), sizeof(int64_t)); /* [g][expert] */
+  int64_t* rank = (int64_t*)malloc(sizeof(int64_t) * (size_t)(b->e * R > 0 ? b->e * R : 1));
+  if (!base || !rank) {
+    free(base);
+    free(rank);
+    return err(OOM, "dispatch_monolithic: oom");
+  }
+  int64_t* seen = (int64_t*)calloc((size_t)(b->E > 0 ? b->E : 1), sizeof(int64_t));
+  for (int g = 0; g < b->e; ++g) {
+    for (int xe = 0; xe < b->E; ++xe) seen[xe] = 0;
+    for (int64_t r = 0; r < b->n_records[g]; ++r) {
+      const int32_t xe = b->expert_of[g * R + r];
+      rank[g * R + r] = (xe >= 0 && xe < b->E) ? seen[xe]++ : -1;
+    }
+    for (int xe = 0; xe < b->E; ++xe) base[(int64_t)g * b->E + xe] = seen[xe]; /* counts for now */
+  }
+  free(seen);
   for (int x = 0; x < b->e; ++x) {
     int64_t at = 0;
-    uint8_t* nr = rows + (int64_t)x * cap * b->row_bytes;
-    int32_t* nt = tags + (int64_t)x * cap * 4;
     for (int l = 0; l < L; ++l)
-      for (int g = 0; g < b->e; ++g)
-        for (int64_t r = 0; r < b->n_records[g]; ++r) {
-          if (b->expert_of[g * R + r] != x * L + l) continue;
-          if (at >= cap) return err(INVALID, "dispatch_monolithic: capacity exceeded");
-          emit(nr, nt, at++, b, g, r, 0, b->row_bytes);
-        }
+      for (int g = 0; g < b->e; ++g) {
+        const int64_t c = base[(int64_t)g * b->E + x * L + l];
+        base[(int64_t)g * b->E + x * L + l] = at;
+        at += c;
+      }
+    if (at > cap) {
+      free(base);
+      free(rank);
+      return err(INVALID, "dispatch_monolithic: capacity exceeded");
+    }
     count[x] = at;
   }
+  for (int g = 0; g < b->e; ++g) {
+#pragma omp parallel for schedule(static)
+    for (int64_t r = 0; r < b->n_records[g]; ++r) {
+      const int32_t xe = b->expert_of[g * R + r];
+      if (xe < 0 || xe >= L * b->e) continue; /* experts no node hosts are dropped */
+      const int x = xe / L;
+      emit(rows + (int64_t)x * cap * b->row_bytes, tags + (int64_t)x * cap * 4,
+           base[(int64_t)g * b->E + xe] + rank[g * R + r], b, g, r, 0, b->row_bytes);
+    }
+  }
+  free(base);
+  free(rank);
   return OK;
 }
 
@@ -274,7 +349,12 @@ int oracle_combine(const oracle_batches* b, int dtype, const uint8_t* y, const i
   int64_t* where = (int64_t*)malloc(sizeof(int64_t) * (size_t)(keys > 0 ? keys : 1));
   if (!where) return err(OOM, "combine: oom");
   for (int64_t q = 0; q < (int64_t)b->e * b->T * width; ++q) out[q] = 0.0;
+  /* every token is independent (its slots accumulate in ascending order, as
+   * in the serial loops): tokens split across threads; the first failing
+   * token in (x, g, i) order reports, as the serial scan would */
   int status = OK;
+  int64_t bad_at = -1;
+  int bad_code = OK;
   for (int x = 0; x < b->e && status == OK; ++x) {
     for (int64_t q = 0; q < keys; ++q) where[q] = -1;
     for (int64_t r = 0; r < y_count[x]; ++r) {
@@ -283,28 +363,50 @@ int oracle_combine(const oracle_batches* b, int dtype, const uint8_t* y, const i
       if (g < 0 || g >= b->e || pos < 0 || pos >= b->T || xe / L != x) continue;
       where[((int64_t)g * b->T + pos) * L + (xe - x * L)] = r;
     }
-    for (int g = 0; g < b->e && status == OK; ++g)
-      for (int64_t i = 0; i < b->T; ++i) {
-        if (inv_len[(int64_t)g * b->T + i] == 0 || inv_len[(int64_t)g * b->T + i] != b->k) {
-          status = err(CORRUPT, "combine_unpermute: inverse map does not match routing");
-          break;
-        }
-        out_token[(int64_t)g * b->T + i] =
-            b->token_ids[(int64_t)g * b->T + b->perm_src[g * R + inv[((int64_t)g * b->T + i) * b->k]]];
+    const int64_t n_tok = (int64_t)b->e * b->T;
+#pragma omp parallel for schedule(static)
+    for (int64_t gi = 0; gi < n_tok; ++gi) {
+      const int64_t g = gi / b->T;
+      int code = OK;
+      if (inv_len[gi] == 0 || inv_len[gi] != b->k) code = CORRUPT + 100; /* inverse map */
+      if (code == OK) {
+        out_token[gi] = b->token_ids[gi - (gi % b->T) + b->perm_src[g * R + inv[gi * b->k]]];
         for (int64_t s = 0; s < b->k; ++s) {
-          const int xe = experts[((int64_t)g * b->T + i) * b->k + s];
+          const int xe = experts[gi * b->k + s];
           if (xe / L != x) continue; /* handled when node xe/L is scanned */
-          const int64_t r = where[((int64_t)g * b->T + i) * L + (xe - x * L)];
+          const int64_t r = where[gi * L + (xe - x * L)];
           if (r < 0) {
-            status = err(CORRUPT, "combine_unpermute: missing expert output");
+            code = CORRUPT;
             break;
           }
           const uint8_t* row = y + ((int64_t)x * cap + r) * b->row_bytes;
-          const double p = probs[((int64_t)g * b->T + i) * b->k + s];
-          double* o = out + ((int64_t)g * b->T + i) * width;
-          for (int64_t q = 0; q < width; ++q) o[q] += p * decode(row + q * esz, dtype);
+          const double p = probs[gi * b->k + s];
+          double* o = out + gi * width;
+          if (dtype == BF16) { /* the common payload, decoded inline (same value as decode()) */
+            for (int64_t q = 0; q < width; ++q) {
+              uint16_t hb;
+              memcpy(&hb, row + q * 2, 2);
+              const uint32_t u = (uint32_t)hb << 16;
+              float v;
+              memcpy(&v, &u, 4);
+              o[q] += p * (double)v;
+            }
+          } else {
+            for (int64_t q = 0; q < width; ++q) o[q] += p * decode(row + q * esz, dtype);
+          }
         }
       }
+      if (code != OK) {
+#pragma omp critical
+        if (bad_at < 0 || gi < bad_at) {
+          bad_at = gi;
+          bad_code = code;
+        }
+      }
+    }
+    if (bad_at >= 0)
+      status = err(CORRUPT, bad_code == CORRUPT + 100 ? "combine_unpermute: inverse map does not match routing"
+                                                      : "combine_unpermute: missing expert output");
   }
   free(where);
   return status;
