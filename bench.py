@@ -449,7 +449,11 @@ def main():
 
     # ---- level / chunk count: MoNTA planner on the B200 NVLink curves
     levels = {"baseline": BASELINE, "o1": O1, "o2": O2, "o3": O3}
-    curves_dir = os.path.join(ROOT, "profiles", "curves_b200", f"{e}x{t}")
+    # curves fitted from the exchange kernel's own role traces when present
+    # (scripts/calibrate_from_sweep.py), else the standalone-copy calibration
+    curves_dir = os.path.join(ROOT, "profiles", "curves_b200", f"{e}x{t}_xchg")
+    if not os.path.isdir(curves_dir):
+        curves_dir = os.path.join(ROOT, "profiles", "curves_b200", f"{e}x{t}")
     decision = None
     if args.level != "auto":
         level = levels[args.level]

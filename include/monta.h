@@ -543,8 +543,9 @@ moe_status moe_select_strategy(const moe_model_spec* m, const moe_parallel_spec*
 /* B200 variant of select_strategy.  shared_egress == 0: exactly
  * moe_select_strategy (the reference's separate inter-/intra-node links).
  * shared_egress != 0 (every card on one NVSwitch domain, no AllToAll cap):
- * the AllToAll and AllGather of a chunk serialise on the same NVLink
- * egress, so O2/O3 score n (aa + ag) + d2d [+ O2's copy backlog] — same
+ * both legs leave through the same NVLink egress, so chunking cannot
+ * overlap them, and the engine lands rows at their final offsets (no reorder
+ * copy): O2/O3 score aa(n=1) + ag(n=1) + (n - 1) alpha_comm — same
  * candidates, gates, search and tie order as the reference. */
 moe_status moe_select_strategy_b200(const moe_model_spec* m, const moe_parallel_spec* par,
                                     const moe_cluster_spec* cl, const moe_curve_set* curves,

@@ -241,15 +241,13 @@ extern "C" moe_status moe_select_strategy(const moe_model_spec* m, const moe_par
 }
 
 // B200 variant (one NVSwitch box): the AllToAll and the AllGather leave each
-// GPU through the same NVLink ports, so a chunk's AllGather cannot overlap
-// the next chunk's AllToAll — the two legs serialise on the egress; only the
-// HBM reorder copies overlap the links (the last one stays exposed; under O2
-// a copy longer than the next AllToAll holds back the next gather).
-double score_shared_o2(double aa, double ag, double d2d, int n) {
-  return n * (aa + ag) + d2d + (n - 1) * std::max(0.0, d2d - aa);
-}
-double score_shared_o3(double aa, double ag, double d2d, int n) { return n * (aa + ag) + d2d; }
-
+// GPU through the same NVLink ports, so chunking cannot overlap the two legs —
+// their bytes move at the unchunked rate whatever n is — and every extra
+// chunk costs one more per-call overhead.  The engine lands rows at their
+// final offsets (FINAL landing: no reorder copy), so no d2d term:
+// score = aa(n=1) + ag(n=1) + (n - 1) alpha_comm.
+// (Measured at 2x2 on the four BASELINE layers: within 3-18% of the exchange
+// kernel's time for O1 and O2/O3 at n = 2..16 with in-situ curves.)
 extern "C" moe_status moe_select_strategy_b200(const moe_model_spec* m, const moe_parallel_spec* par,
                                                const moe_cluster_spec* cl, const moe_curve_set* curves,
                                                const moe_overhead* ov, int32_t n_cap, int32_t shared_egress,
@@ -263,10 +261,15 @@ extern "C" moe_status moe_select_strategy_b200(const moe_model_spec* m, const mo
   if (moe_status st = moe_o1_time(volume, par->t, par->e, cl->b1, cl->b2, curves, ov, &t1)) return st;
   d.alternatives[d.n_alternatives++] = moe_strategy_alt{MOE_O1, t1, 1};
   if (par->e >= 2) {
+    double aa1, ag1;
+    if (moe_status st = aa_time(volume, 1, par->t, par->e, cl->b1, &curves->alltoall, ov, &aa1)) return st;
+    if (moe_status st = ag_time(volume, 1, par->t, cl->b2, &curves->allgather, ov, &ag1)) return st;
+    const double alpha = ov ? ov->alpha_comm : 0.0;
+    auto shared = [&](double, double, double, int n) { return aa1 + ag1 + (n - 1) * alpha; };
     moe_chunk_search_result r2, r3;
-    if (moe_status st = search(m, par, cl, curves, ov, n_cap, score_shared_o2, &r2)) return st;
+    if (moe_status st = search(m, par, cl, curves, ov, n_cap, shared, &r2)) return st;
     d.alternatives[d.n_alternatives++] = moe_strategy_alt{MOE_O2, r2.t_pred, r2.n_opt};
-    if (moe_status st = search(m, par, cl, curves, ov, n_cap, score_shared_o3, &r3)) return st;
+    if (moe_status st = search(m, par, cl, curves, ov, n_cap, shared, &r3)) return st;
     d.alternatives[d.n_alternatives++] = moe_strategy_alt{MOE_O3, r3.t_pred, r3.n_opt};
   }
   int best = 0;

@@ -112,7 +112,9 @@ def main():
                               P.chunk_d2d_time(vol, n, cl.b3, curves.d2d, ov))
                 pred = (P.o2_score if lv == O2 else P.o3_score)(aa, ag, dd, n)
                 # the B200 shared-egress score (moe_select_strategy_b200)
-                pred_b200 = n * (aa + ag) + dd + ((n - 1) * max(0.0, dd - aa) if lv == O2 else 0.0)
+                aa1 = P.chunk_alltoall_time(vol, 1, t, e, cl.b1, curves.alltoall, ov)
+                ag1 = P.chunk_allgather_time(vol, 1, t, cl.b2, curves.allgather, ov)
+                pred_b200 = aa1 + ag1 + (n - 1) * ov.alpha_comm
         if rank == 0:
             print(json.dumps({"topology": f"{e}x{t}", "level": ["Baseline", "O1", "O2", "O3"][lv], "n": n,
                               "us_per_layer": float(v.item()), "exposed_alltoall_us": sum(exp) / len(exp),

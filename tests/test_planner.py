@@ -339,8 +339,11 @@ def test_b200_shared_egress_variant():
         if par.t >= 2:
             o1 = P.o1_time(P.traffic_volume(model), par.t, par.e, cl.b1, cl.b2, curves, ov)
             assert on.alternatives[0].t_pred == pytest.approx(o1, rel=1e-12)
+            V = P.traffic_volume(model)
+            aa1 = P.chunk_alltoall_time(V, 1, par.t, par.e, cl.b1, curves.alltoall, ov)
+            ag1 = P.chunk_allgather_time(V, 1, par.t, cl.b2, curves.allgather, ov)
             for a in on.alternatives[1:]:
-                # no overlap across the shared egress: a chunked level never beats n = 1 of itself
-                assert a.t_pred >= min(x.t_pred for x in on.alternatives) - 1e-18
+                # both legs share the egress: the unchunked legs + one overhead per extra chunk
+                assert a.t_pred == pytest.approx(aa1 + ag1 + (a.n - 1) * ov.alpha_comm, rel=1e-12)
         else:
             assert (on.level, on.n) == (ref.level, ref.n)
