@@ -375,8 +375,8 @@ moe_status moe_ctx_backward(moe_ctx* ctx, int level, int32_t n_chunks, void* str
 /* Dispatch wire format of the cross-node (AllToAll) legs (SURVEY.md §8(f)
  * item 3).  MOE_WIRE_BF16 (default): rows move bit-exactly.  MOE_WIRE_FP8:
  * the sender quantises each 128-element block of a cross-node row slice to
- * e4m3 (x * (448 / amax), round to nearest, saturating) with one fp32 scale
- * amax / 448 and
+ * e4m3 (x / scale, scale = amax / 448, round to nearest, saturating) with
+ * that fp32 scale and
  * stores bytes + scales into the receiver's pre / scale buffers — half the
  * AllToAll bytes; the receiver decodes them into recv before the intra-node
  * AllGather forwards its slice (bf16).  Own-node rows stay bf16.  Lossy by

@@ -102,15 +102,14 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
 #pragma unroll
             for (int m = 8; m > 0; m >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, m));
             const float scale = amax > 0.f ? amax / 448.f : 1.f;
-            const float inv = amax > 0.f ? 448.f / amax : 1.f;  // one division per block, then multiplies
             if (in) {
               uint32_t w[2];
 #pragma unroll
               for (int j = 0; j < 2; ++j) {
                 const __nv_fp8x2_storage_t lo = __nv_cvt_float2_to_fp8x2(
-                    make_float2(f[4 * j] * inv, f[4 * j + 1] * inv), __NV_SATFINITE, __NV_E4M3);
+                    make_float2(f[4 * j] / scale, f[4 * j + 1] / scale), __NV_SATFINITE, __NV_E4M3);
                 const __nv_fp8x2_storage_t hi = __nv_cvt_float2_to_fp8x2(
-                    make_float2(f[4 * j + 2] * inv, f[4 * j + 3] * inv), __NV_SATFINITE, __NV_E4M3);
+                    make_float2(f[4 * j + 2] / scale, f[4 * j + 3] / scale), __NV_SATFINITE, __NV_E4M3);
                 w[j] = uint32_t(lo) | (uint32_t(hi) << 16);
               }
               *reinterpret_cast<uint2*>(q + v * 8) = make_uint2(w[0], w[1]);

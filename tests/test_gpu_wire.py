@@ -1,7 +1,7 @@
 """fp8 wire for the cross-node dispatch legs (moe_ctx_set_wire, SURVEY.md
 §8(f) item 3): every landed row that crossed a node equals the e4m3 round
 trip of its source row — per 128-element block, scale = amax / 448 (fp32),
-q = e4m3_rn_satfinite(x * (448 / amax)), row = bf16(q * scale) — bit for bit (an
+q = e4m3_rn_satfinite(x / scale), row = bf16(q * scale) — bit for bit (an
 emulation of the wire format in PyTorch); own-node rows stay bit-exact; the
 layer output stays within the combine bound of those rows."""
 import numpy as np
@@ -21,8 +21,7 @@ def _fp8_roundtrip(rows: torch.Tensor) -> torch.Tensor:
     f = rows.float().view(n, h // 128, 128)
     amax = f.abs().amax(-1, keepdim=True)
     scale = torch.where(amax > 0, amax / 448.0, torch.ones_like(amax))
-    inv = torch.where(amax > 0, 448.0 / amax, torch.ones_like(amax))
-    q = (f * inv).clamp(-448.0, 448.0).to(torch.float8_e4m3fn).float()
+    q = (f / scale).clamp(-448.0, 448.0).to(torch.float8_e4m3fn).float()
     return (q * scale).view(n, h).to(torch.bfloat16)
 
 
