@@ -128,6 +128,7 @@ struct moe_ctx {
   bool unit_probs = false;  // combine with unit weights (the layer backward's dispatch adjoint)
   int wire = MOE_WIRE_BF16;  // cross-node dispatch payload format (moe_ctx_set_wire)
   struct GraphEntry {
+    int kind;  // 0 forward, 1 layer backward (moe_ctx_backward)
     int level, n, landing;
     const void *hx, *hl;
     void* ho;
@@ -1629,12 +1630,17 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
 // CUDA-graph path: the whole step (every stream of it) is captured once per
 // (level, n, landing, host buffers) and replayed; flags carry the device
 // epoch, so replays stay in lockstep across ranks.
+moe_status backward_impl(moe_ctx* c, int level, int n, cudaStream_t s);
+
 moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
-                         cudaStream_t s) {
+                         cudaStream_t s, int kind = 0) {
+  auto run = [&](cudaStream_t st) {
+    return kind ? backward_impl(c, level, n, st) : forward_impl(c, level, n, landing, hx, hl, ho, st);
+  };
   for (auto& g : c->graphs)
-    if (g.level == level && g.n == n && g.landing == landing && g.hx == hx && g.hl == hl && g.ho == ho &&
-        g.timed == c->timing) {
-      if (!g.exec) return forward_impl(c, level, n, landing, hx, hl, ho, s);
+    if (g.kind == kind && g.level == level && g.n == n && g.landing == landing && g.hx == hx && g.hl == hl &&
+        g.ho == ho && g.timed == c->timing) {
+      if (!g.exec) return run(s);
       if (g.timed) {  // the replay re-records the captured events: restore their labels
         c->span_used = g.span_labels.size();
         for (size_t i = 0; i < g.span_labels.size(); ++i) {
@@ -1651,10 +1657,10 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
       return MOE_OK;
     }
   // capture on the context's own stream (the legacy stream cannot be captured)
-  moe_ctx::GraphEntry e{level, n, landing, hx, hl, ho, nullptr, 0, c->timing, {}};
+  moe_ctx::GraphEntry e{kind, level, n, landing, hx, hl, ho, nullptr, 0, c->timing, {}};
   const int64_t before = c->launches;
   MONTA_CUDA(cudaStreamBeginCapture(c->s_cap, cudaStreamCaptureModeThreadLocal));
-  moe_status st = forward_impl(c, level, n, landing, hx, hl, ho, c->s_cap);
+  moe_status st = run(c->s_cap);
   cudaGraph_t graph = nullptr;
   cudaError_t err = cudaStreamEndCapture(c->s_cap, &graph);
   e.kernels = c->launches - before;
@@ -1670,11 +1676,11 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
     if (graph) cudaGraphDestroy(graph);
     e.exec = nullptr;
     c->graphs.push_back(e);
-    return forward_impl(c, level, n, landing, hx, hl, ho, s);
+    return run(s);
   }
   cudaGraphDestroy(graph);
   c->graphs.push_back(e);
-  return forward_graph(c, level, n, landing, hx, hl, ho, s);
+  return forward_graph(c, level, n, landing, hx, hl, ho, s, kind);
 }
 
 }  // namespace
@@ -1909,13 +1915,21 @@ extern "C" moe_status moe_ctx_backward_dispatch(moe_ctx* c, int level, int32_t n
   return backward_dispatch_impl(c, level, n, static_cast<cudaStream_t>(stream));
 }
 
+namespace {
+moe_status backward_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
+  if (moe_status st = backward_combine_impl(c, level, n, s)) return st;
+  return backward_dispatch_impl(c, level, n, s);
+}
+}  // namespace
+
 extern "C" moe_status moe_ctx_backward(moe_ctx* c, int level, int32_t n, void* stream) {
   if (moe_status st = check_ready(c)) return st;
   if (moe_status st = validate_dispatch(c, level, n, MOE_LAND_FINAL)) return st;
   MONTA_CUDA(cudaSetDevice(c->device));
   cudaStream_t s = static_cast<cudaStream_t>(stream);
-  if (moe_status st = backward_combine_impl(c, level, n, s)) return st;
-  return backward_dispatch_impl(c, level, n, s);
+  if (c->use_graphs)  // the whole backward replays as one CUDA graph
+    return forward_graph(c, level, n, MOE_LAND_FINAL, nullptr, nullptr, nullptr, s, 1);
+  return backward_impl(c, level, n, s);
 }
 
 extern "C" moe_status moe_ctx_forward_host(moe_ctx* c, int level, int32_t n, int landing, const void* host_x,

@@ -174,3 +174,36 @@ def test_ctx_backward_device_side(cuda, e, t, E, k, level, n):
             assert err < 1e-2, (cd.card, err)
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("e,t,E,k,level,n", [(2, 2, 8, 2, O1, 1), (2, 2, 8, 2, O2, 2), (1, 1, 160, 6, BASELINE, 1)])
+def test_ctx_backward_graph_replay(cuda, e, t, E, k, level, n):
+    """moe_ctx_backward captured once and replayed as a CUDA graph gives the
+    eager result bit for bit (device-resident epochs keep replays in step)."""
+    T, h = 128, 256
+    dt = torch.bfloat16
+    gen = torch.Generator().manual_seed(e + t + E + n)
+    x = torch.randn(e, T, h, generator=gen).to(dt)
+    logits = torch.randn(e, T, E, generator=gen)
+    gout = torch.randn(e, T, h, generator=gen).to(dt)
+    outs = []
+    for graphs in (False, True):
+        layer = MoeLayer(e, t, E, k, T, h, dtype=dt, logit_dtype=torch.float32, max_chunks=max(n, 1), device=0)
+        try:
+            layer.enable_graphs(graphs)
+            res = None
+            for _ in range(3):  # graphs: capture, then replays
+                for cd in layer.cards:
+                    cd.x.copy_(x[cd.node])
+                    cd.logits.copy_(logits[cd.node])
+                layer.forward(level, n)
+                for cd in layer.cards:
+                    cd.x.copy_(gout[cd.node])
+                layer.backward(level, n)
+                layer.sync()
+                res = [(cd.out.clone(), cd.grad_probs.clone(), cd.grad_logits.clone()) for cd in layer.cards]
+            outs.append(res)
+        finally:
+            layer.close()
+    for (a0, b0, c0), (a1, b1, c1) in zip(*outs):
+        assert torch.equal(a0, a1) and torch.equal(b0, b1) and torch.equal(c0, c1)
