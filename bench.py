@@ -418,6 +418,9 @@ def main():
     ap.add_argument("--no-graphs", action="store_true", help="launch eagerly instead of replaying CUDA graphs")
     ap.add_argument("--aa-ctas", type=int, default=0,
                     help="B1-throttled mode: cap the cross-node AllToAll legs at this many CTAs (0: off)")
+    ap.add_argument("--link-gbs", type=float, default=0.0,
+                    help="emulate a slow inter-node link for the cross-node legs (GB/s per card; the paper's "
+                         "B1 << B2 regime, PAPER.md:183-184); the planner then uses the reference's separate-links model")
     ap.add_argument("--wire", default="bf16", choices=["bf16", "fp8"],
                     help="cross-node dispatch payload (fp8: e4m3 + per-128 scales, lossy; SURVEY §8(f) item 3)")
     ap.add_argument("--no-persistent", action="store_true",
@@ -469,12 +472,16 @@ def main():
                                 P.EfficiencyCurve.constant(0.8))
             ov = P.OverheadModel(8e-6, 4e-6)
         model = P.ModelSpec(b=1, s=T * k, h=h, k=k, bpe=ELEM)  # routed rows: s_eff = T*k
+        cluster = P.b200_cluster(e, t)
+        if args.link_gbs:  # emulated inter-node link: paced legs move at exactly that rate
+            cluster = P.b200_cluster(e, t, b1=args.link_gbs * 1e9)
+            curves = P.CurveSet(P.EfficiencyCurve.constant(1.0), curves.allgather, curves.d2d)
         # the reference's selection (separate inter-/intra-node links), reported as is
-        decision = P.select_strategy(model, P.ParallelSpec(t=t, e=e), P.b200_cluster(e, t), curves, ov, n_cap=16)
+        decision = P.select_strategy(model, P.ParallelSpec(t=t, e=e), cluster, curves, ov, n_cap=16)
         # the B200 variant: on one NVSwitch box both legs leave through the same
         # NVLink egress (not so when the AllToAll is throttled: B1-emulated mode)
-        decision_b200 = P.select_strategy_b200(model, P.ParallelSpec(t=t, e=e), P.b200_cluster(e, t), curves, ov,
-                                               n_cap=16, shared_egress=not args.aa_ctas)
+        decision_b200 = P.select_strategy_b200(model, P.ParallelSpec(t=t, e=e), cluster, curves, ov,
+                                               n_cap=16, shared_egress=not (args.aa_ctas or args.link_gbs))
         level, n = int(decision_b200.level), decision_b200.n
         while T % n:
             n -= 1
@@ -491,6 +498,8 @@ def main():
         layer.set_aa_ctas(args.aa_ctas)
     if args.wire == "fp8":
         layer.set_wire(_lib.WIRE_FP8)
+    if args.link_gbs:
+        layer.set_link_rate(args.link_gbs)
     cd = layer.cards[0]
     gen = torch.Generator(device=f"cuda:{local}").manual_seed(1234 + node)
     x0 = torch.randn(T, h, generator=gen, device=f"cuda:{local}").to(PD)
@@ -801,7 +810,7 @@ def main():
             "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic (randn x, randn f32 gate logits)",
             "config": workload_config(e, t),
             "schedule": {"level": _lib.LEVEL_NAMES[level], "chunks": n, "landing": args.landing,
-                         "aa_ctas": args.aa_ctas or None, "wire": args.wire,
+                         "aa_ctas": args.aa_ctas or None, "wire": args.wire, "link_gbs": args.link_gbs or None,
                          "cuda_graphs": not args.no_graphs,
                          "planner": None if decision is None else
                          {"reference": {"level": _lib.LEVEL_NAMES[int(decision.level)], "n": decision.n,

@@ -372,6 +372,14 @@ moe_status moe_ctx_forward_host(moe_ctx* ctx, int level, int32_t n_chunks, int l
 moe_status moe_ctx_backward_combine(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
 moe_status moe_ctx_backward_dispatch(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
 moe_status moe_ctx_backward(moe_ctx* ctx, int level, int32_t n_chunks, void* stream);
+/* Emulated inter-node link (the paper's B1 << B2 regime, PAPER.md:183-184,
+ * on one NVSwitch box): every cross-node leg — the dispatch AllToAll and the
+ * combine's reverse AllToAll, naive or deduplicated — completes no sooner
+ * than its bytes / gbps (GB/s per card), while the intra-node AllGather and
+ * local copies run at NVLink / HBM speed.  0 = off.  Applies to the
+ * persistent exchange kernels and the per-leg copy launches (the token-side
+ * per-leg AllToAll of moe_ctx_set_persistent(0) is not paced). */
+moe_status moe_ctx_set_link_rate(moe_ctx* ctx, double gbps);
 /* Dispatch wire format of the cross-node (AllToAll) legs (SURVEY.md §8(f)
  * item 3).  MOE_WIRE_BF16 (default): rows move bit-exactly.  MOE_WIRE_FP8:
  * the sender quantises each 128-element block of a cross-node row slice to

@@ -188,6 +188,7 @@ SIGNATURES = {
     "moe_comm_priority": (C.c_int, [C.c_int]),
     "moe_ctx_enable_checks": (C.c_int, [_P, C.c_int]),
     "moe_ctx_set_wire": (C.c_int, [_P, C.c_int]),
+    "moe_ctx_set_link_rate": (C.c_int, [_P, C.c_double]),
     "moe_ctx_backward_combine": (C.c_int, [_P, C.c_int, _I32, _P]),
     "moe_ctx_backward_dispatch": (C.c_int, [_P, C.c_int, _I32, _P]),
     "moe_ctx_backward": (C.c_int, [_P, C.c_int, _I32, _P]),

@@ -292,7 +292,9 @@ __global__ void __launch_bounds__(kThreads, 2) k_combine_xchg(const __grid_const
   for (int s = 0; s <= n; ++s) {
     if (s < n && a.e > 1) {
       trace_start(a.trace, 0, a.max_chunks, s);
+      const unsigned long long t0 = globaltimer();
       copy_items<V, false, false>(view_of(a.cp), comb_list(a, s), a.cpr, c, ctas);
+      pace_list(comb_list(a, s), t0, a.cp.pace_bpus);
       chunk_done(a.counters + s * 17, ctas, c, [&] {
         trace_end(a.trace, 0, a.max_chunks, s);
         for (int x = 0; x < a.e; ++x)

@@ -24,7 +24,9 @@ __global__ void __launch_bounds__(kCopyThreads) k_seg_copy(const __grid_constant
   const SegList* L = second ? a.list2 : a.list;
   const int64_t cta = second ? int64_t(blockIdx.x) - a.split : int64_t(blockIdx.x);
   const int64_t ctas = a.list2 ? (second ? int64_t(gridDim.x) - a.split : int64_t(a.split)) : int64_t(gridDim.x);
+  const unsigned long long t0 = globaltimer();
   copy_items<V>(view_of(a), L, a.chunks_per_row, cta, ctas);
+  if (!second) pace_list(L, t0, a.pace_bpus);  // `list` carries the cross-node legs (list2: own-node)
   cta_signal(a.sig);
 }
 

@@ -223,4 +223,21 @@ __device__ __forceinline__ void chunk_done(unsigned int* counter, int role_ctas,
   __syncwarp();
 }
 
+// Emulated slow inter-node link (moe_ctx_set_link_rate): a cross-node leg
+// whose bytes would take longer than `bytes / rate` holds its completion
+// until then — every CTA of the leg waits out the whole list's time from its
+// own start t0, so the leg (and the flag it releases) lands at the emulated
+// rate however fast NVLink moved it.
+__device__ __forceinline__ void pace_list(const SegList* L, unsigned long long t0, uint32_t bpus) {
+  if (!bpus) return;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int64_t bytes = 0;
+    for (int i = 0; i < L->nseg; ++i) bytes += int64_t(L->segs[i].rows) * L->segs[i].width;
+    const unsigned long long until = t0 + (unsigned long long)(bytes * 1000 / int64_t(bpus));
+    while (globaltimer() < until) __nanosleep(256);
+  }
+  __syncthreads();
+}
+
 }  // namespace monta

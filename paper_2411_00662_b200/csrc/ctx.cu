@@ -127,6 +127,7 @@ struct moe_ctx {
   bool checks = false;  // poison + verify the landed rows' tags every dispatch (moe_ctx_enable_checks)
   bool unit_probs = false;  // combine with unit weights (the layer backward's dispatch adjoint)
   int wire = MOE_WIRE_BF16;  // cross-node dispatch payload format (moe_ctx_set_wire)
+  uint32_t pace_bpus = 0;     // emulated inter-node link rate, bytes/us (moe_ctx_set_link_rate)
   struct GraphEntry {
     int kind;  // 0 forward, 1 layer backward (moe_ctx_backward)
     int level, n, landing;
@@ -828,6 +829,7 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
   if (d.e > 1) {
     a.list = list_of(c, cd, kPhaseAA, j);
     a.list2 = list_of(c, cd, kPhaseAAL, j);
+    a.pace_bpus = c->pace_bpus;  // the cross-node list
     // time(local) / time(remote) ~= (full / width) * 0.2 / (e - 1)  (HBM copy vs NVLink store)
     const double r = (dedup ? double(d.t) : 1.0) * 0.2 / double(d.e - 1);
     const double frac = std::min(0.5, std::max(0.1, r / (1.0 + r)));
@@ -1050,6 +1052,7 @@ moe_status launch_dispatch_xchg(moe_ctx* c, Card& cd, int level, int n, int land
     --*big;
   }
   CopyArgs& a = x.cp;
+  a.pace_bpus = c->pace_bpus;  // applied by the AllToAll role only
   a.src = static_cast<const char*>(cd.v.x);
   a.src_stride = c->row_bytes;
   a.gather = cd.v.perm_src;
@@ -1243,6 +1246,7 @@ moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bo
   const bool dedup = level != MOE_BASELINE && d.t > 1;
   CopyArgs a{};
   a.list = list_of(c, cd, kPhaseCAA, j);
+  a.pace_bpus = c->pace_bpus;
   a.src = static_cast<const char*>(cd.v.expert_out);
   a.src_stride = c->row_bytes;
   a.synth_tags = 0;
@@ -1351,6 +1355,7 @@ moe_status launch_combine_persistent(moe_ctx* c, Card& cd, int level, int n, cud
   }
   u.err = cd.err;
   CopyArgs& a = x.cp;
+  a.pace_bpus = c->pace_bpus;  // applied by the reverse AllToAll only
   a.src = static_cast<const char*>(cd.v.expert_out);
   a.src_stride = c->row_bytes;
   a.dst_stride = c->row_bytes;
@@ -1684,6 +1689,19 @@ moe_status forward_graph(moe_ctx* c, int level, int n, int landing, const void* 
 }
 
 }  // namespace
+
+extern "C" moe_status moe_ctx_set_link_rate(moe_ctx* c, double gbps) {
+  if (moe_status st = check_ready(c)) return st;
+  if (!(gbps >= 0.0) || gbps > 4.0e6) return fail(MOE_ERR_INVALID_ARGUMENT, "set_link_rate: bad rate %g GB/s", gbps);
+  const uint32_t bpus = uint32_t(gbps * 1000.0 + 0.5);
+  if (bpus != c->pace_bpus) {
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+  }
+  c->pace_bpus = bpus;
+  return MOE_OK;
+}
 
 extern "C" moe_status moe_ctx_set_wire(moe_ctx* c, int wire) {
   if (moe_status st = check_ready(c)) return st;

@@ -63,6 +63,7 @@ struct CopyArgs {
   WaitList wait;
   SignalList sig;
   int32_t* err;
+  uint32_t pace_bpus;        // emulated inter-node link (moe_ctx_set_link_rate): bytes per us, 0 = off
 };
 
 struct UnpermArgs {

@@ -115,7 +115,9 @@ __global__ void __launch_bounds__(kXchgThreads, 2) k_xchg(const __grid_constant_
     for (int s = 0; s <= n; ++s) {
       if (is_aa && s < n && a.e > 1) {
         trace_start(a.trace, 0, a.max_chunks, s);
+        const unsigned long long t0 = globaltimer();
         copy_items<V, false, false>(aa, list_at(a, kPhaseAA, s), a.cpr_full, c, a.r_aa);
+        pace_list(list_at(a, kPhaseAA, s), t0, a.cp.pace_bpus);
         chunk_done(a.counters + (0 * a.max_chunks + s) * 17, a.r_aa, c, [&] {
           trace_end(a.trace, 0, a.max_chunks, s);
           for (int x = 0; x < a.e; ++x)

@@ -203,6 +203,10 @@ class MoeLayer:
     def backward(self, level: int = O1, n: int = 1, stream=None) -> None:
         check(self.lib.moe_ctx_backward(self._ctx, level, n, _stream_ptr(stream)))
 
+    def set_link_rate(self, gbps: float) -> None:
+        """Emulated inter-node link for the cross-node legs (GB/s per card; 0: off)."""
+        check(self.lib.moe_ctx_set_link_rate(self._ctx, float(gbps)))
+
     def set_wire(self, wire: int) -> None:
         """Cross-node dispatch payload format: _lib.WIRE_BF16 (exact) or _lib.WIRE_FP8."""
         check(self.lib.moe_ctx_set_wire(self._ctx, wire))

@@ -470,3 +470,25 @@ def test_routing_checks_pass_and_catch_corruption(cuda, e, t, E, k, level, n, la
         layer.sync()
     finally:
         layer.close()
+
+
+@pytest.mark.parametrize("level,n", [(BASELINE, 1), (O2, 2)])
+def test_link_rate_pacing_changes_timing_not_results(cuda, level, n):
+    """moe_ctx_set_link_rate only delays the cross-node legs: same rows, same output."""
+    e, t, E, k, T, h = 2, 2, 8, 2, 256, 256
+    x, logits = _inputs(e, T, h, E, torch.bfloat16, 17)
+    outs = []
+    for rate in (0.0, 20.0):
+        layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, max_chunks=4)
+        try:
+            layer.set_link_rate(rate)
+            for cd in layer.cards:
+                cd.x.copy_(x[cd.node])
+                cd.logits.copy_(logits[cd.node])
+            layer.forward(level, n)
+            layer.sync()
+            outs.append([(cd.recv[:layer.recv_rows(cd.card)].clone(), cd.out.clone()) for cd in layer.cards])
+        finally:
+            layer.close()
+    for (r0, o0), (r1, o1) in zip(*outs):
+        assert torch.equal(r0, r1) and torch.equal(o0, o1)
