@@ -376,9 +376,9 @@ moe_status moe_ctx_backward(moe_ctx* ctx, int level, int32_t n_chunks, void* str
  * on one NVSwitch box): every cross-node leg — the dispatch AllToAll and the
  * combine's reverse AllToAll, naive or deduplicated — completes no sooner
  * than its bytes / gbps (GB/s per card), while the intra-node AllGather and
- * local copies run at NVLink / HBM speed.  0 = off.  Applies to the
- * persistent exchange kernels and the per-leg copy launches (the token-side
- * per-leg AllToAll of moe_ctx_set_persistent(0) is not paced). */
+ * local copies run at NVLink / HBM speed.  0 = off.  Applies to every
+ * exchange path (persistent kernels and per-leg launches); with the fp8 wire
+ * a leg is paced on its fp8 bytes + scales. */
 moe_status moe_ctx_set_link_rate(moe_ctx* ctx, double gbps);
 /* Dispatch wire format of the cross-node (AllToAll) legs (SURVEY.md §8(f)
  * item 3).  MOE_WIRE_BF16 (default): rows move bit-exactly.  MOE_WIRE_FP8:

@@ -42,6 +42,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
   const int64_t n_items = (a.tok_end - a.tok_begin) * pieces;
   const int64_t warps = int64_t(gridDim.x) * (kTokThreads / 32);
   const uint64_t pol = l2_evict_first_policy();  // x is read once: keep L2 for the stored rows
+  const unsigned long long t0 = globaltimer();
   for (int64_t it = int64_t(blockIdx.x) * (kTokThreads / 32) + (threadIdx.x >> 5); it < n_items; it += warps) {
     const int64_t i = a.tok_begin + it / pieces;
     const int64_t v0 = (it % pieces) * kPieceVec;
@@ -128,6 +129,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
       }
     }
   }
+  if (a.pace_list) pace_list(a.pace_list, t0, a.pace_bpus, a.fp8 != 0);
   cta_signal(a.sig);
 }
 

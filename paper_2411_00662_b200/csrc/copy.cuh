@@ -228,12 +228,13 @@ __device__ __forceinline__ void chunk_done(unsigned int* counter, int role_ctas,
 // until then — every CTA of the leg waits out the whole list's time from its
 // own start t0, so the leg (and the flag it releases) lands at the emulated
 // rate however fast NVLink moved it.
-__device__ __forceinline__ void pace_list(const SegList* L, unsigned long long t0, uint32_t bpus) {
+__device__ __forceinline__ void pace_list(const SegList* L, unsigned long long t0, uint32_t bpus, bool fp8 = false) {
   if (!bpus) return;
   __syncthreads();
   if (threadIdx.x == 0) {
     int64_t bytes = 0;
-    for (int i = 0; i < L->nseg; ++i) bytes += int64_t(L->segs[i].rows) * L->segs[i].width;
+    for (int i = 0; i < L->nseg; ++i)  // fp8 wire: one byte per bf16 element + one fp32 scale per 128
+      bytes += int64_t(L->segs[i].rows) * (fp8 ? L->segs[i].width / 2 + L->segs[i].width / 64 : L->segs[i].width);
     const unsigned long long until = t0 + (unsigned long long)(bytes * 1000 / int64_t(bpus));
     while (globaltimer() < until) __nanosleep(256);
   }

@@ -803,6 +803,10 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
       t.dst_scale[q] = c->peer[q].wscale;
     }
     t.fp8 = c->wire == MOE_WIRE_FP8 ? 1 : 0;
+    if (c->pace_bpus && d.e > 1) {  // the cross-node legs of this chunk set the pace
+      t.pace_list = list_of(c, cd, kPhaseAA, j);
+      t.pace_bpus = c->pace_bpus;
+    }
     t.node = cd.node;
     t.t = d.t;
     t.blocks_per_row = int(std::max<int64_t>(1, d.hidden / 128));

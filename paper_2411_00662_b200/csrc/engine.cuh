@@ -118,6 +118,9 @@ struct TokArgs {
   int32_t fp8, node, t, blocks_per_row;
   char* dst_pre[kMaxCards];
   float* dst_scale[kMaxCards];
+  // emulated inter-node link: the chunk's cross-node list (kPhaseAA) paces the kernel's release
+  const SegList* pace_list;
+  uint32_t pace_bpus;
   SignalList sig;
   int32_t* err;
 };
