@@ -58,7 +58,14 @@ def _check(ranks, e, t, E, runs, elem=2):
             fin, stg = nodes.dispatch_monolithic(), None
         else:
             fin, stg = nodes.dispatch_chunked(level, n, elem)
-        want_out, _ = nodes.combine(oracle.BF16 if elem == 2 else oracle.F32, fin, probs)
+        dt = oracle.BF16 if elem == 2 else oracle.F32
+        want_out, _ = nodes.combine(dt, fin, probs)
+        # per-element bound (north_star: 1e-2 bf16 / 1e-5 fp32 relative) with the k-term sum's
+        # conditioning: |got - want| <= rtol |want| + 8 * 2^-23 * sum_s p_s |y_s|
+        u = np.uint16 if elem == 2 else np.uint32
+        sign = u(0x7fff) if elem == 2 else u(0x7fffffff)
+        mag, _ = nodes.combine(dt, [((r.view(u) & sign).view(np.uint8), tg) for r, tg in fin], probs)
+        rtol = 1e-2 if elem == 2 else 1e-5
         for r in range(e * t):
             node = r // t
             assert np.array_equal(ranks[r][f"recv_{key}"].reshape(fin[node][0].shape), fin[node][0]), (key, r)
@@ -66,8 +73,8 @@ def _check(ranks, e, t, E, runs, elem=2):
             if landing == 1 and stg is not None:
                 assert np.array_equal(ranks[r][f"pre_{key}"].reshape(stg[node][0].shape), stg[node][0]), (key, r)
             w = want_out[node]
-            err = np.abs(ranks[r][f"out_{key}"] - w).max() / np.abs(w).max()
-            assert err < 1e-2, (key, r, err)
+            bad = np.abs(ranks[r][f"out_{key}"] - w) > rtol * np.abs(w) + 8 * 2.0 ** -23 * mag[node] + 1e-300
+            assert not bad.any(), (key, r, int(bad.sum()))
 
 
 def test_two_gpus_ep2(cuda, tmp_path):
