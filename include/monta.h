@@ -387,10 +387,12 @@ moe_status moe_ctx_set_link_rate(moe_ctx* ctx, double gbps);
  * that fp32 scale and
  * stores bytes + scales into the receiver's pre / scale buffers — half the
  * AllToAll bytes; the receiver decodes them into recv before the intra-node
- * AllGather forwards its slice (bf16).  Own-node rows stay bf16.  Lossy by
+ * AllGather forwards its slice (bf16).  The combine's reverse AllToAll uses
+ * the same format (expert outputs -> the source's fp8 landing, decoded per
+ * chunk before the un-permute).  Own-node rows stay bf16.  Lossy by
  * design (one e4m3 rounding, <= 2^-4 relative per element); needs a bf16
  * payload, hidden and hidden/t multiples of 128, top_k <= 16, FINAL landing;
- * runs the per-leg launches.  The combine's return leg stays bf16. */
+ * runs the per-leg launches. */
 #define MOE_WIRE_BF16 0
 #define MOE_WIRE_FP8 1
 moe_status moe_ctx_set_wire(moe_ctx* ctx, int wire);

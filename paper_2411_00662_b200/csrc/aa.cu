@@ -162,7 +162,118 @@ __global__ void __launch_bounds__(256) k_wire_dequant(char* __restrict__ recv, c
   }
 }
 
+// Combine leg, send: warp per (row of the CAA list, pair of 128-element
+// blocks): 16 lanes x 8 bf16 per block, amax over the half-warp, e4m3 bytes
+// + fp32 scale into the source card's cwire / cscale at the same row.
+__global__ void __launch_bounds__(256) k_caa_fp8(const __grid_constant__ CaaFp8Args a) {
+  const int lane = threadIdx.x & 31;
+  const SegList* L = a.list;
+  const unsigned long long t0 = globaltimer();
+  const int64_t total = L->total_rows;
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  for (int64_t q = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); q < total; q += warps) {
+    int lo = 0, hi = L->nseg - 1;  // segment holding list row q
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (L->segs[mid].row_begin <= q) lo = mid;
+      else hi = mid - 1;
+    }
+    const Seg& sg = L->segs[lo];
+    const int64_t i = q - sg.row_begin;
+    const __nv_bfloat16* src =
+        reinterpret_cast<const __nv_bfloat16*>(a.src + (sg.src_row + i) * a.row_bytes + sg.col_off);
+    char* wire = a.dst_wire[sg.dst] + (sg.dst_row + i) * (a.row_bytes / 2) + sg.col_off / 2;
+    float* sc = a.dst_scale[sg.dst] + (sg.dst_row + i) * a.blocks_per_row + sg.col_off / 256;
+    const int nblk = sg.width / 256;  // 128 bf16 per block
+    for (int b0 = 0; b0 < nblk; b0 += 2) {
+      const int blk = b0 + (lane >> 4);
+      const bool in = blk < nblk;
+      const int e0 = blk * 128 + (lane & 15) * 8;
+      float f[8];
+      float amax = 0.f;
+      if (in) {
+        const uint4 raw = *reinterpret_cast<const uint4*>(src + e0);
+        const __nv_bfloat16* hv = reinterpret_cast<const __nv_bfloat16*>(&raw);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          f[j] = __bfloat162float(hv[j]);
+          amax = fmaxf(amax, fabsf(f[j]));
+        }
+      }
+#pragma unroll
+      for (int m = 8; m > 0; m >>= 1) amax = fmaxf(amax, __shfl_xor_sync(0xffffffffu, amax, m));
+      if (in) {
+        const float scale = amax > 0.f ? amax / 448.f : 1.f;
+        uint32_t w[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const __nv_fp8x2_storage_t l2 = __nv_cvt_float2_to_fp8x2(make_float2(f[4 * j] / scale, f[4 * j + 1] / scale),
+                                                                   __NV_SATFINITE, __NV_E4M3);
+          const __nv_fp8x2_storage_t h2 = __nv_cvt_float2_to_fp8x2(
+              make_float2(f[4 * j + 2] / scale, f[4 * j + 3] / scale), __NV_SATFINITE, __NV_E4M3);
+          w[j] = uint32_t(l2) | (uint32_t(h2) << 16);
+        }
+        *reinterpret_cast<uint2*>(wire + e0) = make_uint2(w[0], w[1]);
+        if ((lane & 15) == 0) sc[blk] = scale;
+      }
+    }
+  }
+  pace_list(L, t0, a.pace_bpus, true);
+  cta_signal(a.sig);
+}
+
+// Combine leg, receive: thread per 8 columns of each (token, slot) of the
+// chunk whose expert lives on another node: comb row (bf16) = decode(cwire).
+__global__ void __launch_bounds__(256) k_comb_dequant(char* __restrict__ comb, const char* __restrict__ wire,
+                                                      const float* __restrict__ scales,
+                                                      const int32_t* __restrict__ slot_pos,
+                                                      const int32_t* __restrict__ experts, int64_t tok_begin,
+                                                      int64_t tok_end, int k, int L, int node, int64_t row_bytes,
+                                                      int bpr, int64_t col0, int64_t width) {
+  const int64_t per = width / 8;
+  const int64_t total = (tok_end - tok_begin) * k * per;
+  for (int64_t q = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; q < total; q += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t ps = q / per;  // (token, slot) within the chunk
+    const int64_t qs = tok_begin * k + ps;
+    const int x = experts[qs];
+    if (x < 0 || x / L == node) continue;  // own-node slots are read in place by the un-permute
+    const int64_t r = slot_pos[qs];
+    const int64_t c = col0 + (q - ps * per) * 8;
+    const uint2 b = *reinterpret_cast<const uint2*>(wire + r * (row_bytes / 2) + c);
+    const float scale = scales[r * bpr + c / 128];
+    const uint32_t w[2] = {b.x, b.y};
+    __nv_bfloat162 o[4];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const __half2_raw lo = __nv_cvt_fp8x2_to_halfraw2(__nv_fp8x2_storage_t(w[j] & 0xffffu), __NV_E4M3);
+      const __half2_raw hi = __nv_cvt_fp8x2_to_halfraw2(__nv_fp8x2_storage_t(w[j] >> 16), __NV_E4M3);
+      const float2 fl = __half22float2(__half2(lo)), fh = __half22float2(__half2(hi));
+      o[2 * j] = __floats2bfloat162_rn(fl.x * scale, fl.y * scale);
+      o[2 * j + 1] = __floats2bfloat162_rn(fh.x * scale, fh.y * scale);
+    }
+    *reinterpret_cast<uint4*>(comb + r * row_bytes + c * 2) = *reinterpret_cast<const uint4*>(o);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_caa_fp8(const CaaFp8Args& a, int grid, cudaStream_t s) {
+  k_caa_fp8<<<grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_comb_dequant(char* comb, const char* wire, const float* scales, const int32_t* slot_pos,
+                                const int32_t* experts, int64_t tok_begin, int64_t tok_end, int k, int L, int node,
+                                int64_t row_bytes, int blocks_per_row, int64_t col0, int64_t width, cudaStream_t s) {
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t work = (tok_end - tok_begin) * k * (width / 8);
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, int64_t(sms) * 8)));
+  k_comb_dequant<<<grid, 256, 0, s>>>(comb, wire, scales, slot_pos, experts, tok_begin, tok_end, k, L, node,
+                                      row_bytes, blocks_per_row, col0, width);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_wire_dequant(char* recv, const int32_t* tags, const int64_t* recv_rows, int64_t cap,
                                 const char* pre, const float* scales, int64_t row_bytes, int blocks_per_row,

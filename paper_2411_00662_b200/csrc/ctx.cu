@@ -46,6 +46,8 @@ struct PeerPtrs {
   void* probs = nullptr;
   void* parts = nullptr;            // [T][k][t] grad-prob partials (layer backward)
   float* wscale = nullptr;          // [recv_cap][h / 128] fp8 wire scales
+  char* cwire = nullptr;            // [R][h] fp8 combine leg rows
+  float* cscale = nullptr;          // [R][h / 128]
 };
 
 // Byte offsets of every buffer inside a card's slab.  Identical on every
@@ -54,7 +56,7 @@ struct SlabLayout {
   size_t x, logits, token_ids, experts, probs, perm_src, expert_of, slot_pos, counts, offsets;
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
   size_t lists, local_delta, recv_rows, recv_offs, tune, prow, rowpos, rowslot, dot, parts, gprobs, glogits, ones,
-      wscale, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
+      wscale, cwire, cscale, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
       ready, xchg_counters, xchg_flags, xtrace, aa_table, total;
 };
 
@@ -204,6 +206,8 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.glogits = take(size_t(T) * E * c->lb);
   s.ones = take(size_t(T) * k * c->lb);
   s.wscale = take(size_t(c->recv_cap) * std::max<int64_t>(1, h / 128) * 4);  // fp8 wire scales
+  s.cwire = take(size_t(c->R) * size_t(h));                              // fp8 combine leg: e4m3 rows
+  s.cscale = take(size_t(c->R) * std::max<int64_t>(1, h / 128) * 4);     //   and their scales
   s.scratch = take(plan_scratch_ints(d.e, int(E), d.max_chunks) * 4);
   s.epoch = take(8);
   s.front_done = take(16);
@@ -293,6 +297,8 @@ void set_peer(moe_ctx* c, int card, char* slab) {
   p.probs = slab + s.probs;
   p.parts = slab + s.parts;
   p.wscale = reinterpret_cast<float*>(slab + s.wscale);
+  p.cwire = slab + s.cwire;
+  p.cscale = reinterpret_cast<float*>(slab + s.cscale);
 }
 
 inline int card_of(const moe_ctx* c, int node, int rho) { return node * c->d.t + rho; }
@@ -1248,6 +1254,31 @@ moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bo
   const moe_layer_desc& d = c->d;
   if (d.e == 1) return MOE_OK;  // no other node: the un-permute reads every row in place
   const bool dedup = level != MOE_BASELINE && d.t > 1;
+  if (c->wire == MOE_WIRE_FP8) {  // the reverse AllToAll on the fp8 wire too
+    CaaFp8Args f{};
+    f.list = list_of(c, cd, kPhaseCAA, j);
+    f.src = static_cast<const char*>(cd.v.expert_out);
+    f.row_bytes = c->row_bytes;
+    f.blocks_per_row = int(std::max<int64_t>(1, d.hidden / 128));
+    for (int q = 0; q < c->cards; ++q)
+      if (c->peer[q].slab) {
+        f.dst_wire[q] = c->peer[q].cwire;
+        f.dst_scale[q] = c->peer[q].cscale;
+      }
+    f.pace_bpus = c->pace_bpus;
+    f.sig = no_signal();
+    f.sig.epoch_ptr = cd.epoch_dev;
+    f.sig.done = cd.done + kPsCAA * d.max_chunks + j;
+    if (!is_virtual(c))
+      for (int g = 0; g < d.e; ++g)
+        if (g != cd.node) f.sig.flags[f.sig.n++] = flag_at(c, card_of(c, g, cd.rho), sig_chunk(c, kPsCAA, j), cd.id);
+    size_t sl;
+    span_begin(c, MOE_STAGE_CAA, j, s, &sl);
+    MONTA_CUDA(launch_caa_fp8(f, copy_grid(c, concurrent, true), s));
+    span_end(c, sl, s);
+    ++c->launches;
+    return MOE_OK;
+  }
   CopyArgs a{};
   a.list = list_of(c, cd, kPhaseCAA, j);
   a.pace_bpus = c->pace_bpus;
@@ -1317,6 +1348,12 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
   // resident CTAs (2 per SM at 256 threads); the launcher clamps to the item count
   const int grid = concurrent ? c->sms / 2 : c->sms;  // SM budget (the launcher sizes per kernel)
   if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;
+  if (c->wire == MOE_WIRE_FP8 && d.e > 1) {  // decode this chunk's cross-node slots (fp8 combine leg)
+    MONTA_CUDA(launch_comb_dequant(static_cast<char*>(cd.v.comb), c->peer[cd.id].cwire, c->peer[cd.id].cscale,
+                                   cd.v.slot_pos, cd.v.experts, a.tok_begin, a.tok_end, d.top_k, c->L, cd.node,
+                                   c->row_bytes, int(std::max<int64_t>(1, d.hidden / 128)), a.col_begin, a.cols, s));
+    ++c->launches;
+  }
   size_t sl;
   span_begin(c, MOE_STAGE_UNPERMUTE, j, s, &sl);
   bool ok = true;

@@ -125,6 +125,23 @@ struct TokArgs {
   int32_t* err;
 };
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s);
+// fp8 wire, combine leg (aa.cu): the reverse AllToAll of one chunk (CAA
+// segment list) quantised into each source card's cwire / cscale; the
+// source decodes its cross-node slots into comb before the un-permute.
+struct CaaFp8Args {
+  const SegList* list;
+  const char* src;        // expert outputs (bf16 rows, row_bytes apart)
+  int64_t row_bytes;
+  int32_t blocks_per_row;
+  char* dst_wire[kMaxCards];
+  float* dst_scale[kMaxCards];
+  uint32_t pace_bpus;
+  SignalList sig;
+};
+cudaError_t launch_caa_fp8(const CaaFp8Args& a, int grid, cudaStream_t s);
+cudaError_t launch_comb_dequant(char* comb, const char* wire, const float* scales, const int32_t* slot_pos,
+                                const int32_t* experts, int64_t tok_begin, int64_t tok_end, int k, int L, int node,
+                                int64_t row_bytes, int blocks_per_row, int64_t col0, int64_t width, cudaStream_t s);
 // fp8 wire receive side (aa.cu): rows of this card that came from another
 // node with source position in [p0, p1): columns [col0, col0 + width) of
 // recv (bf16) = dequant(pre (e4m3), wscale)

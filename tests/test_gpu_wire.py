@@ -3,7 +3,8 @@
 trip of its source row — per 128-element block, scale = amax / 448 (fp32),
 q = e4m3_rn_satfinite(x / scale), row = bf16(q * scale) — bit for bit (an
 emulation of the wire format in PyTorch); own-node rows stay bit-exact; the
-layer output stays within the combine bound of those rows."""
+layer output (the combine's reverse AllToAll on the same wire: crossed slots
+make a second round trip) stays within the combine bound of those rows."""
 import numpy as np
 import pytest
 import torch
@@ -64,6 +65,9 @@ def test_fp8_wire_rows_and_combine(cuda, e, t, E, k, level, n):
                 assert ((got[~own].float() - xs).abs() <= bound).all()
         layer.combine(level, n)
         layer.sync()
+        # the combine's reverse AllToAll is on the fp8 wire too: a crossed slot's
+        # expert output (here the dispatched row itself) makes a second round trip
+        rt2 = torch.stack([_fp8_roundtrip(rt[gg]) for gg in range(e)])
         for cd in layer.cards:
             ex = torch.from_numpy(experts[cd.node]).long()
             pr = cd.probs.float().cpu()
@@ -71,7 +75,7 @@ def test_fp8_wire_rows_and_combine(cuda, e, t, E, k, level, n):
             ref = torch.zeros(T, h)
             for s in range(k):
                 crossed = (ex[:, s] // L) != cd.node
-                row = torch.where(crossed[:, None], rt[cd.node].float(), x[cd.node].float())
+                row = torch.where(crossed[:, None], rt2[cd.node].float(), x[cd.node].float())
                 ref += pr[:, s:s + 1] * row
             got = cd.out.float().cpu()
             assert ((got - ref).abs() <= 2.0 ** -8 * ref.abs() + 1e-6 * ref.abs().amax()).all(), cd.card
