@@ -197,6 +197,30 @@ moe_status moe_comm_stream_destroy(void* stream);
  * caller's stream order. */
 
 /* ------------------------------------------------------------------------
+ * 1e. NVSwitch multicast (NVLS) for the intra-node AllGather (SURVEY.md §8(f)
+ * item 3; replaces the TP-shard gather of dataplane.hpp:243-256): one
+ * multimem.st reaches every device bound to a multicast object, so a TP rank
+ * sends its slice once instead of t - 1 times.  Multi-process setup: the
+ * group leader creates the object and exports a POSIX fd (the caller passes
+ * it to the other processes, e.g. SCM_RIGHTS over a Unix socket), the others
+ * import it; every process adds its device, then (after a group barrier)
+ * binds: a physical buffer of `bytes` on its device (local_va) bound into the
+ * object, and the object's multicast address (mc_va).  `bytes` must be a
+ * multiple of moe_mc_granularity.
+ * ------------------------------------------------------------------------ */
+typedef struct moe_mc moe_mc;
+moe_status moe_mc_supported(int device, int* supported);
+moe_status moe_mc_granularity(int ndev, size_t bytes, size_t* granularity);
+moe_status moe_mc_create(int ndev, size_t bytes, int* fd_out, moe_mc** out);
+moe_status moe_mc_import(int fd, int ndev, size_t bytes, moe_mc** out);
+moe_status moe_mc_add_device(moe_mc* mc, int device);
+moe_status moe_mc_bind(moe_mc* mc, void** local_va, void** mc_va);
+/* Store `bytes` (16-byte multiple) from src through the multicast address
+ * mc_dst: lands at the same offset in every bound device's buffer. */
+moe_status moe_mc_store(const void* src, void* mc_dst, size_t bytes, void* stream);
+moe_status moe_mc_destroy(moe_mc* mc);
+
+/* ------------------------------------------------------------------------
  * 1c. Expert compute between dispatch and combine (
  * the reference's expert task gated on the dispatch terminals,
  * pipesim.hpp:102 — the reference models it, it computes nothing).

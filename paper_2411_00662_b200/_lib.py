@@ -196,6 +196,14 @@ SIGNATURES = {
     "moe_comm_stream_priority": (C.c_int, [C.c_int, C.c_int, _P]),
     "moe_comm_stream_create": (C.c_int, [C.c_int, _P]),
     "moe_comm_stream_destroy": (C.c_int, [_P]),
+    "moe_mc_supported": (C.c_int, [C.c_int, _P]),
+    "moe_mc_granularity": (C.c_int, [C.c_int, C.c_size_t, _P]),
+    "moe_mc_create": (C.c_int, [C.c_int, C.c_size_t, _P, _P]),
+    "moe_mc_import": (C.c_int, [C.c_int, C.c_int, C.c_size_t, _P]),
+    "moe_mc_add_device": (C.c_int, [_P, C.c_int]),
+    "moe_mc_bind": (C.c_int, [_P, _P, _P]),
+    "moe_mc_store": (C.c_int, [_P, _P, C.c_size_t, _P]),
+    "moe_mc_destroy": (C.c_int, [_P]),
     "moe_grouped_gemm": (C.c_int, [_P, _I64, _I64, _P, _P, _I32, _I64, _I64, _P, _I64, C.c_int, _P]),
     "moe_interleave_w13": (C.c_int, [_P, _P, _I32, _I64, _I64, _P, _P]),
     "moe_expert_ffn": (C.c_int, [_P, _I64, _I64, _P, _P, _P, _I32, _I64, _I64, _P, _P, _I64, _P]),
