@@ -216,8 +216,9 @@ moe_status moe_mc_import(int fd, int ndev, size_t bytes, moe_mc** out);
 moe_status moe_mc_add_device(moe_mc* mc, int device);
 moe_status moe_mc_bind(moe_mc* mc, void** local_va, void** mc_va);
 /* Store `bytes` (16-byte multiple) from src through the multicast address
- * mc_dst: lands at the same offset in every bound device's buffer. */
-moe_status moe_mc_store(const void* src, void* mc_dst, size_t bytes, void* stream);
+ * mc_dst on `grid` CTAs (0 = default): lands at the same offset in every
+ * bound device's buffer, the storing device's own included. */
+moe_status moe_mc_store(const void* src, void* mc_dst, size_t bytes, int32_t grid, void* stream);
 moe_status moe_mc_destroy(moe_mc* mc);
 
 /* ------------------------------------------------------------------------

@@ -202,7 +202,7 @@ SIGNATURES = {
     "moe_mc_import": (C.c_int, [C.c_int, C.c_int, C.c_size_t, _P]),
     "moe_mc_add_device": (C.c_int, [_P, C.c_int]),
     "moe_mc_bind": (C.c_int, [_P, _P, _P]),
-    "moe_mc_store": (C.c_int, [_P, _P, C.c_size_t, _P]),
+    "moe_mc_store": (C.c_int, [_P, _P, C.c_size_t, C.c_int32, _P]),
     "moe_mc_destroy": (C.c_int, [_P]),
     "moe_grouped_gemm": (C.c_int, [_P, _I64, _I64, _P, _P, _I32, _I64, _I64, _P, _I64, C.c_int, _P]),
     "moe_interleave_w13": (C.c_int, [_P, _P, _I32, _I64, _I64, _P, _P]),

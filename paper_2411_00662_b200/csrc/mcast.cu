@@ -12,7 +12,8 @@
 //   all:     moe_mc_bind -> this device's physical buffer (unicast VA) and the
 //            multicast VA; a store through the multicast VA lands in every
 //            device's buffer at the same offset.
-// Driver entry points are resolved at run time (no libcuda link).
+// Driver entry points are resolved at run time (no libcuda link), at the
+// runtime's own version: the multicast API appeared in 12.1.
 #include <cuda.h>
 
 #include <mutex>
@@ -61,7 +62,7 @@ const Drv& drv() {
     auto get = [](const char* name, auto& fn) {
       void* p = nullptr;
       cudaDriverEntryPointQueryResult q{};
-      if (cudaGetDriverEntryPointByVersion(name, &p, 12000, cudaEnableDefault, &q) == cudaSuccess &&
+      if (cudaGetDriverEntryPointByVersion(name, &p, CUDART_VERSION, cudaEnableDefault, &q) == cudaSuccess &&
           q == cudaDriverEntryPointSuccess)
         fn = reinterpret_cast<std::remove_reference_t<decltype(fn)>>(p);
       return p != nullptr;
@@ -127,8 +128,9 @@ extern "C" moe_status moe_mc_supported(int device, int* supported) {
   *supported = 0;
   int v = 0;
   cudaFree(nullptr);
-  if (drv().ok && drv().devAttr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, CUdevice(device)) == CUDA_SUCCESS && v)
-    *supported = 1;
+  if (!drv().ok) return fail(MOE_ERR_UNSUPPORTED, "multicast driver entry points unavailable");
+  MONTA_CU(drv().devAttr(&v, CU_DEVICE_ATTRIBUTE_MULTICAST_SUPPORTED, CUdevice(device)), "cuDeviceGetAttribute");
+  *supported = v ? 1 : 0;
   return MOE_OK;
 }
 
@@ -222,7 +224,7 @@ extern "C" moe_status moe_mc_bind(moe_mc* m, void** local_va, void** mc_va) {
   return MOE_OK;
 }
 
-extern "C" moe_status moe_mc_store(const void* src, void* mc_dst, size_t bytes, void* stream) {
+extern "C" moe_status moe_mc_store(const void* src, void* mc_dst, size_t bytes, int32_t grid_req, void* stream) {
   if (!src || !mc_dst || bytes % 16 || (reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(mc_dst)) % 16)
     return fail(MOE_ERR_INVALID_ARGUMENT, "mc_store: 16-byte aligned buffers and sizes only");
   if (bytes == 0) return MOE_OK;
@@ -230,7 +232,8 @@ extern "C" moe_status moe_mc_store(const void* src, void* mc_dst, size_t bytes, 
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int64_t nvec = int64_t(bytes / 16);
-  const int grid = int(std::min<int64_t>((nvec + 255) / 256, int64_t(sms) * 4));
+  const int64_t cap = grid_req > 0 ? int64_t(grid_req) : int64_t(sms) * 4;
+  const int grid = int(std::max<int64_t>(1, std::min<int64_t>((nvec + 255) / 256, cap)));
   k_mc_store<<<grid, 256, 0, static_cast<cudaStream_t>(stream)>>>(static_cast<const uint4*>(src),
                                                                   static_cast<uint4*>(mc_dst), nvec);
   MONTA_CHECK_LAUNCH("mc_store launch");

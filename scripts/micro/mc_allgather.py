@@ -28,6 +28,9 @@ from paper_2411_00662_b200 import _lib  # noqa: E402
 from paper_2411_00662_b200.layer import MoeLayer, device_view  # noqa: E402
 
 
+GRIDS = (8, 16, 32, 64, 148, 296, 592)
+
+
 def share_fd(rank, world, fd, tag):
     """Leader's fd -> every rank (SCM_RIGHTS over an abstract Unix socket)."""
     name = f"\0monta_mc_{tag}"
@@ -65,7 +68,7 @@ def main():
         if rank == 0:
             print(json.dumps({"multicast": "unsupported on this device"}))
         return
-    max_part = 256 << 20
+    max_part = int(os.environ.get("MC_MAX_MIB", "64")) << 20
     gran = C.c_size_t()
     _lib.check(lib.moe_mc_granularity(world, max_part * world, C.byref(gran)))
     total = ((max_part * world + gran.value - 1) // gran.value) * gran.value
@@ -84,7 +87,7 @@ def main():
     buf = device_view(uc.value, (total,), torch.uint8, local)
     # the unicast baseline: the library's NVLink store kernel, one "node" of `world` TP cards
     row = 16384
-    layer = MoeLayer(1, world, world, 1, max_part // row, row // 2, dtype=torch.bfloat16, max_chunks=1, device=local,
+    layer = MoeLayer(1, world, world, 1, world * max_part // row, row // 2, dtype=torch.bfloat16, max_chunks=1, device=local,
                      rank=rank, world_size=world)
     layer.connect()
     stream = torch.cuda.current_stream()
@@ -116,20 +119,22 @@ def main():
         dst_mc = C.c_void_p(mcva.value + rank * v)
         buf[: world * v].zero_()
         dist.barrier()
-        _lib.check(lib.moe_mc_store(C.c_void_p(src.data_ptr()), dst_mc, v, C.c_void_p(stream.cuda_stream)))
+        _lib.check(lib.moe_mc_store(C.c_void_p(src.data_ptr()), dst_mc, v, 0, C.c_void_p(stream.cuda_stream)))
         torch.cuda.synchronize()
         dist.barrier()
         parts = [torch.empty(v, dtype=torch.uint8, device=dev) for _ in range(world)]
         dist.all_gather(parts, src)
         good = all(torch.equal(buf[r * v:(r + 1) * v], parts[r]) for r in range(world))
         all_ok &= good
-        mc_us = timed(lambda: _lib.check(lib.moe_mc_store(C.c_void_p(src.data_ptr()), dst_mc, v,
-                                                          C.c_void_p(stream.cuda_stream))))
+        mct = {g: timed(lambda g=g: _lib.check(lib.moe_mc_store(C.c_void_p(src.data_ptr()), dst_mc, v, g,
+                                                                 C.c_void_p(stream.cuda_stream))))
+              for g in GRIDS}
         per = [0] * world
         for c in range(world):
             if c != rank:
                 per[c] = max(1, v // row)
-        uc_us = timed(lambda: layer.xfer(per, row, 0, stream))
+        uc = {g: timed(lambda g=g: layer.xfer(per, row, g, stream)) for g in GRIDS}
+        mc_us, uc_us = min(mct.values()), min(uc.values())
         full = torch.empty(v * world, dtype=torch.uint8, device=dev)
         nccl_us = timed(lambda: dist.all_gather_into_tensor(full, src))
         if rank == 0:
@@ -138,7 +143,9 @@ def main():
                               "nccl_us": round(nccl_us, 2),
                               "multicast_egress_gbs": round(v / mc_us / 1e3, 1),
                               "delivered_gbs_multicast": round((world - 1) * v / mc_us / 1e3, 1),
-                              "delivered_gbs_unicast": round((world - 1) * v / uc_us / 1e3, 1)}), flush=True)
+                              "delivered_gbs_unicast": round((world - 1) * v / uc_us / 1e3, 1),
+                              "multicast_us_by_ctas": {g: round(x, 2) for g, x in mct.items()},
+                              "unicast_us_by_ctas": {g: round(x, 2) for g, x in uc.items()}}), flush=True)
         v *= 4
     layer.close()
     dist.barrier()

@@ -6,6 +6,7 @@ received rows and tags must equal the oracle's bit for bit, for the naive
 (Baseline) exchange and the TP-deduplicated O1/O2/O3 pipeline with both
 landing modes, across repeated steps (epoch flags, buffer reuse); combined
 outputs within 1e-2 relative (bf16)."""
+import json
 import os
 import socket
 import subprocess
@@ -200,3 +201,20 @@ def test_fp8_wire_multiprocess(cuda, e, t, runs):
            "--groups", str(e), "--tp", str(t), "--runs", runs]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=300)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_nvls_multicast_allgather(cuda, world):
+    """moe_mc_*: every rank's slice stored once through the multicast VA lands
+    bit for bit in every rank's buffer (checked against NCCL all_gather)."""
+    if torch.cuda.device_count() < world:
+        pytest.skip(f"needs {world} GPUs, have {torch.cuda.device_count()}")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
+           "--master-addr=127.0.0.1", f"--master-port={_port()}",
+           os.path.join(ROOT, "scripts", "micro", "mc_allgather.py")]
+    res = subprocess.run(cmd, capture_output=True, text=True, timeout=300, env={**os.environ, "MC_MAX_MIB": "4"})
+    assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
+    lines = [json.loads(l) for l in res.stdout.splitlines() if l.startswith("{")]
+    if lines and "multicast" in lines[0]:
+        pytest.skip(lines[0]["multicast"])
+    assert len(lines) == 2 and all(l["correct"] for l in lines), res.stdout
