@@ -762,7 +762,7 @@ def main():
         ach = kern.get("unpermute_combine", 0.0)
         traffic_alg = unp_bytes
         dom_name = ("unpermute_combine (k_unpermute_k2<bf16,bf16,f32>)" if ELEM == 2 and k <= 2
-                    else "unpermute_combine (k_unpermute)")
+                    else "unpermute_combine (k_unpermute_rows)" if ELEM == 2 else "unpermute_combine (k_unpermute)")
     # DRAM bytes of the same kernel from an ncu --set full capture of this
     # workload (profiles/ncu_traffic.json, keyed by workload then stage); null
     # when that workload has no capture or the kernel differs from the one timed

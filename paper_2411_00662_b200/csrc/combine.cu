@@ -249,6 +249,98 @@ __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_co
   cta_signal(a.sig);
 }
 
+// Un-permute for any k with 16-bit rows: CTA per token (the layout of the
+// dispatch backward, backward.cu, which runs the same k-row gather-sum at
+// 0.95 of the HBM peak).  The CTA is sized so every round of U 16-byte
+// vectors per thread covers the row (DeepSeek h = 5120: 160 threads x 2 x 2
+// rounds);
+// threads 0..k-1 resolve the token's slot rows and weights into shared
+// memory (double-buffered: one barrier per token); SG slots' loads are in
+// flight before their multiply-adds, which stay in ascending slot order
+// (bit-identical to k_unpermute).  Many small CTAs per SM keep the gather
+// saturated without a per-warp index pipeline.
+constexpr int kRowThreads = 256;
+template <class TIn, class TOut, class TProb, int U, int SG, int MinB>
+__global__ void __launch_bounds__(kRowThreads, MinB) k_unpermute_rows(const __grid_constant__ UnpermArgs a) {
+  constexpr int N = 16 / sizeof(TIn);
+  __shared__ const char* s_row[2][kMaxK];
+  __shared__ float s_p[2][kMaxK];
+  __shared__ int s_delta[kDeltaSmem];
+  if (!cta_wait(a.wait, a.err)) return;
+  const int nloc = a.local_y ? a.local_hi - a.local_lo : 0;
+  const bool delta_smem = nloc <= kDeltaSmem;
+  if (delta_smem)
+    for (int l = threadIdx.x; l < nloc; l += blockDim.x) s_delta[l] = __ldg(a.local_delta + a.local_lo + l);
+  __syncthreads();  // threads 0..k-1 read the deltas before the token loop's barrier
+  const TProb* probs = static_cast<const TProb*>(a.probs);
+  const int k = a.k;
+  const int nvec = int(a.cols / N);
+  const uint64_t pol = l2_evict_first_policy();
+  int buf = 0;
+  for (int64_t i = a.tok_begin + blockIdx.x; i < a.tok_end; i += gridDim.x, buf ^= 1) {
+    if (threadIdx.x < k) {
+      const int64_t q = i * k + threadIdx.x;
+      const int pos = __ldg(a.slot_pos + q);
+      const int x = __ldg(a.experts + q);
+      const char* row = nullptr;
+      if (pos >= 0) {
+        if (nloc && x >= a.local_lo && x < a.local_hi) {
+          const int d = delta_smem ? s_delta[x - a.local_lo] : __ldg(a.local_delta + x);
+          row = a.local_y + (int64_t(pos) + d) * a.y_stride;
+        } else {
+          row = a.comb + int64_t(pos) * a.y_stride;
+        }
+        row += a.col_begin * int64_t(sizeof(TIn));
+      }
+      s_row[buf][threadIdx.x] = row;
+      s_p[buf][threadIdx.x] = float(__ldg(probs + q));
+    }
+    __syncthreads();
+    for (int c0 = threadIdx.x; c0 < nvec; c0 += blockDim.x * U) {
+      float acc[U][N];
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int j = 0; j < N; ++j) acc[u][j] = 0.f;
+      for (int s0 = 0; s0 < k; s0 += SG) {
+        int4 v[SG][U];
+        const char* rows[SG];
+#pragma unroll
+        for (int g = 0; g < SG; ++g) {
+          rows[g] = s0 + g < k ? s_row[buf][s0 + g] : nullptr;
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int c = c0 + u * int(blockDim.x);
+            if (rows[g] && c < nvec) v[g][u] = ld_stream_ef(reinterpret_cast<const int4*>(rows[g]) + c, pol);
+          }
+        }
+#pragma unroll
+        for (int g = 0; g < SG; ++g) {
+          if (!rows[g]) continue;
+          const float ps = s_p[buf][s0 + g];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const Pack<TIn, N> y = *reinterpret_cast<const Pack<TIn, N>*>(&v[g][u]);
+#pragma unroll
+            for (int j = 0; j < N; ++j) acc[u][j] = madd<float>(acc[u][j], ps, widen<TIn, float>(y.v[j]));
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + u * int(blockDim.x);
+        if (c >= nvec) continue;
+        Pack<TOut, N> o;
+#pragma unroll
+        for (int j = 0; j < N; ++j) o.v[j] = narrow<float, TOut>(acc[u][j]);
+        const int64_t off = i * a.out_stride + (a.col_begin + int64_t(c) * N) * int64_t(sizeof(TOut));
+        for (int d = 0; d < a.n_out; ++d) *reinterpret_cast<Pack<TOut, N>*>(a.out[d] + off) = o;
+      }
+    }
+  }
+  cta_signal(a.sig);
+}
+
 // MinB: resident CTAs per SM the register budget must allow (occupancy, not
 // per-warp depth, is what keeps enough gather loads in flight on B200:
 // scripts/micro/gather_bench.cu measured 5.7 TB/s at 16 warps/SM vs 6.3 TB/s
@@ -373,6 +465,38 @@ cudaError_t launch_combine_xchg(const CombArgs& a, int y_dtype, int probs_dtype,
   return cudaErrorNotSupported;
 }
 
+// A/B switch for the k > 2 un-permute (read once): MONTA_UNPERM_ROWS=0
+// selects the warp-per-item kernel.
+static bool unperm_rows_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MONTA_UNPERM_ROWS");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+// any k, 16-bit rows: CTA per token, sized so each round of U = 2 vectors
+// per thread covers the row in the fewest rounds of <= 160 threads, two
+// slots' loads in flight, <= 48 registers (8 CTAs of 160 threads per SM).
+// Measured on the N=1 DeepSeek layer (scripts/gpu_unperm_ab.sh): 100.8 us
+// against 105.6 (U = 4, one slot, 64 registers), 106.3 (U = 2, one slot),
+// 101.6 (U = 2, three slots) and 113.8 for the warp-per-item k_unpermute;
+// 16 CTAs per SM of grid (8: same, one token per CTA: 104.2).
+template <class TIn, class TAcc, class TOut, class TProb>
+static void launch_rows(const UnpermArgs& a, int grid, cudaStream_t s) {
+  if constexpr (sizeof(TIn) == 2 && sizeof(TAcc) == 4) {
+    const int64_t nvec = a.cols / 8;
+    auto block_of = [&](int U) {
+      const int64_t rounds = (nvec + int64_t(160) * U - 1) / (int64_t(160) * U);
+      const int b = int(((nvec + U * rounds - 1) / (U * rounds) + 31) / 32 * 32);
+      return std::min(std::max(b, 32), kRowThreads);
+    };
+    const int64_t toks = a.tok_end - a.tok_begin;
+    const int rows_grid = int(std::max<int64_t>(1, std::min<int64_t>(toks, int64_t(grid) * 16)));
+    k_unpermute_rows<TIn, TOut, TProb, 2, 2, 5><<<rows_grid, block_of(2), 0, s>>>(a);
+  }
+}
+
 template <class TIn, class TAcc, class TOut, class TProb>
 static cudaError_t launch_n(const UnpermArgs& a, int grid, cudaStream_t s) {
   // Vector of N elements: as wide as 16 bytes of input allows and the column
@@ -403,6 +527,8 @@ static cudaError_t launch_n(const UnpermArgs& a, int grid, cudaStream_t s) {
       k_unpermute_k2<TIn, TOut, TProb, 8, 3, 1><<<g(8, 8, 3), kThreads, 0, s>>>(a);
     else
       k_unpermute_k2<TIn, TOut, TProb, 4, 3><<<g(8, 4, 3), kThreads, 0, s>>>(a);
+  } else if (N16 == 8 && sizeof(TAcc) == 4 && fits(8) && unperm_rows_enabled()) {
+    launch_rows<TIn, TAcc, TOut, TProb>(a, grid, s);
   } else if (N16 >= 8 && fits(8)) {
     k_unpermute<TIn, TAcc, TOut, TProb, 8><<<g(8, unperm_uv<8>()), kThreads, 0, s>>>(a);
   } else if (N16 >= 4 && fits(4)) {
