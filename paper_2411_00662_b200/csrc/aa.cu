@@ -21,6 +21,7 @@
 #include <cuda_fp8.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "copy.cuh"
 
@@ -130,6 +131,109 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
     }
   }
   if (a.pace_list) pace_list(a.pace_list, t0, a.pace_bpus, a.fp8 != 0);
+  cta_signal(a.sig);
+}
+
+// TMA form of the same permute, for destinations in this GPU's memory (a
+// lone card or virtual cards; bf16 wire, no link pacing): one warp per CTA
+// streams its tokens through a ring of S whole-row shared-memory stages.
+// Lane 0 issues the row load (cp.async.bulk global -> shared, completing on
+// the stage's mbarrier, L2 evict-first: x is read once); once it lands, lane
+// s < k issues slot s's row store (cp.async.bulk shared -> global, the
+// destination's column window) and writes its tag.  Every lane commits one
+// bulk group per token, so "at most D groups pending" (wait_group.read D)
+// frees the stage of token m - D for token m - D + S: S - D loads and D
+// tokens' stores stay in flight with no registers holding row data.
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__global__ void __launch_bounds__(32) k_aa_bulk(const __grid_constant__ TokArgs a, int stages, int depth) {
+  extern __shared__ __align__(128) char smem[];
+  const int lane = threadIdx.x;
+  const int E = a.E, k = a.k;
+  const uint32_t rb = uint32_t(a.row_bytes);
+  const uint32_t sb = (rb + 127u) & ~127u;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + size_t(stages) * sb);
+  const int64_t first = a.tok_begin + blockIdx.x;
+  const int64_t ntok = first < a.tok_end ? (a.tok_end - first + gridDim.x - 1) / gridDim.x : 0;
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  if (lane == 0) {
+    for (int q = 0; q < stages; ++q)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_addr(bars + q)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncwarp();
+  auto load = [&](int64_t m) {  // lane 0: token m of this CTA into stage m % S
+    const int q = int(m % stages);
+    const uint32_t bar = smem_addr(bars + q);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(rb) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::
+            "r"(smem_addr(smem + size_t(q) * sb)),
+        "l"(a.x + (first + m * gridDim.x) * a.row_bytes), "r"(rb), "r"(bar), "l"(pol)
+        : "memory");
+  };
+  if (lane == 0)
+    for (int64_t m = 0; m < ntok && m < stages; ++m) load(m);
+  for (int64_t m = 0; m < ntok; ++m) {
+    const int64_t i = first + m * gridDim.x;
+    const int q = int(m % stages);
+    // destination of slot `lane` (index loads overlap the row load)
+    char* dp = nullptr;
+    uint32_t off = 0, len = 0;
+    if (lane < k) {
+      const int64_t qi = i * k + lane;
+      const int x = __ldg(a.experts + qi);
+      if (x >= 0 && x < E) {
+        const int p = __ldg(a.slot_pos + qi);
+        const int card = __ldg(a.table + x);
+        const int base = a.staged ? __ldg(a.table + (4 + a.j) * E + x) : __ldg(a.table + E + x);
+        const int64_t row = int64_t(base) + p;
+        off = uint32_t(__ldg(a.table + 2 * E + x));
+        len = uint32_t(__ldg(a.table + 3 * E + x));
+        dp = a.dst[card] + row * a.dst_stride;
+        if (a.dst_tags[card])
+          *reinterpret_cast<int4*>(a.dst_tags[card] + 4 * row) = make_int4(__ldg(a.token_ids + i), a.source_card,
+                                                                           int(i), x);
+      }
+    }
+    {  // wait for the row (every lane: the stores below are per lane)
+      const uint32_t bar = smem_addr(bars + q), parity = uint32_t((m / stages) & 1);
+      uint32_t done;
+      do {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+      } while (!done);
+    }
+    if (dp && len)
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dp + off),
+                   "r"(smem_addr(smem + size_t(q) * sb + off)), "r"(len)
+                   : "memory");
+    asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    // stage of token m - D is free once every lane's stores of it have read smem
+    const int64_t r = m - depth;
+    if (r >= 0 && r + stages < ntok) {
+      switch (depth) {  // wait_group.read takes an immediate
+        case 1: asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); break;
+        case 2: asm volatile("cp.async.bulk.wait_group.read 2;" ::: "memory"); break;
+        case 4: asm volatile("cp.async.bulk.wait_group.read 4;" ::: "memory"); break;
+        default: asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); break;
+      }
+      __syncwarp();
+      if (lane == 0) load(r + stages);
+    }
+  }
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+  __syncwarp();
   cta_signal(a.sig);
 }
 
@@ -289,8 +393,41 @@ cudaError_t launch_wire_dequant(char* recv, const int32_t* tags, const int64_t* 
   return cudaGetLastError();
 }
 
+// TMA bulk form (k_aa_bulk) when it applies; MONTA_AA_BULK=0 turns it off
+// (A/B), MONTA_AA_STAGES / MONTA_AA_DEPTH / MONTA_AA_CPS tune the ring.
+static int env_int(const char* name, int dflt) {
+  const char* e = std::getenv(name);
+  return e && *e ? std::atoi(e) : dflt;
+}
+
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s) {
   if (a.k > kTokMaxK) return cudaErrorNotSupported;
+  static const int bulk = env_int("MONTA_AA_BULK", 1);
+  const uint32_t sb = uint32_t((a.row_bytes + 127) & ~int64_t(127));
+  if (bulk && a.local_dst && !a.fp8 && !a.pace_list && vec == 16 && a.row_bytes % 16 == 0 &&
+      a.dst_stride % 16 == 0 && reinterpret_cast<uintptr_t>(a.x) % 16 == 0 && sb <= 64 * 1024) {
+    static const int want_stages = env_int("MONTA_AA_STAGES", 8);
+    static const int depth_env = env_int("MONTA_AA_DEPTH", 4);
+    static const int cps_env = env_int("MONTA_AA_CPS", 2);
+    int dev = 0, sms = 148, smem_max = 227 * 1024;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    const int cps = std::max(1, cps_env);
+    const int per_cta = std::min(smem_max, 228 * 1024 / cps - 1024);
+    const int stages = std::max(2, std::min(want_stages, int((per_cta - 256) / int(sb))));
+    const int depth = std::min(depth_env == 1 || depth_env == 2 || depth_env == 4 ? depth_env : 0, stages - 1);
+    const size_t smem = size_t(stages) * sb + size_t(stages) * 8;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_aa_bulk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_max);
+      attr = true;
+    }
+    const int64_t toks = a.tok_end - a.tok_begin;
+    const int g = int(std::max<int64_t>(1, std::min<int64_t>(toks, int64_t(sms) * cps)));
+    k_aa_bulk<<<g, 32, smem, s>>>(a, stages, depth);
+    return cudaGetLastError();
+  }
   switch (vec) {
     case 16: k_aa_token<16><<<grid, kTokThreads, 0, s>>>(a); break;
     case 8: k_aa_token<8><<<grid, kTokThreads, 0, s>>>(a); break;

@@ -823,6 +823,7 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
       for (int x = 0; x < d.e; ++x)
         if (x != cd.node) t.sig.flags[t.sig.n++] = flag_at(c, card_of(c, x, cd.rho), sig_chunk(c, kPsAA, j), cd.id);
     t.err = cd.err;
+    t.local_dst = is_virtual(c) ? 1 : 0;
     // four resident CTAs (32 warps) per SM, at most one item (token x 2 KiB piece) per warp
     const int64_t items = ct * ((c->row_bytes + 2047) / 2048);
     int grid = int(std::min<int64_t>((items + 7) / 8, int64_t(c->sms) * (concurrent ? 2 : 4)));

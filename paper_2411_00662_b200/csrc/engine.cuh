@@ -123,6 +123,9 @@ struct TokArgs {
   uint32_t pace_bpus;
   SignalList sig;
   int32_t* err;
+  // every destination is in this GPU's own memory (a lone card, or virtual
+  // cards on one GPU): the TMA bulk-copy form may run (aa.cu k_aa_bulk)
+  int32_t local_dst;
 };
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s);
 // fp8 wire, combine leg (aa.cu): the reverse AllToAll of one chunk (CAA
