@@ -514,6 +514,8 @@ def main():
         # one: the memset's dirty lines are written back here, outside the
         # events, so the step starts from a cold AND clean L2 (what ncu's
         # --cache-control all gives each kernel)
+        if os.environ.get("MONTA_BENCH_NO_FLUSH") == "1":  # diagnosis only: never for a reported number
+            return
         flush.zero_()
         flush_rd.amax()
     stream = torch.cuda.current_stream()

@@ -425,6 +425,7 @@ cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s)
     }
     const int64_t toks = a.tok_end - a.tok_begin;
     const int g = int(std::max<int64_t>(1, std::min<int64_t>(toks, int64_t(sms) * cps)));
+    apply_carveout(k_aa_bulk);
     k_aa_bulk<<<g, 32, smem, s>>>(a, stages, depth);
     return cudaGetLastError();
   }

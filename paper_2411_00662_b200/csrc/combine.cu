@@ -493,6 +493,7 @@ static void launch_rows(const UnpermArgs& a, int grid, cudaStream_t s) {
     };
     const int64_t toks = a.tok_end - a.tok_begin;
     const int rows_grid = int(std::max<int64_t>(1, std::min<int64_t>(toks, int64_t(grid) * 16)));
+    apply_carveout(k_unpermute_rows<TIn, TOut, TProb, 2, 2, 5>);
     k_unpermute_rows<TIn, TOut, TProb, 2, 2, 5><<<rows_grid, block_of(2), 0, s>>>(a);
   }
 }

@@ -6,9 +6,24 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+
 #include "monta.h"
 
 namespace monta {
+// Diagnosis: MONTA_CARVEOUT=<0..100> sets every data-path kernel's preferred
+// shared-memory carveout (read once; unset leaves the driver's choice).
+inline int carveout_env() {
+  static const int v = [] {
+    const char* e = std::getenv("MONTA_CARVEOUT");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+template <class F> inline void apply_carveout(F* fn) {
+  if (carveout_env() >= 0) cudaFuncSetAttribute(fn, cudaFuncAttributePreferredSharedMemoryCarveout, carveout_env());
+}
+
 
 constexpr int kMaxCards = 64;     // e*t cards per layer context
 constexpr int kWarp = 32;

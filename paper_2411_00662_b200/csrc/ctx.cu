@@ -2151,12 +2151,16 @@ extern "C" int64_t moe_ctx_launch_count(const moe_ctx* c) { return c ? c->launch
 extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint64_t* out20) {
   if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: null ctx");
   c->debug = enable != 0;
-  if (!out20) return MOE_OK;
   MONTA_CUDA(cudaSetDevice(c->device));
+  if (!out20) {
+    for (auto& cd : c->local) MONTA_CUDA(cudaMemset(cd.dbg, 0, 20 * sizeof(uint64_t)));
+    return MOE_OK;
+  }
   for (auto& cd : c->local)
     if (cd.id == card) {
       MONTA_CUDA(cudaDeviceSynchronize());
       MONTA_CUDA(cudaMemcpy(out20, cd.dbg, 160, cudaMemcpyDeviceToHost));
+      MONTA_CUDA(cudaMemset(cd.dbg + 16, 0, 4 * sizeof(uint64_t)));  // the per-launch min/max stamps
       return MOE_OK;
     }
   return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: card %d is not local", card);

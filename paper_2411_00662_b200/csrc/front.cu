@@ -23,6 +23,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <cstdlib>
+
 #include "front.cuh"
 
 namespace monta {
@@ -328,7 +330,12 @@ __global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_co
   int* W = smem + L.exp_ints;
   if (tid == 0) {
     s_epoch = *a.epoch_dev + 1;  // read before this CTA arrives: the bump happens after every arrival
-    if (a.dbg && blockIdx.x == 0) a.dbg[0] = globaltimer();
+    if (a.dbg) {
+      const unsigned long long t = globaltimer();
+      if (blockIdx.x == 0) a.dbg[0] = t;
+      atomicMax(a.dbg + 16, ~t);  // earliest CTA start (complemented)
+      atomicMax(a.dbg + 17, t);   // latest CTA start
+    }
     // the CTA's tiles of gate logits are contiguous: one bulk L2 prefetch up
     // front, so the router's passes over a wide tile (E = 160: four passes)
     // do not each wait for HBM
@@ -480,10 +487,14 @@ __global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_co
       }
       __syncthreads();
     }
-    if (a.dbg && blockIdx.x == 0 && tid == 0) a.dbg[7] = globaltimer();
+    if (a.dbg && tid == 0) {
+      if (blockIdx.x == 0) a.dbg[7] = globaltimer();
+      atomicMax(a.dbg + 18, globaltimer());  // latest CTA end
+    }
     return;
   }
   control_tail(a, s_plan, W, s_epoch);
+  if (a.dbg && tid == 0) atomicMax(a.dbg + 19, globaltimer());  // control CTA end
 }
 
 size_t front_smem_bytes(const FrontArgs* a, int tile_ctas) {
@@ -528,8 +539,16 @@ moe_status launch_t(const FrontArgs* a, cudaStream_t s, bool configure) {
   const int grid = tile_ctas + 1;
   const size_t smem = std::min(smem_max, front_smem_bytes(a, tile_ctas));
   void* args[] = {const_cast<FrontArgs*>(a)};
-  MONTA_CUDA(cudaLaunchCooperativeKernel((const void*)k_front<T, G, PER>, dim3(grid), dim3(front_threads(G, PER)), args, smem,
-                                         s));
+  static const int coop = [] {
+    const char* e = std::getenv("MONTA_FRONT_COOP");
+    return e ? std::atoi(e) : 1;
+  }();
+  apply_carveout(k_front<T, G, PER>);
+  if (coop)
+    MONTA_CUDA(cudaLaunchCooperativeKernel((const void*)k_front<T, G, PER>, dim3(grid), dim3(front_threads(G, PER)),
+                                           args, smem, s));
+  else
+    MONTA_CUDA(cudaLaunchKernel((const void*)k_front<T, G, PER>, dim3(grid), dim3(front_threads(G, PER)), args, smem, s));
   return MOE_OK;
 }
 

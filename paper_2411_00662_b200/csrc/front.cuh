@@ -42,6 +42,75 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
     const int x = sub + m * G;
     v[m] = (active && x < E) ? row[x] : neg_inf<T>();
   }
+  if constexpr (sizeof(T) == 4 && G == 32) {
+    // fp32 scores, whole-warp groups (E > 16).  Each entry's order-preserving
+    // 32-bit key is computed once (-0.0 canonicalised to +0.0 first: the
+    // reference compares values, scores[l] > scores[r] at dataplane.hpp:97-98,
+    // for which the two zeros tie and the lower index wins; entries past E get
+    // key 0, below every real score).  The row max is one redux.sync over the
+    // keys (it differs from a float max only in the sign of a zero maximum,
+    // which leaves every exp(v - max) unchanged).  Round s: the lane's best
+    // key (strict > keeps its lower index on ties), the warp's max key, the
+    // lowest expert index holding it (redux.sync max/min), the owner zeroes
+    // that entry and lane s keeps {winner, exp}; the k winners then leave in
+    // ascending expert order (rank by k shuffles) with probs = exp / sum.
+    unsigned u[PER];
+    unsigned lmax = 0u;
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int x = sub + m * G;
+      unsigned b = __float_as_uint(float(v[m]));
+      b = (b == 0x80000000u) ? 0u : b;
+      u[m] = x < E ? ((b & 0x80000000u) ? ~b : (b | 0x80000000u)) : 0u;
+      lmax = u[m] > lmax ? u[m] : lmax;
+    }
+    const unsigned mkey = __reduce_max_sync(0xffffffffu, lmax);
+    const T mx = T(__uint_as_float((mkey & 0x80000000u) ? (mkey & 0x7fffffffu) : ~mkey));
+    T ex[PER];
+    T sum = T(0);
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      ex[m] = dev_exp<T>(v[m] - mx);  // entries past E: v = -inf, exp = 0 (as the masked form)
+      sum += ex[m];
+    }
+#pragma unroll
+    for (int off = G / 2; off > 0; off >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, off, G);
+    int my_w = -1;
+    T my_e = T(0);
+    for (int s = 0; s < k; ++s) {
+      unsigned key = 0u, bm = 0u;
+#pragma unroll
+      for (int m = 0; m < PER; ++m)
+        if (u[m] > key) {
+          key = u[m];
+          bm = unsigned(m);
+        }
+      const unsigned bi = key ? unsigned(sub) + bm * G : 0xffffffffu;
+      const unsigned mk = __reduce_max_sync(0xffffffffu, key);
+      const unsigned wi = __reduce_min_sync(0xffffffffu, key == mk ? bi : 0xffffffffu);  // k <= E: exists
+      const unsigned mw = wi / G, owner = wi % G;
+      T e = T(0);
+#pragma unroll
+      for (int m = 0; m < PER; ++m)
+        if (unsigned(m) == mw) {
+          e = ex[m];
+          if (owner == unsigned(sub)) u[m] = 0u;
+        }
+      e = __shfl_sync(0xffffffffu, e, int(owner));
+      if (lane == s) {
+        my_w = int(wi);
+        my_e = e;
+      }
+    }
+    int slot = 0;
+    for (int s = 0; s < k; ++s) slot += __shfl_sync(0xffffffffu, my_w, s) < my_w ? 1 : 0;
+    if (active && lane < k) {
+      experts[token * k + slot] = my_w;
+      probs[token * k + slot] = my_e / sum;
+      if (s_exp) s_exp[(token - s_base) * k + slot] = my_w;  // the tile's mirror in shared memory
+    }
+    return;
+  }
   T mx = v[0];
 #pragma unroll
   for (int m = 1; m < PER; ++m) mx = v[m] > mx ? v[m] : mx;
