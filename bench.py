@@ -384,6 +384,15 @@ def experts_leg(layer, cd, e, t, E, h, step, timed, steps, local):
         layer.enable_timing(False)
         layer.sync()
         rows = layer.recv_rows(cd.card)
+        seq = None
+        if e > 1:  # the same step with the reverse AllToAll NOT fused into the down-projection
+            layer.set_expert_overlap(False)
+            for _ in range(3):
+                step()
+            layer.sync()
+            tseq, _ = timed(step, steps)
+            seq = tseq * 1e3 / steps
+            layer.set_expert_overlap(True)
     finally:
         layer.bind_experts(cd.card, None)
     ex_us = 1e3 * statistics.median(sum(v) for v in sp)
@@ -395,7 +404,10 @@ def experts_leg(layer, cd, e, t, E, h, step, timed, steps, local):
     except Exception:
         peak, kind = 1800.0, "fallback"
     ach = flops / ex_us / 1e6
-    return {"us_per_layer_with_experts": tot * 1e3 / steps, "experts_us": ex_us, "rows": rows, "ffn": F,
+    return {"us_per_layer_with_experts": tot * 1e3 / steps,
+            "us_per_layer_with_experts_no_overlap": seq,
+            "reverse_alltoall_fused_into_down_proj": e > 1,
+            "experts_us": ex_us, "rows": rows, "ffn": F,
             "local_experts": L, "flops_per_card": flops,
             "roofline": {"bound": "tensor", "kernel": "k_grouped_gemm x2 (SwiGLU gate/up, down)", "achieved": ach,
                          "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "peak_kind": kind},

@@ -341,6 +341,15 @@ moe_status moe_ctx_bind_experts(moe_ctx* ctx, int card, const void* w13, const v
 /* Run the bound experts of every local card on the rows of the last
  * dispatch (waits for every incoming row first).  No-op when none bound. */
 moe_status moe_ctx_experts(moe_ctx* ctx, void* stream);
+/* Bound experts fused with the reverse AllToAll inside moe_ctx_forward
+ * (multi-GPU, bf16 wire, no link pacing): the down-projection GEMM's epilogue
+ * stores every finished tile row both to expert_out and, when the row's
+ * source card sits on another node, straight into that card's landing buffer
+ * over NVLink (the reference's expert task feeding its combine,
+ * pipesim.hpp:102) — the reverse AllToAll overlaps the tensor-core tiles in
+ * one kernel.  enable = 0: experts, then the combine's own AllToAll.
+ * Default on.  Results are identical either way. */
+moe_status moe_ctx_set_expert_overlap(moe_ctx* ctx, int32_t enable);
 
 /* Route every local card (moe_route_topk on its logits). */
 moe_status moe_ctx_route(moe_ctx* ctx, void* stream);

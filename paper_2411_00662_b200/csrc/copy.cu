@@ -58,6 +58,19 @@ __global__ void __launch_bounds__(kCopyThreads)
   }
 }
 
+// rowdst: block per (chunk list, segment), threads over the segment's rows.
+__global__ void __launch_bounds__(256) k_rowdst(const char* __restrict__ lists, size_t list_stride, int nseg_cap,
+                                                const PeerRows comb, int64_t row_bytes, char** __restrict__ rowdst) {
+  const int j = blockIdx.x / nseg_cap, q = blockIdx.x % nseg_cap;
+  const SegList* L = reinterpret_cast<const SegList*>(lists + size_t(j) * list_stride);
+  if (q >= L->nseg) return;
+  const Seg sg = L->segs[q];
+  if (sg.dst < 0) return;
+  char* base = comb.base[sg.dst];
+  for (int i = threadIdx.x; i < sg.rows; i += blockDim.x)
+    rowdst[sg.src_row + i] = base + (sg.dst_row + i) * row_bytes;
+}
+
 __global__ void k_wait(const WaitList w, int32_t* err) { cta_wait(w, err); }
 
 __global__ void k_signal(const SignalList s) {
@@ -104,6 +117,15 @@ cudaError_t launch_gather_rows(const void* src, int64_t src_stride, int64_t col_
     case 2: k_gather_rows<2><<<grid, kCopyThreads, 0, s>>>(sp, src_stride, col_off, width, perm, R, op, out_stride); break;
     default: k_gather_rows<1><<<grid, kCopyThreads, 0, s>>>(sp, src_stride, col_off, width, perm, R, op, out_stride); break;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rowdst(const SegList* lists, size_t list_stride, int n, int nseg_cap, const PeerRows& comb,
+                          int64_t row_bytes, char** rowdst, int64_t cap, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(rowdst, 0, size_t(cap) * sizeof(char*), s);
+  if (e != cudaSuccess || n <= 0) return e;
+  k_rowdst<<<n * nseg_cap, 256, 0, s>>>(reinterpret_cast<const char*>(lists), list_stride, nseg_cap, comb, row_bytes,
+                                        rowdst);
   return cudaGetLastError();
 }
 

@@ -64,10 +64,12 @@ struct CopyView {
   uint64_t dst_mask;
   char* const* dst;
   int32_t* const* dst_tags;
+  const int32_t* bounds;  // source-row filter (null: none)
+  int32_t b_lo, b_hi;
 };
 __device__ __forceinline__ CopyView view_of(const CopyArgs& a) {
   return CopyView{a.src, a.src_stride, a.gather, a.src_tags, a.token_ids, a.source_card, a.synth_tags,
-                  a.dst_stride, a.dst_mask, a.dst, a.dst_tags};
+                  a.dst_stride, a.dst_mask, a.dst, a.dst_tags, a.bounds, a.b_lo, a.b_hi};
 }
 
 // kStage: stage the segment starts in shared memory (one CTA barrier).  The
@@ -97,6 +99,8 @@ __device__ __forceinline__ void copy_items(const CopyView& a, const SegList* L, 
   // loads: 8 for the fine-grained 160-expert lists).
   int cur = 0;
   auto beg = [&](int i) -> int64_t { return cached ? sbeg[i] : L->segs[i].row_begin; };
+  const int64_t flo = a.bounds ? int64_t(__ldg(a.bounds + a.b_lo)) : 0;
+  const int64_t fhi = a.bounds ? int64_t(__ldg(a.bounds + a.b_hi)) : INT64_MAX;
   for (int64_t item = cta * wpc + (threadIdx.x >> 5); item < total; item += ctas * wpc) {
     const int64_t r = item / cpr;
     const int64_t chunk = item - r * cpr;
@@ -114,6 +118,7 @@ __device__ __forceinline__ void copy_items(const CopyView& a, const SegList* L, 
     const Seg sg = L->segs[lo];
     const int64_t off = chunk * kItemBytes;
     if (off >= sg.width) continue;
+    if (sg.src_row < flo || sg.src_row >= fhi) continue;  // another expert group's segment
     const int64_t bytes = sg.width - off < kItemBytes ? sg.width - off : kItemBytes;
     const int64_t i = r - sg.row_begin;
     const int64_t src_row = a.gather ? int64_t(__ldg(a.gather + sg.src_row + i)) : sg.src_row + i;

@@ -57,7 +57,7 @@ struct SlabLayout {
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
   size_t lists, local_delta, recv_rows, recv_offs, tune, prow, rowpos, rowslot, dot, parts, gprobs, glogits, ones,
       wscale, cwire, cscale, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
-      ready, xchg_counters, xchg_flags, xtrace, aa_table, total;
+      ready, xchg_counters, xchg_flags, xtrace, aa_table, rowdst, total;
 };
 
 struct Card {
@@ -83,6 +83,7 @@ struct Card {
   uint64_t* xchg_flags = nullptr;     // [max_chunks] own-node chunk completion
   unsigned long long* xtrace = nullptr;  // [2 kernels][4 roles][max_chunks][2] role trace (ns)
   int32_t* aa_table = nullptr;        // [4 + max_chunks][E] token-side AA destinations
+  char** rowdst = nullptr;            // [recv_cap] reverse-AllToAll row address (peer comb) or null
   unsigned* front_done = nullptr;  // CTA election counter of the front kernel
   // layer backward scratch (moe_ctx_backward)
   void* prow = nullptr;
@@ -120,6 +121,7 @@ struct moe_ctx {
   cudaStream_t s_aa = nullptr, s_ag = nullptr, s_d2d = nullptr, s_cap = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join_aa = nullptr, ev_join_ag = nullptr, ev_join_d2d = nullptr;
   std::vector<cudaEvent_t> ev_aa, ev_ag;
+  bool expert_fused = true;  // moe_ctx_set_expert_overlap: down-projection epilogue issues the reverse AllToAll
   int aa_ctas = 0;
   bool combine_ready = false;  // a dispatch whose combine has not run yet
   bool debug = false;          // record front-kernel phase timestamps
@@ -222,6 +224,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.xchg_flags = take(size_t(d.max_chunks) * 8);
   s.xtrace = take(size_t(2) * 4 * d.max_chunks * 2 * 8);
   s.aa_table = take(size_t(4 + d.max_chunks) * E * 4);
+  s.rowdst = take(size_t(c->recv_cap) * 8);  // fused combine: each landed row's reverse-AllToAll destination
   s.total = off;
   return s;
 }
@@ -279,6 +282,7 @@ void bind_card(moe_ctx* c, Card& cd) {
   cd.xchg_flags = reinterpret_cast<uint64_t*>(b + s.xchg_flags);
   cd.xtrace = reinterpret_cast<unsigned long long*>(b + s.xtrace);
   cd.aa_table = reinterpret_cast<int32_t*>(b + s.aa_table);
+  cd.rowdst = reinterpret_cast<char**>(b + s.rowdst);
 }
 
 void set_peer(moe_ctx* c, int card, char* slab) {
@@ -1251,7 +1255,11 @@ extern "C" moe_status moe_ctx_dispatch(moe_ctx* c, int level, int32_t n, int lan
 
 namespace {
 
-moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bool concurrent) {
+// The reverse AllToAll of chunk j.  With l0 >= 0 only the rows of local
+// experts [l0, l1) (a contiguous final-layout range) move, and `signal`
+// says whether this launch releases the chunk's flags (the last group's).
+moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bool concurrent, int l0 = -1,
+                      int l1 = -1, bool signal = true, int grid_cap = 0) {
   const moe_layer_desc& d = c->d;
   if (d.e == 1) return MOE_OK;  // no other node: the un-permute reads every row in place
   const bool dedup = level != MOE_BASELINE && d.t > 1;
@@ -1299,9 +1307,18 @@ moe_status launch_caa(moe_ctx* c, Card& cd, int level, int j, cudaStream_t s, bo
     for (int g = 0; g < d.e; ++g)
       if (g != cd.node) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, g, cd.rho), sig_chunk(c, kPsCAA, j), cd.id);
   a.err = cd.err;
+  if (l0 >= 0) {
+    a.bounds = cd.v.recv_expert_offsets;
+    a.b_lo = l0;
+    a.b_hi = l1;
+  }
+  if (!signal) a.sig.n = 0;
   size_t sl;
   span_begin(c, MOE_STAGE_CAA, j, s, &sl);
-  MONTA_CUDA(launch_seg_copy(a, copy_vec(c, dedup), copy_grid(c, concurrent, true), s));
+  int grid = copy_grid(c, concurrent, true);
+  if (grid_cap > 0) grid = std::min(grid, grid_cap);
+  a.split = grid;
+  MONTA_CUDA(launch_seg_copy(a, copy_vec(c, dedup), grid, s));
   span_end(c, sl, s);
   ++c->launches;
   return MOE_OK;
@@ -1637,6 +1654,88 @@ moe_status experts_impl(moe_ctx* c, cudaStream_t s) {
   return MOE_OK;
 }
 
+// Expert compute fused with the reverse AllToAll (the
+// reference gates its expert task on the dispatch terminals and its combine
+// on the expert task, pipesim.hpp:102).  The down-projection GEMM's epilogue
+// stores every finished 128-row tile to this card's expert outputs AND, for
+// rows whose source sits on another node, straight into that source card's
+// landing buffer (`comb`) over NVLink — the reverse AllToAll leaves tile by
+// tile while the tensor cores work on the next tiles, in one kernel (the row
+// addresses come from the chunk CAA lists, k_rowdst).  One signal kernel then
+// releases every chunk's CAA flags and the un-permute runs as in the
+// per-launch combine.  Results are identical to experts-then-combine.
+bool overlap_experts(const moe_ctx* c) {
+  if (is_virtual(c) || !c->expert_fused || c->d.e < 2 || c->wire != MOE_WIRE_BF16 || c->pace_bpus) return false;
+  return c->local.size() == 1 && c->local[0].w13 != nullptr;
+}
+
+moe_status experts_combine_fused(moe_ctx* c, int level, int n, cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  Card& cd = c->local[0];
+  if (c->last_level < 0 || !c->combine_ready)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "experts: no dispatched rows to compute on");
+  if (n != c->last_n) return fail(MOE_ERR_INVALID_ARGUMENT, "combine: n = %d differs from the dispatch's %d", n, c->last_n);
+  if ((level != MOE_BASELINE && d.t > 1) != (c->last_level != MOE_BASELINE && d.t > 1))
+    return fail(MOE_ERR_INVALID_ARGUMENT, "combine: level must mirror the dispatch (baseline vs deduplicated)");
+  const bool dedup = level != MOE_BASELINE && d.t > 1;
+  if (moe_status st = dispatch_tail_wait(c, cd, c->last_level, c->last_n, MOE_LAND_FINAL, s)) return st;
+  PeerRows comb{};
+  for (int q = 0; q < c->cards; ++q)
+    if (c->peer[q].slab) comb.base[q] = c->peer[q].comb;
+  MONTA_CUDA(launch_rowdst(list_of(c, cd, kPhaseCAA, 0), seglist_bytes(d.num_experts), n, d.num_experts, comb,
+                           c->row_bytes, cd.rowdst, c->recv_cap, s));
+  ++c->launches;
+  // the CAA column window of this card: its 1/t slice under TP dedup, else the row
+  const int32_t col_lo = dedup ? int32_t(int64_t(cd.rho) * (c->row_bytes / d.t)) : 0;
+  const int32_t col_hi = dedup ? int32_t(col_lo + c->row_bytes / d.t) : int32_t(c->row_bytes);
+  size_t sl;
+  span_begin(c, MOE_STAGE_EXPERTS, -1, s, &sl);
+  if (moe_status st = expert_ffn_fused(cd.v.recv, d.hidden, c->recv_cap, cd.w13, cd.w2, cd.v.recv_expert_offsets, c->L,
+                                       d.hidden, cd.ffn, cd.ffn_ws, cd.v.expert_out, d.hidden, cd.rowdst, col_lo, col_hi,
+                                       s))
+    return st;
+  span_end(c, sl, s);
+  c->launches += 2;
+  c->combine_ready = false;
+  // every chunk's rows have left: release the sources' CAA flags
+  SignalList sg = no_signal();
+  sg.epoch_ptr = cd.epoch_dev;
+  for (int j = 0; j < n; ++j)
+    for (int g = 0; g < d.e; ++g) {
+      if (g == cd.node) continue;
+      if (sg.n == kMaxCards) {
+        MONTA_CUDA(launch_signal(sg, s));
+        ++c->launches;
+        sg.n = 0;
+      }
+      sg.flags[sg.n++] = flag_at(c, card_of(c, g, cd.rho), sig_chunk(c, kPsCAA, j), cd.id);
+    }
+  if (sg.n) {
+    MONTA_CUDA(launch_signal(sg, s));
+    ++c->launches;
+  }
+  for (int j = 0; j < n; ++j)
+    if (moe_status st = launch_unperm(c, cd, level, n, j, s, false)) return st;
+  if (dedup) {
+    WaitList w = no_wait();
+    w.epoch_ptr = cd.epoch_dev;
+    for (int j = 0; j < n; ++j) {
+      if (w.n + d.t - 1 > kMaxCards) {
+        MONTA_CUDA(launch_wait(w, cd.err, s));
+        ++c->launches;
+        w.n = 0;
+      }
+      for (int r = 0; r < d.t; ++r)
+        if (r != cd.rho) w.flags[w.n++] = flag_at(c, cd.id, sig_chunk(c, kPsCAG, j), card_of(c, cd.node, r));
+    }
+    if (w.n) {
+      MONTA_CUDA(launch_wait(w, cd.err, s));
+      ++c->launches;
+    }
+  }
+  return MOE_OK;
+}
+
 moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
                         cudaStream_t s) {
   const moe_layer_desc& d = c->d;
@@ -1665,8 +1764,12 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
   c->in_forward = false;
   if (st != MOE_OK) return st;
   if (moe_status st0 = verify_dispatch(c, s)) return st0;
-  if (moe_status st1 = experts_impl(c, s)) return st1;
-  if (moe_status st2 = combine_impl(c, level, n, s)) return st2;
+  if (overlap_experts(c)) {
+    if (moe_status st1 = experts_combine_fused(c, level, n, s)) return st1;
+  } else {
+    if (moe_status st1 = experts_impl(c, s)) return st1;
+    if (moe_status st2 = combine_impl(c, level, n, s)) return st2;
+  }
   if (ho)
     for (size_t i = 0; i < c->local.size(); ++i)
       MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(ho) + i * obytes, c->local[i].v.out, obytes,
@@ -2164,6 +2267,18 @@ extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint
       return MOE_OK;
     }
   return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: card %d is not local", card);
+}
+
+extern "C" moe_status moe_ctx_set_expert_overlap(moe_ctx* c, int32_t enable) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "set_expert_overlap: null ctx");
+  if (c->expert_fused != (enable != 0)) {
+    MONTA_CUDA(cudaSetDevice(c->device));
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+  }
+  c->expert_fused = enable != 0;
+  return MOE_OK;
 }
 
 extern "C" moe_status moe_ctx_set_persistent(moe_ctx* c, int enable) {

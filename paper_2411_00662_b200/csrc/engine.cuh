@@ -64,6 +64,10 @@ struct CopyArgs {
   SignalList sig;
   int32_t* err;
   uint32_t pace_bpus;        // emulated inter-node link (moe_ctx_set_link_rate): bytes per us, 0 = off
+  // optional source-row filter: only segments with bounds[b_lo] <= src_row <
+  // bounds[b_hi] are copied (the reverse AllToAll of one expert group)
+  const int32_t* bounds;
+  int32_t b_lo, b_hi;
 };
 
 struct UnpermArgs {
@@ -127,6 +131,20 @@ struct TokArgs {
   // cards on one GPU): the TMA bulk-copy form may run (aa.cu k_aa_bulk)
   int32_t local_dst;
 };
+// Fused combine (experts.cu + ctx.cu): rowdst[r] = the address of final-layout
+// row r's reverse-AllToAll destination row (a peer's comb) from the CAA lists
+// of chunks [0, n), null for rows that stay on this node.
+struct PeerRows {
+  char* base[kMaxCards];
+};
+cudaError_t launch_rowdst(const SegList* lists, size_t list_stride, int n, int nseg_cap, const PeerRows& comb,
+                          int64_t row_bytes, char** rowdst, int64_t cap, cudaStream_t s);
+// SwiGLU expert FFN whose down-projection epilogue also stores each row's
+// bytes [col_lo, col_hi) to rowdst[r] (when non-null): the reverse AllToAll
+// issued tile by tile from the GEMM (experts.cu).
+moe_status expert_ffn_fused(const void* x, int64_t ldx, int64_t x_rows, const void* w13, const void* w2,
+                            const int32_t* offs, int L, int64_t hidden, int64_t ffn, void* workspace, void* y,
+                            int64_t ldy, char* const* rowdst, int32_t col_lo, int32_t col_hi, cudaStream_t s);
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s);
 // fp8 wire, combine leg (aa.cu): the reverse AllToAll of one chunk (CAA
 // segment list) quantised into each source card's cwire / cscale; the

@@ -39,6 +39,7 @@ constexpr int kUK = 16;                   // UMMA K for kind::f16
 constexpr int kThreads = 192;             // 6 warps: producer, MMA, 4 epilogue
 constexpr int kMaxExperts = 1024;
 constexpr uint32_t kABytes = kBM * kBK * 2;
+constexpr int kStgRow = 144;  // staged row pitch (128 B of data + 16 B against bank conflicts)
 
 template <int BN> struct Cfg {
   static constexpr int kStages = BN == 256 ? 4 : 6;
@@ -46,8 +47,9 @@ template <int BN> struct Cfg {
   static constexpr uint32_t kStageBytes = kABytes + kBBytes;
   static constexpr uint32_t kTmemCols = 2 * BN;  // two accumulators
   // ring | barriers (2*stages + 4) x 8 B | tmem slot | tile prefix [kMaxExperts+1]
+  // ... | fused-store staging: 4 epilogue warps x 32 rows x (128 + 16) B
   static constexpr size_t kSmem = 1024 + size_t(kStages) * kStageBytes + (2 * kStages + 4) * 8 + 16 +
-                                  (kMaxExperts + 1) * 4 + 4 * (kMaxExperts + 1);
+                                  (kMaxExperts + 1) * 4 + 4 * (kMaxExperts + 1) + 16 + 4 * 32 * kStgRow;
 };
 
 // ---------------------------------------------------------------------------
@@ -146,6 +148,10 @@ struct GemmArgs {
   __nv_bfloat16* y;
   int64_t ldy;          // elements
   int32_t swiglu;       // epilogue: columns [0, BN/2) gate, [BN/2, BN) up of the tile
+  // fused reverse AllToAll (plain epilogue only): row r's bytes [col_lo, col_hi)
+  // also go to rowdst[r] when it is non-null (a peer's landing row over NVLink)
+  char* const* rowdst;
+  int32_t col_lo, col_hi;
 };
 
 // Tile t -> (expert, n-block, m-block); tiles of one expert are n-major,
@@ -181,6 +187,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
   int* prefix = reinterpret_cast<int*>(tmem_slot + 4);
   int* mtiles = prefix + kMaxExperts + 1;
+  uint8_t* stage_rows = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(mtiles + kMaxExperts + 1) + 15) &
+                                                   ~uintptr_t(15));
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int L = p.L;
@@ -330,22 +338,55 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       } else {
+        // fused reverse AllToAll: this row's peer landing row (null: stays on
+        // this node).  The remote copy goes through a per-warp staging block
+        // of 32 rows x 128 B so each store instruction writes four whole
+        // 128-byte row segments over NVLink (a thread-per-row store would
+        // send 32 scattered 16-byte pieces per instruction).
+        const char* rrow = (valid && p.rowdst) ? p.rowdst[r0 + row_in_tile] : nullptr;
+        const bool any_remote = __any_sync(0xffffffffu, rrow != nullptr);
+        uint8_t* stg = stage_rows + size_t(q) * 32 * kStgRow;
 #pragma unroll 1
         for (int c = 0; c < BN; c += 32) {
           uint32_t a[32];
           tmem_ld32(tbase + uint32_t(c), a);
           tmem_wait_ld();
+          uint4 o[4];
+#pragma unroll
+          for (int v = 0; v < 4; ++v) {
+            uint32_t w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int i = v * 8 + 2 * j;
+              w[j] = pack_bf16(__uint_as_float(a[i]), __uint_as_float(a[i + 1]));
+            }
+            o[v] = make_uint4(w[0], w[1], w[2], w[3]);
+          }
           if (valid) {
             uint4* dst = reinterpret_cast<uint4*>(yrow + int64_t(nb) * BN + c);
 #pragma unroll
-            for (int v = 0; v < 4; ++v) {
-              uint32_t w[4];
+            for (int v = 0; v < 4; ++v) dst[v] = o[v];
+          }
+          if (any_remote) {
+            const int half = (c >> 5) & 1;  // 64 B of the 128-B staged segment
+            uint4* srow = reinterpret_cast<uint4*>(stg + lane * kStgRow + half * 64);
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                const int i = v * 8 + 2 * j;
-                w[j] = pack_bf16(__uint_as_float(a[i]), __uint_as_float(a[i + 1]));
+            for (int v = 0; v < 4; ++v) srow[v] = o[v];
+            if (half == 1 || c + 32 >= BN) {  // a 128-B segment (or the tile's last 64 B) is staged
+              __syncwarp();
+              const int64_t seg_b = (int64_t(nb) * BN + (c & ~63)) * 2;  // byte column of the segment
+              const int nchunk = half == 1 ? 8 : 4;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const int r = i * 4 + (lane >> 3), ch = lane & 7;
+                const char* rr = reinterpret_cast<const char*>(
+                    __shfl_sync(0xffffffffu, reinterpret_cast<unsigned long long>(rrow), r));
+                const int64_t bc = seg_b + ch * 16;
+                if (rr && ch < nchunk && bc >= p.col_lo && bc < p.col_hi)
+                  *reinterpret_cast<uint4*>(const_cast<char*>(rr) + bc) =
+                      *reinterpret_cast<const uint4*>(stg + r * kStgRow + ch * 16);
               }
-              dst[v] = make_uint4(w[0], w[1], w[2], w[3]);
+              __syncwarp();
             }
           }
         }
@@ -455,7 +496,8 @@ moe_status configure_grouped_gemm() {
 }
 
 moe_status grouped_gemm(const void* x, int64_t ldx, int64_t x_rows, const void* w, const int32_t* offs, int L,
-                        int64_t N, int64_t K, void* y, int64_t ldy, int act, int grid, cudaStream_t s) {
+                        int64_t N, int64_t K, void* y, int64_t ldy, int act, int grid, cudaStream_t s,
+                        char* const* rowdst = nullptr, int32_t col_lo = 0, int32_t col_hi = 0) {
   if (L < 1 || L > kMaxExperts) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: need 1 <= L <= %d", kMaxExperts);
   if (!x || !w || !offs || !y) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: null pointer");
   if (K < kBK || K % kBK) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: K must be a positive multiple of 64");
@@ -475,9 +517,21 @@ moe_status grouped_gemm(const void* x, int64_t ldx, int64_t x_rows, const void* 
   CUtensorMap ta, tb;
   if (moe_status st = make_map(&ta, x, x_rows, K, ldx, kBM)) return st;
   if (moe_status st = make_map(&tb, w, int64_t(L) * N, K, K, bn)) return st;
-  GemmArgs a{offs, L, int32_t(N), int32_t(K), static_cast<__nv_bfloat16*>(y), ldy, act == MOE_ACT_SWIGLU};
+  if (rowdst && act != MOE_ACT_NONE) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: fused stores need act NONE");
+  GemmArgs a{offs, L, int32_t(N), int32_t(K), static_cast<__nv_bfloat16*>(y), ldy, act == MOE_ACT_SWIGLU,
+             rowdst, col_lo, col_hi};
   if (grid <= 0) grid = sm_count_of_current();
   return bn == 256 ? launch_gemm<256>(ta, tb, a, grid, s) : launch_gemm<128>(ta, tb, a, grid, s);
+}
+
+moe_status expert_ffn_fused(const void* x, int64_t ldx, int64_t x_rows, const void* w13, const void* w2,
+                            const int32_t* offs, int L, int64_t hidden, int64_t ffn, void* workspace, void* y,
+                            int64_t ldy, char* const* rowdst, int32_t col_lo, int32_t col_hi, cudaStream_t s) {
+  if (!workspace) return fail(MOE_ERR_INVALID_ARGUMENT, "expert_ffn: null workspace");
+  if (moe_status st = grouped_gemm(x, ldx, x_rows, w13, offs, L, 2 * ffn, hidden, workspace, ffn, MOE_ACT_SWIGLU, 0, s))
+    return st;
+  return grouped_gemm(workspace, ffn, x_rows, w2, offs, L, hidden, ffn, y, ldy, MOE_ACT_NONE, 0, s, rowdst, col_lo,
+                      col_hi);
 }
 
 }  // namespace monta

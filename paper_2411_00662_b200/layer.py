@@ -221,6 +221,10 @@ class MoeLayer:
     def experts(self, stream=None) -> None:
         check(self.lib.moe_ctx_experts(self._ctx, _stream_ptr(stream)))
 
+    def set_expert_overlap(self, enable: bool) -> None:
+        """Fuse the reverse AllToAll into the experts' down-projection epilogue (multi-GPU forward)."""
+        check(self.lib.moe_ctx_set_expert_overlap(self._ctx, int(bool(enable))))
+
     def bind_expert_out(self, card: int, tensor: torch.Tensor | None) -> None:
         check(self.lib.moe_ctx_bind_expert_out(self._ctx, card, tensor.data_ptr() if tensor is not None else None))
 

@@ -93,6 +93,13 @@ def main():
             results[f"pre_{key}"] = cd.pre[:rows].contiguous().view(torch.uint8).cpu().numpy()
             results[f"pretags_{key}"] = cd.pre_tags[:rows].cpu().numpy()
         results[f"out_{key}"] = cd.out.float().cpu().numpy()
+        if a.ffn:  # the fused down-projection + reverse AllToAll must give the sequential result bit for bit
+            out_on = cd.out.clone()
+            layer.set_expert_overlap(False)
+            layer.forward(level, n, landing)
+            layer.sync()
+            results[f"overlap_same_{key}"] = np.array([bool(torch.equal(out_on, cd.out))])
+            layer.set_expert_overlap(True)
     results["experts"] = cd.experts.cpu().numpy()
     results["probs"] = cd.probs.double().cpu().numpy()
     results["x"] = x.contiguous().view(torch.uint8).numpy()

@@ -179,6 +179,8 @@ def _check_experts(ranks, e, t, E, F, runs):
             got = torch.from_numpy(ranks[r][f"out_{level}_{n}_{landing}"]).cuda()
             bad = (got - ref).abs() > 2.0 ** -8 * ref.abs() + mag + 1e-6
             assert not bool(bad.any()), (spec, r, int(bad.sum()))
+            # experts overlapped with the reverse AllToAll == experts then combine, bit for bit
+            assert bool(ranks[r][f"overlap_same_{level}_{n}_{landing}"][0]), (spec, r)
 
 
 def test_two_gpus_ep2_with_experts(cuda, tmp_path):
