@@ -351,10 +351,11 @@ FFN_DIM = {"deepseek-v2-finegrained-moe-layer": 1536, "mixtral-8x7b-moe-layer": 
            "2x70b-moe-layer": 28672}  # expert intermediate size of each workload's model
 
 
-def experts_leg(layer, cd, e, t, E, h, step, timed, steps, local):
+def experts_leg(layer, cd, e, t, E, h, step, timed, steps, local, dedup=False):
     """Layer step with the experts bound (random-init SwiGLU weights of the
     workload's expert shape): us/layer, the experts stage's time and its
-    tensor-core throughput (2 * rows * 3 * F * h flops per card) against
+    tensor-core throughput (2 * rows * (2F * h + F * down_cols) flops per card:
+    down_cols = h / t under TP dedup, the slice the card's combine reads) against
     MEASURED_PEAKS.json's sustained bf16 figure."""
     import torch
     from paper_2411_00662_b200 import ops
@@ -396,7 +397,10 @@ def experts_leg(layer, cd, e, t, E, h, step, timed, steps, local):
     finally:
         layer.bind_experts(cd.card, None)
     ex_us = 1e3 * statistics.median(sum(v) for v in sp)
-    flops = 2.0 * rows * 3 * F * h
+    # gate/up over every landed row; the down-projection over the columns the
+    # card's combine reads (its 1/t slice under TP dedup, csrc/ctx.cu)
+    down_cols = h // t if (dedup and (h // t) % 128 == 0) else h
+    flops = 2.0 * rows * (2 * F * h + F * down_cols)
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             pk = json.load(f)
@@ -408,7 +412,7 @@ def experts_leg(layer, cd, e, t, E, h, step, timed, steps, local):
             "us_per_layer_with_experts_no_overlap": seq,
             "reverse_alltoall_fused_into_down_proj": e > 1,
             "experts_us": ex_us, "rows": rows, "ffn": F,
-            "local_experts": L, "flops_per_card": flops,
+            "local_experts": L, "flops_per_card": flops, "down_proj_cols": down_cols,
             "roofline": {"bound": "tensor", "kernel": "k_grouped_gemm x2 (SwiGLU gate/up, down)", "achieved": ach,
                          "peak": peak, "unit": "TFLOP/s", "frac": ach / peak, "peak_kind": kind},
             "note": "random-init SwiGLU experts of the workload's expert shape (h x F) between dispatch and "
@@ -729,7 +733,8 @@ def main():
     experts = None
     if not args.quick and CONFIG["dtype"] == "bf16":
         try:
-            experts = experts_leg(layer, cd, e, t, E, h, step, timed, args.steps, local)
+            experts = experts_leg(layer, cd, e, t, E, h, step, timed, args.steps, local,
+                                  dedup=(level != BASELINE and t > 1))
         except Exception as exc:  # extra figures: never lose the bench line to them
             experts = {"error": f"{type(exc).__name__}: {exc}"}
 

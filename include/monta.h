@@ -334,7 +334,10 @@ moe_status moe_ctx_bind_expert_out(moe_ctx* ctx, int card, void* expert_out);
  * default).  w13 [L][2 ffn][h] from moe_interleave_w13, w2 [L][h][ffn], bf16,
  * owned by the caller; the context allocates a [recv_cap, ffn] workspace.
  * Under TP (t > 1) every rank of a node holds the node's full rows after the
- * AllGather and computes the full FFN with the weights bound to it.  Pass
+ * AllGather and runs the gate/up projection on all of them; with TP dedup
+ * (level != MOE_BASELINE) the down-projection computes only the rank's 1/t
+ * output column slice — the only columns its combine reads — so expert_out
+ * columns outside the slice are left untouched.  Pass
  * w13 == NULL to unbind (identity experts).  Needs dtype bf16, h % 64 == 0,
  * ffn % 128 == 0. */
 moe_status moe_ctx_bind_experts(moe_ctx* ctx, int card, const void* w13, const void* w2, int64_t ffn);

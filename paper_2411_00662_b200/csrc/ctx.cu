@@ -1645,8 +1645,11 @@ moe_status experts_impl(moe_ctx* c, cudaStream_t s) {
     if (!cd.w13) continue;
     size_t sl;
     span_begin(c, MOE_STAGE_EXPERTS, -1, s, &sl);
-    if (moe_status st = moe_expert_ffn(cd.v.recv, h, c->recv_cap, cd.w13, cd.w2, cd.v.recv_expert_offsets, c->L, h,
-                                       cd.ffn, cd.ffn_ws, cd.v.expert_out, h, s))
+    // under TP dedup the combine reads only this card's 1/t column slice
+    const bool slice = c->last_level != MOE_BASELINE && c->d.t > 1 && (h / c->d.t) % 128 == 0;
+    const int64_t oc0 = slice ? int64_t(cd.rho) * (h / c->d.t) : 0, ocn = slice ? h / c->d.t : h;
+    if (moe_status st = expert_ffn_fused(cd.v.recv, h, c->recv_cap, cd.w13, cd.w2, cd.v.recv_expert_offsets, c->L, h,
+                                         cd.ffn, cd.ffn_ws, cd.v.expert_out, h, nullptr, 0, 0, oc0, ocn, s))
       return st;
     span_end(c, sl, s);
     c->launches += 2;
@@ -1690,9 +1693,15 @@ moe_status experts_combine_fused(moe_ctx* c, int level, int n, cudaStream_t s) {
   const int32_t col_hi = dedup ? int32_t(col_lo + c->row_bytes / d.t) : int32_t(c->row_bytes);
   size_t sl;
   span_begin(c, MOE_STAGE_EXPERTS, -1, s, &sl);
+  // under TP dedup this card's combine reads only its 1/t column slice of
+  // the expert outputs (local rows in place, remote rows via the fused
+  // stores): the down-projection computes just that slice
+  const bool slice = dedup && (d.hidden / d.t) % 128 == 0;  // the GEMM's 128-column blocks
+  const int64_t oc0 = slice ? int64_t(cd.rho) * (d.hidden / d.t) : 0;
+  const int64_t ocn = slice ? d.hidden / d.t : d.hidden;
   if (moe_status st = expert_ffn_fused(cd.v.recv, d.hidden, c->recv_cap, cd.w13, cd.w2, cd.v.recv_expert_offsets, c->L,
                                        d.hidden, cd.ffn, cd.ffn_ws, cd.v.expert_out, d.hidden, cd.rowdst, col_lo, col_hi,
-                                       s))
+                                       oc0, ocn, s))
     return st;
   span_end(c, sl, s);
   c->launches += 2;

@@ -139,12 +139,15 @@ struct PeerRows {
 };
 cudaError_t launch_rowdst(const SegList* lists, size_t list_stride, int n, int nseg_cap, const PeerRows& comb,
                           int64_t row_bytes, char** rowdst, int64_t cap, cudaStream_t s);
-// SwiGLU expert FFN whose down-projection epilogue also stores each row's
-// bytes [col_lo, col_hi) to rowdst[r] (when non-null): the reverse AllToAll
-// issued tile by tile from the GEMM (experts.cu).
+// SwiGLU expert FFN whose down-projection computes output columns
+// [out_col0, out_col0 + out_cols) only (a TP rank's combine slice) and whose
+// epilogue also stores each row's bytes [col_lo, col_hi) to rowdst[r] (when
+// rowdst and the entry are non-null): the reverse AllToAll issued tile by
+// tile from the GEMM (experts.cu).
 moe_status expert_ffn_fused(const void* x, int64_t ldx, int64_t x_rows, const void* w13, const void* w2,
                             const int32_t* offs, int L, int64_t hidden, int64_t ffn, void* workspace, void* y,
-                            int64_t ldy, char* const* rowdst, int32_t col_lo, int32_t col_hi, cudaStream_t s);
+                            int64_t ldy, char* const* rowdst, int32_t col_lo, int32_t col_hi, int64_t out_col0,
+                            int64_t out_cols, cudaStream_t s);
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s);
 // fp8 wire, combine leg (aa.cu): the reverse AllToAll of one chunk (CAA
 // segment list) quantised into each source card's cwire / cscale; the

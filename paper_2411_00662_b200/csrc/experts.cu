@@ -152,6 +152,9 @@ struct GemmArgs {
   // also go to rowdst[r] when it is non-null (a peer's landing row over NVLink)
   char* const* rowdst;
   int32_t col_lo, col_hi;
+  // plain epilogue: compute output columns [n_off, n_off + N) of each expert
+  // whose weight has n_stride rows (N == n_stride, n_off == 0: all of them)
+  int32_t n_stride, n_off;
 };
 
 // Tile t -> (expert, n-block, m-block); tiles of one expert are n-major,
@@ -254,7 +257,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         int l, nb, mb;
         decode_tile(t, prefix, mtiles, L, nblocks, l, nb, mb);
         const int arow = __ldg(p.offs + l) + mb * kBM;
-        const int brow = l * p.N + nb * BN;
+        const int brow = l * p.n_stride + p.n_off + nb * BN;
         for (int kb = 0; kb < kblocks; ++kb) {
           mbar_wait(&empty[stage], phase ^ 1);
           uint8_t* sa = ring + size_t(stage) * C::kStageBytes;
@@ -363,7 +366,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             o[v] = make_uint4(w[0], w[1], w[2], w[3]);
           }
           if (valid) {
-            uint4* dst = reinterpret_cast<uint4*>(yrow + int64_t(nb) * BN + c);
+            uint4* dst = reinterpret_cast<uint4*>(yrow + p.n_off + int64_t(nb) * BN + c);
 #pragma unroll
             for (int v = 0; v < 4; ++v) dst[v] = o[v];
           }
@@ -374,7 +377,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int v = 0; v < 4; ++v) srow[v] = o[v];
             if (half == 1 || c + 32 >= BN) {  // a 128-B segment (or the tile's last 64 B) is staged
               __syncwarp();
-              const int64_t seg_b = (int64_t(nb) * BN + (c & ~63)) * 2;  // byte column of the segment
+              const int64_t seg_b = (p.n_off + int64_t(nb) * BN + (c & ~63)) * 2;  // byte column of the segment
               const int nchunk = half == 1 ? 8 : 4;
 #pragma unroll
               for (int i = 0; i < 8; ++i) {
@@ -497,7 +500,8 @@ moe_status configure_grouped_gemm() {
 
 moe_status grouped_gemm(const void* x, int64_t ldx, int64_t x_rows, const void* w, const int32_t* offs, int L,
                         int64_t N, int64_t K, void* y, int64_t ldy, int act, int grid, cudaStream_t s,
-                        char* const* rowdst = nullptr, int32_t col_lo = 0, int32_t col_hi = 0) {
+                        char* const* rowdst = nullptr, int32_t col_lo = 0, int32_t col_hi = 0, int64_t n_stride = 0,
+                        int64_t n_off = 0) {
   if (L < 1 || L > kMaxExperts) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: need 1 <= L <= %d", kMaxExperts);
   if (!x || !w || !offs || !y) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: null pointer");
   if (K < kBK || K % kBK) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: K must be a positive multiple of 64");
@@ -514,24 +518,28 @@ moe_status grouped_gemm(const void* x, int64_t ldx, int64_t x_rows, const void* 
   if (x_rows <= 0) return MOE_OK;
   if (x_rows > INT32_MAX || int64_t(L) * N > INT32_MAX)
     return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: too many rows for 32-bit TMA coordinates");
+  if (n_stride == 0) n_stride = N;
+  if (n_off < 0 || n_off + N > n_stride || (act != MOE_ACT_NONE && n_stride != N) || n_off % 8)
+    return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: bad output column window");
   CUtensorMap ta, tb;
   if (moe_status st = make_map(&ta, x, x_rows, K, ldx, kBM)) return st;
-  if (moe_status st = make_map(&tb, w, int64_t(L) * N, K, K, bn)) return st;
+  if (moe_status st = make_map(&tb, w, int64_t(L) * n_stride, K, K, bn)) return st;
   if (rowdst && act != MOE_ACT_NONE) return fail(MOE_ERR_INVALID_ARGUMENT, "grouped_gemm: fused stores need act NONE");
   GemmArgs a{offs, L, int32_t(N), int32_t(K), static_cast<__nv_bfloat16*>(y), ldy, act == MOE_ACT_SWIGLU,
-             rowdst, col_lo, col_hi};
+             rowdst, col_lo, col_hi, int32_t(n_stride), int32_t(n_off)};
   if (grid <= 0) grid = sm_count_of_current();
   return bn == 256 ? launch_gemm<256>(ta, tb, a, grid, s) : launch_gemm<128>(ta, tb, a, grid, s);
 }
 
 moe_status expert_ffn_fused(const void* x, int64_t ldx, int64_t x_rows, const void* w13, const void* w2,
                             const int32_t* offs, int L, int64_t hidden, int64_t ffn, void* workspace, void* y,
-                            int64_t ldy, char* const* rowdst, int32_t col_lo, int32_t col_hi, cudaStream_t s) {
+                            int64_t ldy, char* const* rowdst, int32_t col_lo, int32_t col_hi, int64_t out_col0,
+                            int64_t out_cols, cudaStream_t s) {
   if (!workspace) return fail(MOE_ERR_INVALID_ARGUMENT, "expert_ffn: null workspace");
   if (moe_status st = grouped_gemm(x, ldx, x_rows, w13, offs, L, 2 * ffn, hidden, workspace, ffn, MOE_ACT_SWIGLU, 0, s))
     return st;
-  return grouped_gemm(workspace, ffn, x_rows, w2, offs, L, hidden, ffn, y, ldy, MOE_ACT_NONE, 0, s, rowdst, col_lo,
-                      col_hi);
+  return grouped_gemm(workspace, ffn, x_rows, w2, offs, L, out_cols, ffn, y, ldy, MOE_ACT_NONE, 0, s, rowdst, col_lo,
+                      col_hi, hidden, out_col0);
 }
 
 }  // namespace monta
