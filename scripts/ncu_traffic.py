@@ -11,7 +11,8 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 import bench  # noqa: E402
 
-STAGE = (("k_front", "front"), ("k_aa_token", "fused_permute_aa"), ("k_unpermute", "unpermute_combine"))
+STAGE = (("k_front", "front"), ("k_aa_token", "fused_permute_aa"), ("k_aa_bulk", "fused_permute_aa"),
+         ("k_unpermute", "unpermute_combine"))
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-3, "us": 1.0, "usecond": 1.0,
          "nsecond": 1e-3, "ms": 1e3, "msecond": 1e3}
 METRICS = ("gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum")
