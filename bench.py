@@ -267,7 +267,8 @@ def cpu_baseline_value(e, t, E, k, T, h, budget_s=10.0, max_reps=100):
 
 def run_reference(args):
     """--impl reference: the reference's CPU path on this host (rank 0 only).
-    The reference headers (oracle/_ref) cannot run this workload — with more
+    With one expert per node (E == e: the 2x70B layer at N = 2) the unmodified
+    reference headers (oracle/_ref) run.  Otherwise they cannot — with more
     experts than nodes (E = 160 on e <= 4) its dispatch drops records and its
     combine indexes out of bounds (SURVEY.md §7 decision 1) — so the arm times
     the oracle port, the C restatement of the same algorithm generalised to
@@ -277,6 +278,42 @@ def run_reference(args):
         return
     e, t = topo_for(args.gpus)
     T, h, E, k = CONFIG["tokens_per_node"], CONFIG["hidden"], CONFIG["experts"], CONFIG["top_k"]
+    import oracle
+    if E == e and oracle.ref_available():
+        # one expert per node (the 2x70B layer at N = 2): the reference itself
+        # runs — its route_topk and dispatch + combine on its own int64
+        # payload records, single-threaded, on a bounded token sample scaled
+        # to the node batch
+        import numpy as np
+        Ts = min(T, 1024)
+
+        def ref_layer(seed):
+            rng = np.random.default_rng(seed)
+            pay = rng.integers(-1000, 1000, size=(e, Ts, h), dtype=np.int64)
+            sc = rng.standard_normal((e, Ts, E))
+            t0 = time.perf_counter()
+            ex = np.zeros((e, Ts, k), np.int32)
+            pr = np.zeros((e, Ts, k), np.float64)
+            for g in range(e):
+                ex[g], pr[g] = oracle.ref_route_topk(sc[g], k)
+            oracle.ref_dataplane(e, t, pay, ex, pr, level=-1 if t == 1 else 1, n=1)
+            return (time.perf_counter() - t0) * T / Ts
+
+        for _ in range(max(1, args.warmup)):
+            ref_layer(0)
+        vals = [ref_layer(s + 1) * 1e6 for s in range(max(1, args.steps))]
+        v = statistics.mean(vals)
+        line = {"metric": METRIC, "value": v, "unit": "us/layer", "n_gpus": args.gpus, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": v / 1e3, "higher_is_better": False, "scaling": "weak",
+                "vs_baseline": None, "dtype": CONFIG["dtype"], "data": "synthetic", "impl": "reference",
+                "config": workload_config(e, t),
+                "cpu_baseline": {"value": v, "unit": "us/layer", "cores": 1, "kind": "reference",
+                                 "sample": f"{Ts} of {T} tokens per node x {e} nodes per step, scaled x{T / Ts:g}; "
+                                           "unmodified reference headers (oracle/_ref: route_topk, dispatch, "
+                                           "combine_unpermute on int64 payload records), 1 thread"},
+                "e2e": {"value": v, "unit": "us/layer", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
     for _ in range(max(1, args.warmup)):
         cpu_port_layer(e, t, E, k, T, h)
     vals = [cpu_port_layer(e, t, E, k, T, h, seed=s) * 1e6 for s in range(max(1, args.steps))]
