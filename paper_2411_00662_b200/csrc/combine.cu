@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(kThreads, MinB) k_unpermute_k2(const __grid_co
   const int warps = int(gridDim.x) * (kThreads / 32);
   const uint64_t pol = l2_evict_first_policy();
   for (int it = int(blockIdx.x) * (kThreads / 32) + (threadIdx.x >> 5); it < n_items; it += warps) {
-    const int64_t i = a.tok_begin + it / nb;
+    const int64_t i = a.reverse ? a.tok_end - 1 - it / nb : a.tok_begin + it / nb;  // newest rows first (L2)
     const int cv = (it % nb) * (32 * UV);  // first vector of the item
     const char* row = nullptr;
     float p = 0.f;
@@ -277,7 +277,10 @@ __global__ void __launch_bounds__(kRowThreads, MinB) k_unpermute_rows(const __gr
   const int nvec = int(a.cols / N);
   const uint64_t pol = l2_evict_first_policy();
   int buf = 0;
-  for (int64_t i = a.tok_begin + blockIdx.x; i < a.tok_end; i += gridDim.x, buf ^= 1) {
+  for (int64_t it = a.tok_begin + blockIdx.x; it < a.tok_end; it += gridDim.x, buf ^= 1) {
+    // newest rows first: the permute wrote tokens in ascending order, so the
+    // highest tokens' rows are the ones still in L2
+    const int64_t i = a.reverse ? a.tok_end - 1 - (it - a.tok_begin) : it;
     if (threadIdx.x < k) {
       const int64_t q = i * k + threadIdx.x;
       const int pos = __ldg(a.slot_pos + q);

@@ -1363,6 +1363,16 @@ moe_status launch_unperm(moe_ctx* c, Card& cd, int level, int n, int j, cudaStre
         if (r != cd.rho) a.sig.flags[a.sig.n++] = flag_at(c, card_of(c, cd.node, r), sig_chunk(c, kPsCAG, j), cd.id);
   }
   a.err = cd.err;
+  {
+    // a lone card's un-permute reads the rows its permute just wrote: newest
+    // (highest tokens) first, while they are still in L2 (MONTA_UNPERM_REV
+    // overrides, A/B)
+    static const int rev = [] {
+      const char* e = std::getenv("MONTA_UNPERM_REV");
+      return e ? std::atoi(e) : -1;
+    }();
+    a.reverse = rev >= 0 ? rev : (is_virtual(c) && c->local.size() == 1 ? 1 : 0);
+  }
   // resident CTAs (2 per SM at 256 threads); the launcher clamps to the item count
   const int grid = concurrent ? c->sms / 2 : c->sms;  // SM budget (the launcher sizes per kernel)
   if (moe_status st = hoist_wait(c, a.wait, cd.err, s)) return st;

@@ -84,6 +84,7 @@ struct UnpermArgs {
   int64_t col_begin, cols;   // element columns to produce
   int64_t out_stride;        // bytes per output row
   int32_t n_out;
+  int32_t reverse;           // k_unpermute_rows: tokens in descending order
   char* out[kMaxCards];      // every destination (fused all-gather)
   WaitList wait;
   SignalList sig;
