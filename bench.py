@@ -814,7 +814,7 @@ def main():
         ach = kern["fused_permute_aa"]
         traffic_alg = aa_bytes
         # the lone card's full-batch permute runs the TMA ring (aa.cu launch_aa_token)
-        bulk = (world == 1 and T >= 2048 and (h * ELEM) % 16 == 0 and os.environ.get("MONTA_AA_BULK", "1") != "0"
+        bulk = (world == 1 and T >= 2048 and k >= 4 and (h * ELEM) % 16 == 0 and os.environ.get("MONTA_AA_BULK", "1") != "0"
                 and args.wire == "bf16" and not args.link_gbs)
         dom_name = "fused_permute_aa (k_aa_bulk)" if bulk else "fused_permute_aa (k_aa_token<16>)"
     else:

@@ -404,10 +404,13 @@ cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s)
   if (a.k > kTokMaxK) return cudaErrorNotSupported;
   static const int bulk = env_int("MONTA_AA_BULK", 1);
   const uint32_t sb = uint32_t((a.row_bytes + 127) & ~int64_t(127));
-  // the ring pays when each CTA streams many tokens (the full-batch launch);
-  // a pipelined chunk of a few hundred tokens stays on the register path
+  // the ring pays when each CTA streams many tokens (the full-batch launch;
+  // a pipelined chunk of a few hundred tokens stays on the register path) and
+  // each row fans out to many slots: DeepSeek k = 6 107.5 -> 103 us, while at
+  // k = 2 / k = 1 the register path is faster (Mixtral 19.6 vs 26.5 us, 2x70B
+  // 44.9 vs 51.0 us)
   const int64_t ntok = a.tok_end - a.tok_begin;
-  if (bulk && ntok >= 2048 && a.local_dst && !a.fp8 && !a.pace_list && vec == 16 && a.row_bytes % 16 == 0 &&
+  if (bulk && ntok >= 2048 && a.k >= 4 && a.local_dst && !a.fp8 && !a.pace_list && vec == 16 && a.row_bytes % 16 == 0 &&
       a.dst_stride % 16 == 0 && reinterpret_cast<uintptr_t>(a.x) % 16 == 0 && sb <= 64 * 1024) {
     static const int want_stages = env_int("MONTA_AA_STAGES", 8);
     static const int depth_env = env_int("MONTA_AA_DEPTH", 4);
