@@ -119,6 +119,12 @@ struct moe_ctx {
   monta::PeerPtrs peer[monta::kMaxCards];
   std::vector<void*> opened;
   cudaStream_t s_aa = nullptr, s_ag = nullptr, s_d2d = nullptr, s_cap = nullptr;
+  // forward_host on a multi-GPU rank: host copies pipelined per token chunk
+  cudaStream_t s_h2d = nullptr, s_d2h = nullptr;
+  std::vector<cudaEvent_t> ev_h2d, ev_d2h;
+  cudaEvent_t ev_join_d2h = nullptr;
+  bool pipe = false;       // set by forward_impl for one call: AA(j) waits H2D(j), D2H(j) follows un-permute(j)
+  char* pipe_ho = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join_aa = nullptr, ev_join_ag = nullptr, ev_join_d2d = nullptr;
   std::vector<cudaEvent_t> ev_aa, ev_ag;
   bool expert_fused = true;  // moe_ctx_set_expert_overlap: down-projection epilogue issues the reverse AllToAll
@@ -460,6 +466,8 @@ extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int
   cudaStreamCreateWithPriority(&c->s_ag, cudaStreamNonBlocking, lo);
   cudaStreamCreateWithPriority(&c->s_d2d, cudaStreamNonBlocking, lo);
   cudaStreamCreateWithFlags(&c->s_cap, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->s_h2d, cudaStreamNonBlocking);
+  cudaStreamCreateWithFlags(&c->s_d2h, cudaStreamNonBlocking);
   if (moe_status st = configure_front(desc->num_experts, desc->logit_dtype)) {
     moe_ctx_destroy(c);
     return st;
@@ -474,6 +482,13 @@ extern "C" moe_status moe_ctx_create(const moe_layer_desc* desc, int device, int
     cudaEventCreateWithFlags(&c->ev_aa[j], cudaEventDisableTiming);
     cudaEventCreateWithFlags(&c->ev_ag[j], cudaEventDisableTiming);
   }
+  c->ev_h2d.resize(size_t(desc->max_chunks));
+  c->ev_d2h.resize(size_t(desc->max_chunks));
+  for (int j = 0; j < desc->max_chunks; ++j) {
+    cudaEventCreateWithFlags(&c->ev_h2d[j], cudaEventDisableTiming);
+    cudaEventCreateWithFlags(&c->ev_d2h[j], cudaEventDisableTiming);
+  }
+  cudaEventCreateWithFlags(&c->ev_join_d2h, cudaEventDisableTiming);
   cudaEventCreate(&c->ev_base);
   cudaError_t err = cudaDeviceSynchronize();
   if (err != cudaSuccess) {
@@ -511,6 +526,11 @@ extern "C" moe_status moe_ctx_destroy(moe_ctx* c) {
   if (c->s_ag) cudaStreamDestroy(c->s_ag);
   if (c->s_d2d) cudaStreamDestroy(c->s_d2d);
   if (c->s_cap) cudaStreamDestroy(c->s_cap);
+  for (auto ev : c->ev_h2d) cudaEventDestroy(ev);
+  for (auto ev : c->ev_d2h) cudaEventDestroy(ev);
+  if (c->ev_join_d2h) cudaEventDestroy(c->ev_join_d2h);
+  if (c->s_h2d) cudaStreamDestroy(c->s_h2d);
+  if (c->s_d2h) cudaStreamDestroy(c->s_d2h);
   for (auto& g : c->graphs)
     if (g.exec) cudaGraphExecDestroy(g.exec);
   delete c;
@@ -1221,6 +1241,7 @@ moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t
   MONTA_CUDA(cudaStreamWaitEvent(c->s_ag, c->ev_fork, 0));
   MONTA_CUDA(cudaStreamWaitEvent(c->s_d2d, c->ev_fork, 0));
   for (int j = 0; j < n; ++j) {
+    if (c->pipe) MONTA_CUDA(cudaStreamWaitEvent(c->s_aa, c->ev_h2d[j], 0));  // this chunk's x is on the card
     if (moe_status st = launch_aa(c, cd, level, j, landing, c->s_aa, true)) return st;
     MONTA_CUDA(cudaEventRecord(c->ev_aa[j], c->s_aa));
     if (dedup) {
@@ -1528,14 +1549,38 @@ moe_status combine_impl(moe_ctx* c, int level, int n, cudaStream_t s) {
   MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
   MONTA_CUDA(cudaStreamWaitEvent(c->s_aa, c->ev_fork, 0));
   MONTA_CUDA(cudaStreamWaitEvent(c->s_ag, c->ev_fork, 0));
+  if (c->pipe) {
+    MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
+    MONTA_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_fork, 0));
+  }
+  const size_t crow = size_t(d.hidden) * c->ob;
+  const int64_t ct = d.tokens / n;
   for (int j = 0; j < n; ++j) {
     if (moe_status st = launch_caa(c, cd, level, j, c->s_aa, true)) return st;
     if (moe_status st = launch_unperm(c, cd, level, n, j, c->s_ag, true)) return st;
+    if (c->pipe) {  // chunk j's output rows leave for the host as soon as they are complete
+      MONTA_CUDA(cudaEventRecord(c->ev_d2h[j], c->s_ag));
+      MONTA_CUDA(cudaStreamWaitEvent(c->s_d2h, c->ev_d2h[j], 0));
+      if (dedup) {  // the TP peers' slices of chunk j (their un-permute stores into this card's out)
+        WaitList w = no_wait();
+        w.epoch_ptr = cd.epoch_dev;
+        for (int r = 0; r < d.t; ++r)
+          if (r != cd.rho) w.flags[w.n++] = flag_at(c, cd.id, sig_chunk(c, kPsCAG, j), card_of(c, cd.node, r));
+        MONTA_CUDA(launch_wait(w, cd.err, c->s_d2h));
+        ++c->launches;
+      }
+      MONTA_CUDA(cudaMemcpyAsync(c->pipe_ho + size_t(j) * ct * crow, static_cast<const char*>(cd.v.out) +
+                                 size_t(j) * ct * crow, size_t(ct) * crow, cudaMemcpyDeviceToHost, c->s_d2h));
+    }
   }
   MONTA_CUDA(cudaEventRecord(c->ev_join_aa, c->s_aa));
   MONTA_CUDA(cudaEventRecord(c->ev_join_ag, c->s_ag));
   MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_aa, 0));
   MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_ag, 0));
+  if (c->pipe) {
+    MONTA_CUDA(cudaEventRecord(c->ev_join_d2h, c->s_d2h));
+    MONTA_CUDA(cudaStreamWaitEvent(s, c->ev_join_d2h, 0));
+  }
   if (dedup) {
     WaitList w = no_wait();
     w.epoch_ptr = cd.epoch_dev;
@@ -1755,6 +1800,63 @@ moe_status experts_combine_fused(moe_ctx* c, int level, int n, cudaStream_t s) {
   return MOE_OK;
 }
 
+// forward_host on a multi-GPU rank, pipelined per token chunk: the x rows of
+// chunk j go up on their own stream while the front routes (it needs only
+// the logits), the chunk's AllToAll waits for them, and the chunk's output
+// rows go down as soon as its un-permute (and, under TP dedup, the peers'
+// slices of it) landed.  The final layout does not depend on the chunk count,
+// so the result equals the caller's schedule; the exchange runs on the
+// per-launch kernels (the persistent ones cannot wait for copies).
+bool host_pipeline_ok(const moe_ctx* c, int landing) {
+  // EP-only topologies (t == 1): under TP the 2x2 run measured no gain (4 GPUs
+  // share the host's copy bandwidth: 5.5 -> 5.1 ms, and 7.9 ms replayed as a
+  // graph) and one bench run hit an illegal address that did not reproduce
+  if (c->d.t != 1) return false;
+  if (is_virtual(c) || c->local.size() != 1 || c->timing || landing != MOE_LAND_FINAL || c->local[0].w13 ||
+      c->wire != MOE_WIRE_BF16 || c->pace_bpus || c->d.tokens <= 0)
+    return false;
+  static const int env = [] {
+    const char* e = std::getenv("MONTA_HOST_PIPE");
+    return e ? std::atoi(e) : 1;
+  }();
+  return env != 0;
+}
+
+moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
+                        cudaStream_t s);
+
+moe_status forward_host_multi(moe_ctx* c, int level, const void* hx, const void* hl, void* ho, cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  Card& cd = c->local[0];
+  int P = std::min(8, d.max_chunks);
+  while (P > 1 && d.tokens % P) --P;
+  const int64_t ct = d.tokens / P;
+  const size_t xrow = size_t(c->row_bytes);
+  MONTA_CUDA(cudaMemcpyAsync(cd.v.logits, hl, size_t(d.tokens) * d.num_experts * c->lb, cudaMemcpyHostToDevice, s));
+  MONTA_CUDA(cudaEventRecord(c->ev_fork, s));
+  MONTA_CUDA(cudaStreamWaitEvent(c->s_h2d, c->ev_fork, 0));
+  for (int j = 0; j < P; ++j) {
+    MONTA_CUDA(cudaMemcpyAsync(static_cast<char*>(cd.v.x) + size_t(j) * ct * xrow,
+                               static_cast<const char*>(hx) + size_t(j) * ct * xrow, size_t(ct) * xrow,
+                               cudaMemcpyHostToDevice, c->s_h2d));
+    MONTA_CUDA(cudaEventRecord(c->ev_h2d[j], c->s_h2d));
+  }
+  // chunked O3 with final landing (rows at their final offsets, no reorder
+  // copies): the only chunked schedule the reference's levels allow with
+  // final landing; every level's combine gives the same output rows
+  (void)level;
+  const int lv = MOE_O3;
+  const bool saved = c->use_xchg;
+  c->use_xchg = false;
+  c->pipe = true;
+  c->pipe_ho = static_cast<char*>(ho);
+  moe_status st = forward_impl(c, lv, P, MOE_LAND_FINAL, nullptr, nullptr, nullptr, s);
+  c->pipe = false;
+  c->pipe_ho = nullptr;
+  c->use_xchg = saved;
+  return st;
+}
+
 moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,
                         cudaStream_t s) {
   const moe_layer_desc& d = c->d;
@@ -1767,6 +1869,8 @@ moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* h
   const size_t xbytes = size_t(d.tokens) * c->row_bytes;
   const size_t lbytes = size_t(d.tokens) * d.num_experts * c->lb;
   const size_t obytes = size_t(d.tokens) * d.hidden * c->ob;
+  if (hx && ho && host_pipeline_ok(c, landing))
+    return forward_host_multi(c, level, hx, hl, ho, s);
   if (hx)
     for (size_t i = 0; i < c->local.size(); ++i) {
       MONTA_CUDA(cudaMemcpyAsync(c->local[i].v.x, static_cast<const char*>(hx) + i * xbytes, xbytes,

@@ -46,6 +46,7 @@ def main():
     ap.add_argument("--graphs", type=int, default=0)
     ap.add_argument("--persistent", type=int, default=1)
     ap.add_argument("--ffn", type=int, default=0)  # > 0: SwiGLU experts of this size bound on every card
+    ap.add_argument("--host", type=int, default=0)  # 1: also forward_host (pipelined host copies) vs forward
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -100,6 +101,24 @@ def main():
             layer.sync()
             results[f"overlap_same_{key}"] = np.array([bool(torch.equal(out_on, cd.out))])
             layer.set_expert_overlap(True)
+    if a.host:  # forward_host (host copies pipelined per chunk) must equal forward on device buffers
+        from paper_2411_00662_b200 import ops
+        level, n, landing = (int(v) for v in a.runs.split(",")[0].split(":"))
+        layer.forward(level, n, landing)
+        layer.sync()
+        want = cd.out.clone()
+        hx = ops.host_empty(tuple(x.shape), dt)
+        hx.copy_(x)
+        hl = ops.host_empty(tuple(logits.shape), torch.float32)
+        hl.copy_(logits)
+        ho = ops.host_empty(tuple(want.shape), want.dtype)
+        cd.out.zero_()
+        cd.x.zero_()  # forward_host must bring its own rows up
+        for _ in range(2):
+            layer.forward_host(hx, hl, ho, level, n, landing)
+        layer.sync()
+        results["host_same"] = np.array([bool(torch.equal(ho.cuda(), want))])
+        cd.x.copy_(x.cuda())
     results["experts"] = cd.experts.cpu().numpy()
     results["probs"] = cd.probs.double().cpu().numpy()
     results["x"] = x.contiguous().view(torch.uint8).numpy()

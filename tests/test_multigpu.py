@@ -31,14 +31,15 @@ def _port():
 
 
 def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0, persistent=1,
-            per_gpu=1, ffn=0):
+            per_gpu=1, ffn=0, host=0):
     world = e * t
     if torch.cuda.device_count() * per_gpu < world:
         pytest.skip(f"needs {world // per_gpu} GPUs, have {torch.cuda.device_count()}")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={world}",
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--out", str(tmp), "--groups", str(e), "--tp", str(t), "--experts", str(E), "--topk", str(k), "--tokens", str(T),
-           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs), "--persistent", str(persistent), "--ffn", str(ffn)]
+           "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs), "--persistent", str(persistent), "--ffn", str(ffn),
+           "--host", str(host)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=240 * per_gpu)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
@@ -220,3 +221,12 @@ def test_nvls_multicast_allgather(cuda, world):
     if lines and "multicast" in lines[0]:
         pytest.skip(lines[0]["multicast"])
     assert len(lines) == 2 and all(l["correct"] for l in lines), res.stdout
+
+
+@pytest.mark.parametrize("e,t,runs,graphs", [(2, 1, "0:1:0", 0), (2, 1, "0:1:0", 1), (2, 2, "1:1:0", 1)])
+def test_forward_host_pipelined_multigpu(cuda, tmp_path, e, t, runs, graphs):
+    """moe_ctx_forward_host on a multi-GPU rank (host copies pipelined per token
+    chunk on the per-launch exchange) returns the device forward's output bit for bit."""
+    ranks = _launch(tmp_path, e, t, runs=runs, T=512, h=512, graphs=graphs, host=1)
+    for r in range(e * t):
+        assert bool(ranks[r]["host_same"][0]), r
