@@ -221,3 +221,32 @@ def test_build_index_empty_slots_are_skipped(cuda):
     assert (sp[drop] == -1).all()
     for i in range(T):
         np.testing.assert_array_equal(np.sort(sp[i][sp[i] >= 0]), inv_ref[i][:il_ref[i]])
+
+
+@pytest.mark.parametrize("k,h", [(3, 8), (5, 264), (6, 5120), (8, 1032), (16, 256)])
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float16])
+def test_unpermute_any_k_with_empty_slots(cuda, k, h, dtype):
+    """The CTA-per-token un-permute (k > 2, 16-bit rows): fp32 accumulation in
+    ascending slot order, empty slots (slot_pos < 0) contribute nothing."""
+    g = torch.Generator().manual_seed(k * 1000 + h)
+    T = 301
+    R = T * k
+    y = torch.randn(R, h, generator=g).to(dtype)
+    pos = torch.randperm(R, generator=g).reshape(T, k).to(torch.int32)
+    pos[torch.rand(T, k, generator=g) < 0.2] = -1
+    p = torch.rand(T, k, generator=g)
+    out = ops.unpermute_combine(y.cuda(), pos.cuda(), p.cuda())
+    torch.cuda.synchronize()
+    want = torch.zeros(T, h, dtype=torch.float64)
+    mag = torch.zeros(T, h, dtype=torch.float64)
+    for s in range(k):
+        m = pos[:, s] >= 0
+        term = p[m, s:s + 1].double() * y[pos[m, s].long()].double()
+        want[m] += term
+        mag[m] += term.abs()
+    # one rounding to the output type (unit roundoff, with slack for fp32 sums
+    # landing next to a rounding boundary; fp16 subnormals: absolute) + fp32
+    # accumulation over k slots
+    ulp = 2.0 ** -8 if dtype == torch.bfloat16 else 2.0 ** -11
+    err = (out.cpu().double() - want).abs()
+    assert bool((err <= 1.5 * ulp * want.abs() + k * 2.0 ** -23 * mag + 2.0 ** -24).all()), float(err.max())
