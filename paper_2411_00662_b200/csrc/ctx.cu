@@ -1809,17 +1809,15 @@ moe_status experts_combine_fused(moe_ctx* c, int level, int n, cudaStream_t s) {
 // per-launch kernels (the persistent ones cannot wait for copies).
 bool host_pipeline_ok(const moe_ctx* c, int landing) {
   // EP-only topologies (t == 1): under TP the 2x2 run measured no gain (4 GPUs
-  // share the host's copy bandwidth: 5.5 -> 5.1 ms, and 7.9 ms replayed as a
-  // graph) and one bench run hit an illegal address that did not reproduce
-  if (c->d.t != 1) return false;
-  if (is_virtual(c) || c->local.size() != 1 || c->timing || landing != MOE_LAND_FINAL || c->local[0].w13 ||
-      c->wire != MOE_WIRE_BF16 || c->pace_bpus || c->d.tokens <= 0)
-    return false;
-  static const int env = [] {
+  // share the host's copy bandwidth: 5.5 -> 5.1 ms, and 7.8 ms replayed as a
+  // graph against 5.5 ms for the persistent exchange)
+  static const int env = [] {  // 0: off, 2: also under TP (diagnosis)
     const char* e = std::getenv("MONTA_HOST_PIPE");
     return e ? std::atoi(e) : 1;
   }();
-  return env != 0;
+  if (env == 0 || (c->d.t != 1 && env != 2)) return false;
+  return !(is_virtual(c) || c->local.size() != 1 || c->timing || landing != MOE_LAND_FINAL || c->local[0].w13 ||
+           c->wire != MOE_WIRE_BF16 || c->pace_bpus || c->d.tokens <= 0);
 }
 
 moe_status forward_impl(moe_ctx* c, int level, int n, int landing, const void* hx, const void* hl, void* ho,

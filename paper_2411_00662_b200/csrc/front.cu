@@ -213,14 +213,16 @@ __device__ __forceinline__ void control_tail(const FrontArgs& a, const PlanArgs&
   (void)nt;
   // chunk counts: the tile CTAs accumulated them (one atomic per tile and
   // expert) into this launch's parity buffer; the other buffer is zeroed for
-  // the next launch (every reader of it finished in the previous one)
+  // the next launch (every reader of it finished in the previous one) — all
+  // max_chunks of it: the next launch may use more chunks than this one, and
+  // a launch with fewer chunks than the one before must not leave that
+  // launch's upper chunks behind (n = 4, then 1, then 8 read stale counts)
   const int32_t* acc = a.counts_acc + size_t(epoch & 1ull) * a.max_chunks * E;
   int32_t* other = a.counts_acc + size_t((epoch + 1ull) & 1ull) * a.max_chunks * E;
   #pragma unroll 1
-  for (int q = tid; q < n * E; q += blockDim.x) {
-    cnt[q] = __ldcg(acc + q);
-    other[q] = 0;
-  }
+  for (int q = tid; q < n * E; q += blockDim.x) cnt[q] = __ldcg(acc + q);
+  #pragma unroll 1
+  for (int q = tid; q < a.max_chunks * E; q += blockDim.x) other[q] = 0;
   __syncthreads();
   #pragma unroll 1
   for (int x = tid; x < E; x += blockDim.x) {

@@ -1,5 +1,5 @@
 """forward_host (pipelined host copies) vs forward at full size on N GPUs (dev tool):
-    torchrun --nproc-per-node N scripts/host_pipe_check.py E k T h level n graphs"""
+    torchrun --nproc-per-node N scripts/host_pipe_check.py E k T h level n graphs [lv:n:landing,...]"""
 import os
 import sys
 
@@ -26,9 +26,27 @@ def main():
     lg = torch.randn(T, E, generator=g)
     cd.x.copy_(x.cuda())
     cd.logits.copy_(lg.cuda())
+    # optional warm-up schedules before the check, "lv:n:landing,..." (argv[8])
+    for spec in (sys.argv[8].split(",") if len(sys.argv) > 8 and sys.argv[8] else []):
+        lv, nn, ld = (int(v) for v in spec.split(":"))
+        for _ in range(3):
+            layer.forward(lv, nn, ld)
+        layer.sync()
+        print(f"rank {rank} warm-up {spec} ok", flush=True)
     layer.forward(level, n)
     layer.sync()
+    print(f"rank {rank} forward {level}:{n} ok", flush=True)
     want = cd.out.clone()
+    if os.environ.get("CHECK_PER_LAUNCH"):  # the per-launch exchange at O3 n=8 instead of forward_host
+        layer.set_persistent(False)
+        for i in range(3):
+            layer.forward(3, 8, 0)
+            layer.sync()
+            print(f"rank {rank} per-launch step {i}: same = {torch.equal(cd.out, want)}", flush=True)
+        dist.barrier()
+        layer.close()
+        dist.destroy_process_group()
+        return
     hx = ops.host_empty((T, h), torch.bfloat16)
     hx.copy_(x)
     hl = ops.host_empty((T, E), torch.float32)

@@ -492,3 +492,31 @@ def test_link_rate_pacing_changes_timing_not_results(cuda, level, n):
             layer.close()
     for (r0, o0), (r1, o1) in zip(*outs):
         assert torch.equal(r0, r1) and torch.equal(o0, o1)
+
+
+def test_chunk_count_sequence_matches_fresh_context(cuda):
+    """forward at n = 4, then 1, then 8 on one context gives what a fresh
+    context gives at n = 8 (the front's per-chunk count buffers are reset for
+    every chunk, not just the previous launch's)."""
+    e, t, E, k, T, h = 2, 2, 8, 2, 512, 256
+    x, logits = _inputs(e, T, h, E, torch.bfloat16, 23)
+
+    def run(seq):
+        layer = MoeLayer(e, t, E, k, T, h, dtype=torch.bfloat16, max_chunks=8)
+        try:
+            for cd in layer.cards:
+                cd.x.copy_(x[cd.node])
+                cd.logits.copy_(logits[cd.node])
+            for lv, n in seq:
+                for _ in range(3):
+                    layer.forward(lv, n)
+            layer.sync()
+            return [(cd.recv[:layer.recv_rows(cd.card)].clone(), cd.recv_tags[:layer.recv_rows(cd.card)].clone(),
+                     cd.out.clone()) for cd in layer.cards]
+        finally:
+            layer.close()
+
+    got = run([(O3, 4), (O1, 1), (O3, 8)])
+    want = run([(O3, 8)])
+    for g, w in zip(got, want):
+        assert all(torch.equal(a, b) for a, b in zip(g, w))

@@ -116,6 +116,14 @@ def test_four_gpus_2x2_per_chunk_launches(cuda, tmp_path):
     _check(_launch(tmp_path, 2, 2, runs=runs, T=512, h=512, persistent=0), 2, 2, 8, runs)
 
 
+@pytest.mark.parametrize("persistent", [1, 0])
+def test_four_gpus_2x2_chunk_count_sequence(cuda, tmp_path, persistent):
+    # more chunks after fewer after more: the front's per-chunk count buffers
+    # must not carry a previous launch's upper chunks (n = 4, 1, 8)
+    runs = "3:4:0,1:1:0,3:8:0,2:2:1"
+    _check(_launch(tmp_path, 2, 2, runs=runs, T=512, h=512, persistent=persistent), 2, 2, 8, runs)
+
+
 def test_four_gpus_2x2_deep_chunking(cuda, tmp_path):
     # many chunks through the persistent exchange (per-chunk flags in-kernel)
     runs = "3:16:0,2:8:1,3:16:1"
