@@ -186,6 +186,7 @@ SIGNATURES = {
     "moe_ctx_bind_experts": (C.c_int, [_P, C.c_int, _P, _P, _I64]),
     "moe_ctx_experts": (C.c_int, [_P, _P]),
     "moe_ctx_set_expert_overlap": (C.c_int, [_P, C.c_int32]),
+    "moe_ctx_set_node_dedup": (C.c_int, [_P, C.c_int32]),
     "moe_comm_priority": (C.c_int, [C.c_int]),
     "moe_ctx_enable_checks": (C.c_int, [_P, C.c_int]),
     "moe_ctx_set_wire": (C.c_int, [_P, C.c_int]),

@@ -31,7 +31,7 @@ namespace {
 constexpr int kTokThreads = 256;
 constexpr int kTokMaxK = 16;
 
-template <int V>
+template <int V, bool ND = false>
 __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_constant__ TokArgs a) {
   using Vec = typename VecT<V>::type;
   constexpr int U = 64 / V > 4 ? 4 : (64 / V < 1 ? 1 : 64 / V);  // 16-byte vectors: 4 per lane (2 KiB pieces)
@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
     char* qp = nullptr;   // fp8 wire: e4m3 row on the receiver (cross-node legs)
     float* sp = nullptr;  //           its per-128-element scales
     int off = 0, end = 0;
+    int rcard = -1;       // node dedup: the remote card this lane's row would cross to
     if (lane < k) {
       const int64_t q = i * k + lane;
       const int x = __ldg(a.experts + q);
@@ -62,14 +63,26 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
         const int64_t row = int64_t(base) + p;
         off = __ldg(a.table + 2 * E + x);
         end = off + __ldg(a.table + 3 * E + x);
-        dp = a.dst[card] + row * a.dst_stride;
-        if (a.fp8 && card / a.t != a.node) {
-          qp = a.dst_pre[card] + row * a.dst_stride;
-          sp = a.dst_scale[card] + row * a.blocks_per_row;
+        if (ND && card / a.t != a.node) {
+          rcard = card;  // staged below, once per (token, card); the receiver writes the tags
+        } else {
+          dp = a.dst[card] + row * a.dst_stride;
+          if (a.fp8 && card / a.t != a.node) {
+            qp = a.dst_pre[card] + row * a.dst_stride;
+            sp = a.dst_scale[card] + row * a.blocks_per_row;
+          }
+          if (v0 == 0 && a.dst_tags[card])
+            *reinterpret_cast<int4*>(a.dst_tags[card] + 4 * row) = make_int4(__ldg(a.token_ids + i), a.source_card,
+                                                                               int(i), x);
         }
-        if (v0 == 0 && a.dst_tags[card])
-          *reinterpret_cast<int4*>(a.dst_tags[card] + 4 * row) = make_int4(__ldg(a.token_ids + i), a.source_card,
-                                                                             int(i), x);
+      }
+    }
+    if constexpr (ND) {  // node dedup
+      const unsigned same = __match_any_sync(0xffffffffu, rcard);
+      if (rcard >= 0 && (same & ((1u << lane) - 1u)) == 0) {  // the token's first slot on that card
+        dp = a.stage[rcard] + int64_t(__ldg(a.nslot + i * a.e + rcard / a.t)) * a.dst_stride;
+        off = 0;
+        end = int(a.row_bytes);
       }
     }
     const Vec* src = reinterpret_cast<const Vec*>(a.x + i * a.row_bytes);
@@ -237,6 +250,93 @@ __global__ void __launch_bounds__(32) k_aa_bulk(const __grid_constant__ TokArgs 
   cta_signal(a.sig);
 }
 
+// Node dedup, sender pre-pass: thread per token; per remote node, the warp's
+// tokens that reach it claim consecutive staging slots with one atomic, and
+// each writes its descriptor {token id, position, k destination rows (-1:
+// not on that node), k experts} into the receiver's block for this node.
+__global__ void __launch_bounds__(256) k_node_slots(const __grid_constant__ NodeSlotArgs a) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
+  const int64_t Tr = (a.T + 31) / 32 * 32;
+  const int k = a.k, E = a.E;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Tr; i += nthreads) {
+    const bool active = i < a.T;
+    for (int g = 0; g < a.e; ++g) {
+      if (g == a.node) continue;
+      const int card = g * a.t;  // EP only (t == 1): node g's card
+      bool has = false;
+      if (active)
+        for (int s = 0; s < k; ++s) {
+          const int x = __ldg(a.experts + i * k + s);
+          has |= x >= 0 && x < E && __ldg(a.table + x) == card;
+        }
+      const unsigned bal = __ballot_sync(0xffffffffu, has);
+      if (!bal) continue;
+      int base = 0;
+      if (lane == 0) base = int(atomicAdd(a.scount + card, uint32_t(__popc(bal))));
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (!has) continue;
+      const int slot = base + __popc(bal & ((1u << lane) - 1u));
+      a.nslot[i * a.e + g] = slot;
+      int32_t* d = a.sdesc[card] + int64_t(slot) * (2 + 2 * k);
+      d[0] = __ldg(a.token_ids + i);
+      d[1] = int32_t(i);
+      for (int s = 0; s < k; ++s) {
+        const int x = __ldg(a.experts + i * k + s);
+        const bool on = x >= 0 && x < E && __ldg(a.table + x) == card;
+        d[2 + s] = on ? __ldg(a.table + E + x) + __ldg(a.slot_pos + i * k + s) : -1;
+        d[2 + k + s] = x;
+      }
+    }
+  }
+}
+
+// Node dedup, receiver: warp per (staged row, 2 KiB piece) of every remote
+// sender (blockIdx.y); the piece is loaded once and stored to each of its
+// destination rows on this card, tags written with the first piece.
+__global__ void __launch_bounds__(256) k_node_fanout(const __grid_constant__ FanoutArgs a) {
+  constexpr int U = 4;
+  constexpr int kPieceVec = 32 * U;
+  const int lane = threadIdx.x & 31;
+  const int y = blockIdx.y;
+  const int64_t cnt = int64_t(*a.count[y]);
+  const int64_t nvec = a.row_bytes / 16;
+  const int64_t pieces = (nvec + kPieceVec - 1) / kPieceVec;
+  const int k = a.k;
+  const int dw = 2 + 2 * k;
+  const uint64_t pol = l2_evict_first_policy();
+  const int64_t warps = int64_t(gridDim.x) * (blockDim.x / 32);
+  for (int64_t it = int64_t(blockIdx.x) * (blockDim.x / 32) + (threadIdx.x >> 5); it < cnt * pieces; it += warps) {
+    const int64_t q = it / pieces;
+    const int64_t v0 = (it % pieces) * kPieceVec;
+    const int32_t* d = a.sdesc[y] + q * dw;
+    int row = -1;
+    if (lane < k) {
+      row = __ldg(d + 2 + lane);
+      if (v0 == 0 && row >= 0)
+        *reinterpret_cast<int4*>(a.recv_tags + 4 * int64_t(row)) =
+            make_int4(__ldg(d), a.source_card[y], __ldg(d + 1), __ldg(d + 2 + k + lane));
+    }
+    const int4* src = reinterpret_cast<const int4*>(a.stage[y] + q * a.row_bytes);
+    int4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + u * 32 + lane;
+      if (v < nvec) r[u] = ld_stream_ef(src + v, pol);
+    }
+    for (int s = 0; s < k; ++s) {
+      const int rs = __shfl_sync(0xffffffffu, row, s);
+      if (rs < 0) continue;
+      int4* dst = reinterpret_cast<int4*>(a.recv + int64_t(rs) * a.row_bytes);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + u * 32 + lane;
+        if (v < nvec) dst[v] = r[u];
+      }
+    }
+  }
+}
+
 // fp8 wire receive: thread per 8 columns of a row that came cross-node.
 __global__ void __launch_bounds__(256) k_wire_dequant(char* __restrict__ recv, const int32_t* __restrict__ tags,
                                                       const int64_t* __restrict__ recv_rows, const char* __restrict__ pre,
@@ -400,6 +500,27 @@ static int env_int(const char* name, int dflt) {
   return e && *e ? std::atoi(e) : dflt;
 }
 
+cudaError_t launch_node_slots(const NodeSlotArgs& a, cudaStream_t s) {
+  if (a.T <= 0) return cudaSuccess;
+  const int64_t threads = (a.T + 31) / 32 * 32;
+  const int grid = int(std::min<int64_t>((threads + 255) / 256, 148 * 8));
+  k_node_slots<<<grid, 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_node_fanout(const FanoutArgs& a, int64_t max_rows, int vec, cudaStream_t s) {
+  if (a.nsend <= 0 || max_rows <= 0) return cudaSuccess;
+  if (vec != 16 || a.row_bytes % 16) return cudaErrorNotSupported;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t pieces = (a.row_bytes / 16 + 127) / 128;
+  const int64_t items = max_rows * pieces;
+  const int gx = int(std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, int64_t(sms) * 4 / a.nsend + 1)));
+  k_node_fanout<<<dim3(gx, a.nsend), 256, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s) {
   if (a.k > kTokMaxK) return cudaErrorNotSupported;
   static const int bulk = env_int("MONTA_AA_BULK", 1);
@@ -433,6 +554,11 @@ cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s)
     const int g = int(std::max<int64_t>(1, std::min<int64_t>(toks, int64_t(sms) * cps)));
     apply_carveout(k_aa_bulk);
     k_aa_bulk<<<g, 32, smem, s>>>(a, stages, depth);
+    return cudaGetLastError();
+  }
+  if (a.nslot) {  // node dedup (16-byte rows only)
+    if (vec != 16) return cudaErrorNotSupported;
+    k_aa_token<16, true><<<grid, kTokThreads, 0, s>>>(a);
     return cudaGetLastError();
   }
   switch (vec) {

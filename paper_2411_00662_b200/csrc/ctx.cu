@@ -48,6 +48,9 @@ struct PeerPtrs {
   float* wscale = nullptr;          // [recv_cap][h / 128] fp8 wire scales
   char* cwire = nullptr;            // [R][h] fp8 combine leg rows
   float* cscale = nullptr;          // [R][h / 128]
+  char* stage = nullptr;            // node dedup: [e][T] staged rows, block g from sender node g
+  int32_t* sdesc = nullptr;         //             [e][T][2 + 2k] their descriptors
+  uint32_t* scount = nullptr;       //             [kMaxCards] rows this card staged to each card
 };
 
 // Byte offsets of every buffer inside a card's slab.  Identical on every
@@ -57,7 +60,7 @@ struct SlabLayout {
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
   size_t lists, local_delta, recv_rows, recv_offs, tune, prow, rowpos, rowslot, dot, parts, gprobs, glogits, ones,
       wscale, cwire, cscale, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
-      ready, xchg_counters, xchg_flags, xtrace, aa_table, rowdst, total;
+      ready, xchg_counters, xchg_flags, xtrace, aa_table, rowdst, stage, sdesc, scount, nslot, total;
 };
 
 struct Card {
@@ -84,6 +87,7 @@ struct Card {
   unsigned long long* xtrace = nullptr;  // [2 kernels][4 roles][max_chunks][2] role trace (ns)
   int32_t* aa_table = nullptr;        // [4 + max_chunks][E] token-side AA destinations
   char** rowdst = nullptr;            // [recv_cap] reverse-AllToAll row address (peer comb) or null
+  int32_t* nslot = nullptr;           // node dedup: [T][e] staging slot of (token, remote node), -1 none
   unsigned* front_done = nullptr;  // CTA election counter of the front kernel
   // layer backward scratch (moe_ctx_backward)
   void* prow = nullptr;
@@ -128,6 +132,8 @@ struct moe_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join_aa = nullptr, ev_join_ag = nullptr, ev_join_d2d = nullptr;
   std::vector<cudaEvent_t> ev_aa, ev_ag;
   bool expert_fused = true;  // moe_ctx_set_expert_overlap: down-projection epilogue issues the reverse AllToAll
+  bool node_dedup_now = false;  // set by dispatch_node_dedup for its launch_aa
+  bool node_dedup = true;       // moe_ctx_set_node_dedup
   int aa_ctas = 0;
   bool combine_ready = false;  // a dispatch whose combine has not run yet
   bool debug = false;          // record front-kernel phase timestamps
@@ -231,6 +237,12 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.xtrace = take(size_t(2) * 4 * d.max_chunks * 2 * 8);
   s.aa_table = take(size_t(4 + d.max_chunks) * E * 4);
   s.rowdst = take(size_t(c->recv_cap) * 8);  // fused combine: each landed row's reverse-AllToAll destination
+  // node dedup (EP only): a token's row crosses to a remote node once
+  const bool nd = d.t == 1 && d.e > 1 && c->world > 1;
+  s.stage = take(nd ? size_t(d.e) * T * c->row_bytes : 0);
+  s.sdesc = take(nd ? size_t(d.e) * T * (2 + 2 * k) * 4 : 0);
+  s.scount = take(size_t(kMaxCards) * 4);
+  s.nslot = take(nd ? size_t(T) * d.e * 4 : 0);
   s.total = off;
   return s;
 }
@@ -289,6 +301,7 @@ void bind_card(moe_ctx* c, Card& cd) {
   cd.xtrace = reinterpret_cast<unsigned long long*>(b + s.xtrace);
   cd.aa_table = reinterpret_cast<int32_t*>(b + s.aa_table);
   cd.rowdst = reinterpret_cast<char**>(b + s.rowdst);
+  cd.nslot = reinterpret_cast<int32_t*>(b + s.nslot);
 }
 
 void set_peer(moe_ctx* c, int card, char* slab) {
@@ -309,6 +322,9 @@ void set_peer(moe_ctx* c, int card, char* slab) {
   p.wscale = reinterpret_cast<float*>(slab + s.wscale);
   p.cwire = slab + s.cwire;
   p.cscale = reinterpret_cast<float*>(slab + s.cscale);
+  p.stage = slab + s.stage;
+  p.sdesc = reinterpret_cast<int32_t*>(slab + s.sdesc);
+  p.scount = reinterpret_cast<uint32_t*>(slab + s.scount);
 }
 
 inline int card_of(const moe_ctx* c, int node, int rho) { return node * c->d.t + rho; }
@@ -671,6 +687,8 @@ moe_status do_route(moe_ctx* c, cudaStream_t s) {
 
 bool xchg_eligible(moe_ctx* c, int level);
 
+bool node_dedup_ok(const moe_ctx* c, int level, int n, int landing);
+
 PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
   const moe_layer_desc& d = c->d;
   PlanArgs a{};
@@ -689,9 +707,10 @@ PlanArgs make_plan_args(moe_ctx* c, Card& cd, int level, int n, int landing) {
   a.seg_cap = d.num_experts;
   a.lists = cd.lists;
   a.local_delta = cd.local_delta;
-  // the per-expert destination table feeds only the token-side AA kernel;
-  // the persistent exchange reads the segment lists instead
-  a.aa_table = xchg_eligible(c, level) ? nullptr : cd.aa_table;
+  // the per-expert destination table feeds only the token-side AA kernel
+  // (per-launch path and node dedup); the persistent exchange reads the
+  // segment lists instead
+  a.aa_table = xchg_eligible(c, level) && !node_dedup_ok(c, level, n, landing) ? nullptr : cd.aa_table;
   a.recv_rows = cd.recv_rows;
   a.recv_offs = cd.v.recv_expert_offsets;
   a.err = cd.err;
@@ -848,6 +867,12 @@ moe_status launch_aa(moe_ctx* c, Card& cd, int level, int j, int landing, cudaSt
         if (x != cd.node) t.sig.flags[t.sig.n++] = flag_at(c, card_of(c, x, cd.rho), sig_chunk(c, kPsAA, j), cd.id);
     t.err = cd.err;
     t.local_dst = is_virtual(c) ? 1 : 0;
+    if (c->node_dedup_now) {
+      t.nslot = cd.nslot;
+      t.e = d.e;
+      for (int q = 0; q < c->cards; ++q)
+        if (c->peer[q].slab) t.stage[q] = c->peer[q].stage + size_t(cd.node) * d.tokens * c->row_bytes;
+    }
     // four resident CTAs (32 warps) per SM, at most one item (token x 2 KiB piece) per warp
     const int64_t items = ct * ((c->row_bytes + 2047) / 2048);
     int grid = int(std::min<int64_t>((items + 7) / 8, int64_t(c->sms) * (concurrent ? 2 : 4)));
@@ -1194,6 +1219,76 @@ extern "C" moe_status moe_ctx_permute(moe_ctx* c, int32_t n, void* stream) {
 
 namespace {
 
+// Node dedup for EP-only topologies (t == 1): with k slots spread over e
+// nodes a token reaches several experts on one remote node, and the plain
+// AllToAll sends its row once per such expert.  Here it crosses once per
+// (token, remote node): k_node_slots claims a staging slot on the receiver
+// (one atomic per warp and node) and writes the slot's descriptor (token id,
+// position, the k destination rows on that node, the experts); the token
+// kernel stores own-node rows as before and each remote row once into the
+// receiver's staging block; after the chunk flags the receiver's
+// k_node_fanout copies every staged row to its destination rows and writes
+// their tags.  The recv layout is the plain dispatch's, row for row.
+bool node_dedup_ok(const moe_ctx* c, int level, int n, int landing) {
+  (void)level;
+  static const int env = [] {  // MONTA_NODE_DEDUP=0 overrides (A/B)
+    const char* e = std::getenv("MONTA_NODE_DEDUP");
+    return e ? std::atoi(e) : 1;
+  }();
+  const moe_layer_desc& d = c->d;
+  return env != 0 && c->node_dedup && !is_virtual(c) && d.t == 1 && d.e > 1 && n == 1 && landing == MOE_LAND_FINAL &&
+         c->wire == MOE_WIRE_BF16 && !c->pace_bpus && c->aa_ctas == 0 && d.top_k <= 16 && c->row_bytes % 16 == 0 &&
+         c->local.size() == 1;  // (the staging regions exist exactly when t == 1, e > 1 and world > 1)
+}
+
+moe_status dispatch_node_dedup(moe_ctx* c, Card& cd, int level, int landing, cudaStream_t s) {
+  const moe_layer_desc& d = c->d;
+  const int dw = 2 + 2 * d.top_k;
+  MONTA_CUDA(cudaMemsetAsync(c->peer[cd.id].scount, 0, size_t(kMaxCards) * 4, s));
+  NodeSlotArgs ns{};
+  ns.experts = cd.v.experts;
+  ns.slot_pos = cd.v.slot_pos;
+  ns.token_ids = cd.v.token_ids;
+  ns.table = cd.aa_table;
+  ns.T = d.tokens;
+  ns.E = d.num_experts;
+  ns.k = d.top_k;
+  ns.e = d.e;
+  ns.t = d.t;
+  ns.node = cd.node;
+  ns.scount = c->peer[cd.id].scount;
+  ns.nslot = cd.nslot;
+  for (int g = 0; g < d.e; ++g)
+    if (g != cd.node) {
+      const int q = card_of(c, g, 0);
+      ns.sdesc[q] = c->peer[q].sdesc + size_t(cd.node) * d.tokens * dw;
+    }
+  MONTA_CUDA(launch_node_slots(ns, s));
+  ++c->launches;
+  c->node_dedup_now = true;
+  moe_status st = launch_aa(c, cd, level, 0, landing, s, false);
+  c->node_dedup_now = false;
+  if (st != MOE_OK) return st;
+  if (moe_status st2 = dispatch_tail_wait(c, cd, level, 1, landing, s)) return st2;
+  FanoutArgs fa{};
+  for (int g = 0; g < d.e; ++g) {
+    if (g == cd.node) continue;
+    const int q = card_of(c, g, 0);
+    const int i = fa.nsend++;
+    fa.stage[i] = c->peer[cd.id].stage + size_t(g) * d.tokens * c->row_bytes;
+    fa.sdesc[i] = c->peer[cd.id].sdesc + size_t(g) * d.tokens * dw;
+    fa.count[i] = c->peer[q].scount + cd.id;
+    fa.source_card[i] = q;
+  }
+  fa.row_bytes = c->row_bytes;
+  fa.k = d.top_k;
+  fa.recv = static_cast<char*>(cd.v.recv);
+  fa.recv_tags = cd.v.recv_tags;
+  MONTA_CUDA(launch_node_fanout(fa, d.tokens, 16, s));
+  ++c->launches;
+  return MOE_OK;
+}
+
 moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t s, bool route) {
   const moe_layer_desc& d = c->d;
   if (level == MOE_BASELINE) landing = MOE_LAND_FINAL;
@@ -1230,6 +1325,7 @@ moe_status dispatch_impl(moe_ctx* c, int level, int n, int landing, cudaStream_t
   // AllGather on its own stream, reorder copies on the AllGather stream (O2)
   // or their own (O3).
   Card& cd = c->local[0];
+  if (node_dedup_ok(c, level, n, landing)) return dispatch_node_dedup(c, cd, level, landing, s);
   if (c->use_xchg) {
     bool done = false;
     if (moe_status st = launch_dispatch_xchg(c, cd, level, n, landing, s, &done)) return st;
@@ -2388,6 +2484,18 @@ extern "C" moe_status moe_ctx_debug_front(moe_ctx* c, int enable, int card, uint
       return MOE_OK;
     }
   return fail(MOE_ERR_INVALID_ARGUMENT, "debug_front: card %d is not local", card);
+}
+
+extern "C" moe_status moe_ctx_set_node_dedup(moe_ctx* c, int32_t enable) {
+  if (!c) return fail(MOE_ERR_INVALID_ARGUMENT, "set_node_dedup: null ctx");
+  if (c->node_dedup != (enable != 0)) {
+    MONTA_CUDA(cudaSetDevice(c->device));
+    for (auto& g : c->graphs)
+      if (g.exec) cudaGraphExecDestroy(g.exec);
+    c->graphs.clear();
+  }
+  c->node_dedup = enable != 0;
+  return MOE_OK;
 }
 
 extern "C" moe_status moe_ctx_set_expert_overlap(moe_ctx* c, int32_t enable) {

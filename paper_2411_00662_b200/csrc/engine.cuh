@@ -131,7 +131,38 @@ struct TokArgs {
   // every destination is in this GPU's own memory (a lone card, or virtual
   // cards on one GPU): the TMA bulk-copy form may run (aa.cu k_aa_bulk)
   int32_t local_dst;
+  // node dedup (EP only): a remote card gets the token's row once, into its
+  // staging block for this node at slot nslot[i * e + node]; the receiver
+  // fans it out (k_node_fanout).  null: every (token, expert) row crosses.
+  const int32_t* nslot;
+  int32_t e;
+  char* stage[kMaxCards];
 };
+// Node dedup: staging slots + descriptors (sender), fan-out (receiver).
+struct NodeSlotArgs {
+  const int32_t* experts;    // [T, k]
+  const int32_t* slot_pos;   // [T, k]
+  const int32_t* token_ids;  // [T]
+  const int32_t* table;      // aa_table: [0, E) card, [E, 2E) row base
+  int64_t T;
+  int32_t E, k, e, t, node;
+  uint32_t* scount;          // this card's [kMaxCards] staged-row counters (zeroed per dispatch)
+  int32_t* nslot;            // [T][e]
+  int32_t* sdesc[kMaxCards]; // each card's descriptor block for this node
+};
+cudaError_t launch_node_slots(const NodeSlotArgs& a, cudaStream_t s);
+struct FanoutArgs {
+  int32_t nsend;                     // remote senders
+  const char* stage[kMaxCards];      // this card's staging block of sender i
+  const int32_t* sdesc[kMaxCards];   // its descriptors
+  const uint32_t* count[kMaxCards];  // rows sender i staged to this card (sender's scount[this card])
+  int32_t source_card[kMaxCards];
+  int64_t row_bytes;
+  int32_t k;
+  char* recv;
+  int32_t* recv_tags;
+};
+cudaError_t launch_node_fanout(const FanoutArgs& a, int64_t max_rows, int vec, cudaStream_t s);
 // Fused combine (experts.cu + ctx.cu): rowdst[r] = the address of final-layout
 // row r's reverse-AllToAll destination row (a peer's comb) from the CAA lists
 // of chunks [0, n), null for rows that stay on this node.

@@ -221,6 +221,10 @@ class MoeLayer:
     def experts(self, stream=None) -> None:
         check(self.lib.moe_ctx_experts(self._ctx, _stream_ptr(stream)))
 
+    def set_node_dedup(self, enable: bool) -> None:
+        """EP-only: send a token's row once per remote node (fanned out there); False: once per (token, expert)."""
+        check(self.lib.moe_ctx_set_node_dedup(self._ctx, int(bool(enable))))
+
     def set_expert_overlap(self, enable: bool) -> None:
         """Fuse the reverse AllToAll into the experts' down-projection epilogue (multi-GPU forward)."""
         check(self.lib.moe_ctx_set_expert_overlap(self._ctx, int(bool(enable))))

@@ -31,7 +31,7 @@ def _port():
 
 
 def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=0, graphs=0, persistent=1,
-            per_gpu=1, ffn=0, host=0):
+            per_gpu=1, ffn=0, host=0, node_dedup=1):
     world = e * t
     if torch.cuda.device_count() * per_gpu < world:
         pytest.skip(f"needs {world // per_gpu} GPUs, have {torch.cuda.device_count()}")
@@ -39,7 +39,7 @@ def _launch(tmp, e, t, E=8, k=2, T=256, h=256, runs="0:1:0", dtype="bf16", seed=
            "--master-addr=127.0.0.1", f"--master-port={_port()}", os.path.join(ROOT, "tests", "mp_worker.py"),
            "--out", str(tmp), "--groups", str(e), "--tp", str(t), "--experts", str(E), "--topk", str(k), "--tokens", str(T),
            "--hidden", str(h), "--runs", runs, "--dtype", dtype, "--seed", str(seed), "--graphs", str(graphs), "--persistent", str(persistent), "--ffn", str(ffn),
-           "--host", str(host)]
+           "--host", str(host), "--node-dedup", str(node_dedup)]
     res = subprocess.run(cmd, capture_output=True, text=True, timeout=240 * per_gpu)
     assert res.returncode == 0, res.stdout[-3000:] + res.stderr[-3000:]
     return [dict(np.load(os.path.join(tmp, f"rank{r}.npz"))) for r in range(world)]
@@ -82,6 +82,12 @@ def _check(ranks, e, t, E, runs, elem=2):
 def test_two_gpus_ep2(cuda, tmp_path):
     runs = "0:1:0"
     _check(_launch(tmp_path, 2, 1, runs=runs), 2, 1, 8, runs)
+
+
+def test_two_gpus_ep2_without_node_dedup(cuda, tmp_path):
+    # the plain cross-node AllToAll (one row per (token, expert)), node dedup off
+    runs = "0:1:0"
+    _check(_launch(tmp_path, 2, 1, runs=runs, node_dedup=0), 2, 1, 8, runs)
 
 
 def test_two_gpus_tp2(cuda, tmp_path):
