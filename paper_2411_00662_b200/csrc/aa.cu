@@ -80,9 +80,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
     if constexpr (ND) {  // node dedup
       const unsigned same = __match_any_sync(0xffffffffu, rcard);
       if (rcard >= 0 && (same & ((1u << lane) - 1u)) == 0) {  // the token's first slot on that card
-        dp = a.stage[rcard] + int64_t(__ldg(a.nslot + i * a.e + rcard / a.t)) * a.dst_stride;
-        off = 0;
-        end = int(a.row_bytes);
+        dp = a.stage[rcard] + int64_t(__ldg(a.nslot + i * a.e + rcard / a.t)) * a.dst_stride;  // same window
       }
     }
     const Vec* src = reinterpret_cast<const Vec*>(a.x + i * a.row_bytes);
@@ -263,7 +261,7 @@ __global__ void __launch_bounds__(256) k_node_slots(const __grid_constant__ Node
     const bool active = i < a.T;
     for (int g = 0; g < a.e; ++g) {
       if (g == a.node) continue;
-      const int card = g * a.t;  // EP only (t == 1): node g's card
+      const int card = g * a.t + a.rho;  // node g's card of this rank's TP index
       bool has = false;
       if (active)
         for (int s = 0; s < k; ++s) {
@@ -317,12 +315,13 @@ __global__ void __launch_bounds__(256) k_node_fanout(const __grid_constant__ Fan
         *reinterpret_cast<int4*>(a.recv_tags + 4 * int64_t(row)) =
             make_int4(__ldg(d), a.source_card[y], __ldg(d + 1), __ldg(d + 2 + k + lane));
     }
+    if (v0 * 16 + kPieceVec * 16 <= a.col_lo || v0 * 16 >= a.col_hi) continue;  // piece outside the window
     const int4* src = reinterpret_cast<const int4*>(a.stage[y] + q * a.row_bytes);
     int4 r[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int64_t v = v0 + u * 32 + lane;
-      if (v < nvec) r[u] = ld_stream_ef(src + v, pol);
+      if (v < nvec && v * 16 >= a.col_lo && v * 16 < a.col_hi) r[u] = ld_stream_ef(src + v, pol);
     }
     for (int s = 0; s < k; ++s) {
       const int rs = __shfl_sync(0xffffffffu, row, s);
@@ -331,7 +330,7 @@ __global__ void __launch_bounds__(256) k_node_fanout(const __grid_constant__ Fan
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int64_t v = v0 + u * 32 + lane;
-        if (v < nvec) dst[v] = r[u];
+        if (v < nvec && v * 16 >= a.col_lo && v * 16 < a.col_hi) dst[v] = r[u];
       }
     }
   }

@@ -237,8 +237,8 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.xtrace = take(size_t(2) * 4 * d.max_chunks * 2 * 8);
   s.aa_table = take(size_t(4 + d.max_chunks) * E * 4);
   s.rowdst = take(size_t(c->recv_cap) * 8);  // fused combine: each landed row's reverse-AllToAll destination
-  // node dedup (EP only): a token's row crosses to a remote node once
-  const bool nd = d.t == 1 && d.e > 1 && c->world > 1;
+  // node dedup: a token's row (slice under TP) crosses to a remote node once
+  const bool nd = d.e > 1 && c->world > 1;
   s.stage = take(nd ? size_t(d.e) * T * c->row_bytes : 0);
   s.sdesc = take(nd ? size_t(d.e) * T * (2 + 2 * k) * 4 : 0);
   s.scount = take(size_t(kMaxCards) * 4);
@@ -1230,13 +1230,16 @@ namespace {
 // k_node_fanout copies every staged row to its destination rows and writes
 // their tags.  The recv layout is the plain dispatch's, row for row.
 bool node_dedup_ok(const moe_ctx* c, int level, int n, int landing) {
-  (void)level;
   static const int env = [] {  // MONTA_NODE_DEDUP=0 overrides (A/B)
     const char* e = std::getenv("MONTA_NODE_DEDUP");
     return e ? std::atoi(e) : 1;
   }();
   const moe_layer_desc& d = c->d;
-  return env != 0 && c->node_dedup && !is_virtual(c) && d.t == 1 && d.e > 1 && n == 1 && landing == MOE_LAND_FINAL &&
+  // under TP only the deduplicated levels (each rank's slice crosses to the
+  // same-rank card, the AllGather forwards it); the naive level at t > 1
+  // keeps the reference's full-row exchange
+  if (d.t > 1 && level == MOE_BASELINE) return false;
+  return env != 0 && c->node_dedup && !is_virtual(c) && d.e > 1 && n == 1 && landing == MOE_LAND_FINAL &&
          c->wire == MOE_WIRE_BF16 && !c->pace_bpus && c->aa_ctas == 0 && d.top_k <= 16 && c->row_bytes % 16 == 0 &&
          c->local.size() == 1;  // (the staging regions exist exactly when t == 1, e > 1 and world > 1)
 }
@@ -1256,11 +1259,12 @@ moe_status dispatch_node_dedup(moe_ctx* c, Card& cd, int level, int landing, cud
   ns.e = d.e;
   ns.t = d.t;
   ns.node = cd.node;
+  ns.rho = cd.rho;
   ns.scount = c->peer[cd.id].scount;
   ns.nslot = cd.nslot;
   for (int g = 0; g < d.e; ++g)
     if (g != cd.node) {
-      const int q = card_of(c, g, 0);
+      const int q = card_of(c, g, cd.rho);
       ns.sdesc[q] = c->peer[q].sdesc + size_t(cd.node) * d.tokens * dw;
     }
   MONTA_CUDA(launch_node_slots(ns, s));
@@ -1269,23 +1273,37 @@ moe_status dispatch_node_dedup(moe_ctx* c, Card& cd, int level, int landing, cud
   moe_status st = launch_aa(c, cd, level, 0, landing, s, false);
   c->node_dedup_now = false;
   if (st != MOE_OK) return st;
-  if (moe_status st2 = dispatch_tail_wait(c, cd, level, 1, landing, s)) return st2;
+  const bool dedup = d.t > 1;  // (node_dedup_ok: a deduplicated level under TP)
+  {  // every remote sender's rows (this rank's slice under TP) are staged here
+    WaitList w = no_wait();
+    w.epoch_ptr = cd.epoch_dev;
+    for (int g = 0; g < d.e; ++g)
+      if (g != cd.node) w.flags[w.n++] = flag_at(c, cd.id, sig_chunk(c, kPsAA, 0), card_of(c, g, cd.rho));
+    MONTA_CUDA(launch_wait(w, cd.err, s));
+    ++c->launches;
+  }
   FanoutArgs fa{};
   for (int g = 0; g < d.e; ++g) {
     if (g == cd.node) continue;
-    const int q = card_of(c, g, 0);
+    const int q = card_of(c, g, cd.rho);
     const int i = fa.nsend++;
     fa.stage[i] = c->peer[cd.id].stage + size_t(g) * d.tokens * c->row_bytes;
     fa.sdesc[i] = c->peer[cd.id].sdesc + size_t(g) * d.tokens * dw;
     fa.count[i] = c->peer[q].scount + cd.id;
-    fa.source_card[i] = q;
+    fa.source_card[i] = card_of(c, g, 0);  // the tag names the source node's first card (as the token kernel does)
   }
   fa.row_bytes = c->row_bytes;
+  fa.col_lo = dedup ? int64_t(cd.rho) * (c->row_bytes / d.t) : 0;
+  fa.col_hi = dedup ? fa.col_lo + c->row_bytes / d.t : c->row_bytes;
   fa.k = d.top_k;
   fa.recv = static_cast<char*>(cd.v.recv);
   fa.recv_tags = cd.v.recv_tags;
   MONTA_CUDA(launch_node_fanout(fa, d.tokens, 16, s));
   ++c->launches;
+  if (dedup) {  // forward this rank's landed slices to the node's TP peers, then wait for theirs
+    if (moe_status st3 = launch_ag(c, cd, 0, landing, s, false)) return st3;
+    if (moe_status st4 = dispatch_tail_wait(c, cd, level, 1, landing, s)) return st4;
+  }
   return MOE_OK;
 }
 

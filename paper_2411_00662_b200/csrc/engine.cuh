@@ -145,7 +145,7 @@ struct NodeSlotArgs {
   const int32_t* token_ids;  // [T]
   const int32_t* table;      // aa_table: [0, E) card, [E, 2E) row base
   int64_t T;
-  int32_t E, k, e, t, node;
+  int32_t E, k, e, t, node, rho;
   uint32_t* scount;          // this card's [kMaxCards] staged-row counters (zeroed per dispatch)
   int32_t* nslot;            // [T][e]
   int32_t* sdesc[kMaxCards]; // each card's descriptor block for this node
@@ -158,6 +158,7 @@ struct FanoutArgs {
   const uint32_t* count[kMaxCards];  // rows sender i staged to this card (sender's scount[this card])
   int32_t source_card[kMaxCards];
   int64_t row_bytes;
+  int64_t col_lo, col_hi;            // byte window of a row this card owns (its 1/t slice under TP)
   int32_t k;
   char* recv;
   int32_t* recv_tags;
