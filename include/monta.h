@@ -353,12 +353,13 @@ moe_status moe_ctx_experts(moe_ctx* ctx, void* stream);
  * one kernel.  enable = 0: experts, then the combine's own AllToAll.
  * Default on.  Results are identical either way. */
 moe_status moe_ctx_set_expert_overlap(moe_ctx* ctx, int32_t enable);
-/* Node dedup of the cross-node AllToAll on EP-only topologies (t == 1,
- * unchunked, final landing, bf16 wire): a token's row crosses to a remote
- * node once, however many of its experts live there, into a staging block
- * the receiver fans out to the experts' rows (the recv layout and tags are
- * the plain dispatch's, row for row).  Default on; 0 sends one row per
- * (token, expert) as the reference's dispatch_monolithic does. */
+/* Node dedup of the cross-node AllToAll (multi-GPU, unchunked, final
+ * landing, bf16 wire; EP-only, or a TP-deduplicated level): a token's row
+ * (this rank's 1/t slice under TP) crosses to a remote node once, however
+ * many of its experts live there, into a staging block the receiving card
+ * fans out to the experts' rows before the AllGather (the recv layout and
+ * tags are the plain dispatch's, row for row).  Default on; 0 sends one row
+ * per (token, expert) as the reference's dispatch does. */
 moe_status moe_ctx_set_node_dedup(moe_ctx* ctx, int32_t enable);
 
 /* Route every local card (moe_route_topk on its logits). */

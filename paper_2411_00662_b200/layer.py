@@ -222,7 +222,7 @@ class MoeLayer:
         check(self.lib.moe_ctx_experts(self._ctx, _stream_ptr(stream)))
 
     def set_node_dedup(self, enable: bool) -> None:
-        """EP-only: send a token's row once per remote node (fanned out there); False: once per (token, expert)."""
+        """Send a token's row (TP slice) once per remote node, fanned out there; False: once per (token, expert)."""
         check(self.lib.moe_ctx_set_node_dedup(self._ctx, int(bool(enable))))
 
     def set_expert_overlap(self, enable: bool) -> None:
