@@ -31,7 +31,7 @@ namespace {
 constexpr int kTokThreads = 256;
 constexpr int kTokMaxK = 16;
 
-template <int V, bool ND = false>
+template <int V, bool ND = false, bool FP8 = false>
 __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_constant__ TokArgs a) {
   using Vec = typename VecT<V>::type;
   constexpr int U = 64 / V > 4 ? 4 : (64 / V < 1 ? 1 : 64 / V);  // 16-byte vectors: 4 per lane (2 KiB pieces)
@@ -67,7 +67,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
           rcard = card;  // staged below, once per (token, card); the receiver writes the tags
         } else {
           dp = a.dst[card] + row * a.dst_stride;
-          if (a.fp8 && card / a.t != a.node) {
+          if (FP8 && card / a.t != a.node) {
             qp = a.dst_pre[card] + row * a.dst_stride;
             sp = a.dst_scale[card] + row * a.blocks_per_row;
           }
@@ -95,7 +95,7 @@ __global__ void __launch_bounds__(kTokThreads, 4) k_aa_token(const __grid_consta
       char* d = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(dp), s));
       const int o = __shfl_sync(0xffffffffu, off, s), e = __shfl_sync(0xffffffffu, end, s);
       if (!d || e <= piece_lo || o >= piece_hi) continue;  // warp-uniform
-      if constexpr (V == 16) {
+      if constexpr (V == 16 && FP8) {  // (the fp8 wire is an instantiation of its own: bf16 rows keep their registers)
         char* q = reinterpret_cast<char*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(qp), s));
         if (q) {  // warp-uniform: the fp8 wire for this cross-node leg
           float* sc = reinterpret_cast<float*>(__shfl_sync(0xffffffffu, reinterpret_cast<uintptr_t>(sp), s));
@@ -558,6 +558,11 @@ cudaError_t launch_aa_token(const TokArgs& a, int vec, int grid, cudaStream_t s)
   if (a.nslot) {  // node dedup (16-byte rows only)
     if (vec != 16) return cudaErrorNotSupported;
     k_aa_token<16, true><<<grid, kTokThreads, 0, s>>>(a);
+    return cudaGetLastError();
+  }
+  if (a.fp8) {  // the fp8 wire needs 16-byte bf16 rows (moe_ctx_set_wire checks the shape)
+    if (vec != 16) return cudaErrorNotSupported;
+    k_aa_token<16, false, true><<<grid, kTokThreads, 0, s>>>(a);
     return cudaGetLastError();
   }
   switch (vec) {
