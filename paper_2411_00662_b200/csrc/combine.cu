@@ -481,7 +481,7 @@ static bool unperm_rows_enabled() {
 // any k, 16-bit rows: CTA per token, sized so each round of U = 2 vectors
 // per thread covers the row in the fewest rounds of <= 160 threads, two
 // slots' loads in flight, <= 48 registers (8 CTAs of 160 threads per SM).
-// Measured on the N=1 DeepSeek layer (scripts/gpu_unperm_ab.sh): 100.8 us
+// Measured on the N=1 DeepSeek layer (MONTA_UNPERM_* A/B runs): 100.8 us
 // against 105.6 (U = 4, one slot, 64 registers), 106.3 (U = 2, one slot),
 // 101.6 (U = 2, three slots) and 113.8 for the warp-per-item k_unpermute;
 // 16 CTAs per SM of grid (8: same, one token per CTA: 104.2).
