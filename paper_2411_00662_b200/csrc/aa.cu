@@ -248,45 +248,122 @@ __global__ void __launch_bounds__(32) k_aa_bulk(const __grid_constant__ TokArgs 
   cta_signal(a.sig);
 }
 
-// Node dedup, sender pre-pass: thread per token; per remote node, the warp's
-// tokens that reach it claim consecutive staging slots with one atomic, and
-// each writes its descriptor {token id, position, k destination rows (-1:
-// not on that node), k experts} into the receiver's block for this node.
-__global__ void __launch_bounds__(256) k_node_slots(const __grid_constant__ NodeSlotArgs a) {
-  const int lane = threadIdx.x & 31;
-  const int64_t nthreads = int64_t(gridDim.x) * blockDim.x;
-  const int64_t Tr = (a.T + 31) / 32 * 32;
+// Node dedup, sender pre-pass (two launches, thread per token, 1024-token
+// blocks): k_node_count marks the tokens that reach each remote node and
+// counts them per block; k_node_slots gives each such token its staging slot
+// = earlier blocks' counts + its rank in the block — token order, so the TP
+// ranks of a node (same tokens, same routing) stage a token at the same slot
+// on their same-rank receivers, which lets the receivers exchange staged
+// slices (k_stage_ag) — and writes the descriptor {token id, position, its k
+// destination rows on that node (-1: elsewhere), the k experts} to the
+// receiver; the last block records the total in scount[card].
+__device__ __forceinline__ bool reaches(const NodeSlotArgs& a, int64_t i, int card) {
+  bool has = false;
+  for (int s = 0; s < a.k; ++s) {
+    const int x = __ldg(a.experts + i * a.k + s);
+    has |= x >= 0 && x < a.E && __ldg(a.table + x) == card;
+  }
+  return has;
+}
+
+__device__ __forceinline__ int block_rank(bool has, int* warp_tot, int* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const unsigned bal = __ballot_sync(0xffffffffu, has);
+  if (lane == 0) warp_tot[wid] = __popc(bal);
+  __syncthreads();
+  int before = 0, tot = 0;
+  for (int w = 0; w < nw; ++w) {
+    const int c = warp_tot[w];
+    before += w < wid ? c : 0;
+    tot += c;
+  }
+  __syncthreads();
+  *total = tot;
+  return before + __popc(bal & ((1u << lane) - 1u));
+}
+
+__global__ void __launch_bounds__(1024) k_node_count(const __grid_constant__ NodeSlotArgs a) {
+  __shared__ int warp_tot[32];
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int nb = gridDim.x;
+  for (int g = 0; g < a.e; ++g) {
+    if (g == a.node) continue;
+    const bool has = i < a.T && reaches(a, i, g * a.t + a.rho);
+    if (i < a.T) a.nslot[i * a.e + g] = has ? 0 : -1;
+    int tot;
+    block_rank(has, warp_tot, &tot);
+    if (threadIdx.x == 0) a.bcnt[g * nb + blockIdx.x] = tot;
+  }
+}
+
+__global__ void __launch_bounds__(1024) k_node_slots(const __grid_constant__ NodeSlotArgs a) {
+  __shared__ int warp_tot[32];
+  const int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int nb = gridDim.x;
   const int k = a.k, E = a.E;
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < Tr; i += nthreads) {
-    const bool active = i < a.T;
-    for (int g = 0; g < a.e; ++g) {
-      if (g == a.node) continue;
-      const int card = g * a.t + a.rho;  // node g's card of this rank's TP index
-      bool has = false;
-      if (active)
-        for (int s = 0; s < k; ++s) {
-          const int x = __ldg(a.experts + i * k + s);
-          has |= x >= 0 && x < E && __ldg(a.table + x) == card;
-        }
-      const unsigned bal = __ballot_sync(0xffffffffu, has);
-      if (!bal) continue;
-      int base = 0;
-      if (lane == 0) base = int(atomicAdd(a.scount + card, uint32_t(__popc(bal))));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (!has) continue;
-      const int slot = base + __popc(bal & ((1u << lane) - 1u));
-      a.nslot[i * a.e + g] = slot;
-      int32_t* d = a.sdesc[card] + int64_t(slot) * (2 + 2 * k);
-      d[0] = __ldg(a.token_ids + i);
-      d[1] = int32_t(i);
-      for (int s = 0; s < k; ++s) {
-        const int x = __ldg(a.experts + i * k + s);
-        const bool on = x >= 0 && x < E && __ldg(a.table + x) == card;
-        d[2 + s] = on ? __ldg(a.table + E + x) + __ldg(a.slot_pos + i * k + s) : -1;
-        d[2 + k + s] = x;
+  for (int g = 0; g < a.e; ++g) {
+    if (g == a.node) continue;
+    const int card = g * a.t + a.rho;
+    const bool has = i < a.T && __ldg(a.nslot + i * a.e + g) == 0;
+    int tot;
+    const int r = block_rank(has, warp_tot, &tot);
+    int base = 0, all = 0;
+    for (int b = 0; b < nb; ++b) {
+      const int c = __ldg(a.bcnt + g * nb + b);
+      base += b < int(blockIdx.x) ? c : 0;
+      all += c;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.scount[card] = uint32_t(all);
+    if (!has) continue;
+    const int slot = base + r;
+    a.nslot[i * a.e + g] = slot;
+    int32_t* d = a.sdesc[card] + int64_t(slot) * (2 + 2 * k);
+    d[0] = __ldg(a.token_ids + i);
+    d[1] = int32_t(i);
+    for (int s = 0; s < k; ++s) {
+      const int x = __ldg(a.experts + i * k + s);
+      const bool on = x >= 0 && x < E && __ldg(a.table + x) == card;
+      d[2 + s] = on ? __ldg(a.table + E + x) + __ldg(a.slot_pos + i * k + s) : -1;
+      d[2 + k + s] = x;
+    }
+  }
+}
+
+// Node dedup under TP, receiver: this rank's slice of every staged row goes
+// to the same rows of each TP peer's staging block (the peers hold the same
+// tokens at the same slots), so each card ends with whole staged rows and
+// fans them out itself — the AllGather moves one slice per (token, node)
+// instead of one per (token, expert).  Warp per (staged row, 2 KiB piece).
+__global__ void __launch_bounds__(256) k_stage_ag(const __grid_constant__ StageAgArgs a) {
+  constexpr int U = 4;
+  constexpr int kPieceVec = 32 * U;
+  const int lane = threadIdx.x & 31;
+  const int gx = int(gridDim.x) / a.nsend;  // one 1-D grid (cta_signal counts gridDim.x): sender = block / gx
+  const int y = int(blockIdx.x) / gx, bx = int(blockIdx.x) % gx;
+  const int64_t cnt = int64_t(*a.count[y]);
+  const int64_t v_lo = a.col_lo / 16, v_hi = a.col_hi / 16;
+  const int64_t pieces = (v_hi - v_lo + kPieceVec - 1) / kPieceVec;
+  const int64_t warps = int64_t(gx) * (blockDim.x / 32);
+  for (int64_t it = int64_t(bx) * (blockDim.x / 32) + (threadIdx.x >> 5); it < cnt * pieces; it += warps) {
+    const int64_t q = it / pieces;
+    const int64_t v0 = v_lo + (it % pieces) * kPieceVec;
+    const int4* src = reinterpret_cast<const int4*>(a.stage[y] + q * a.row_bytes);
+    int4 r[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t v = v0 + u * 32 + lane;
+      if (v < v_hi) r[u] = ld_stream_ef(src + v, l2_evict_first_policy());
+    }
+    for (int p = 0; p < a.npeer; ++p) {
+      int4* dst = reinterpret_cast<int4*>(a.peer_stage[p][y] + q * a.row_bytes);
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t v = v0 + u * 32 + lane;
+        if (v < v_hi) dst[v] = r[u];
       }
     }
   }
+  cta_signal(a.sig);
 }
 
 // Node dedup, receiver: warp per (staged row, 2 KiB piece) of every remote
@@ -500,10 +577,23 @@ static int env_int(const char* name, int dflt) {
 }
 
 cudaError_t launch_node_slots(const NodeSlotArgs& a, cudaStream_t s) {
-  if (a.T <= 0) return cudaSuccess;
-  const int64_t threads = (a.T + 31) / 32 * 32;
-  const int grid = int(std::min<int64_t>((threads + 255) / 256, 148 * 8));
-  k_node_slots<<<grid, 256, 0, s>>>(a);
+  if (a.T <= 0 || a.e < 2) return cudaSuccess;
+  const int nb = int((a.T + 1023) / 1024);
+  k_node_count<<<nb, 1024, 0, s>>>(a);
+  k_node_slots<<<nb, 1024, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_stage_ag(const StageAgArgs& a, int64_t max_rows, cudaStream_t s) {
+  if (a.nsend <= 0 || max_rows <= 0) return cudaSuccess;
+  if (a.row_bytes % 16 || a.col_lo % 16 || a.col_hi % 16) return cudaErrorNotSupported;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int64_t pieces = ((a.col_hi - a.col_lo) / 16 + 127) / 128;
+  const int64_t items = max_rows * pieces;
+  const int gx = int(std::max<int64_t>(1, std::min<int64_t>((items + 7) / 8, int64_t(sms) * 4 / a.nsend + 1)));
+  k_stage_ag<<<gx * a.nsend, 256, 0, s>>>(a);
   return cudaGetLastError();
 }
 

@@ -60,7 +60,7 @@ struct SlabLayout {
   size_t permuted, recv, recv_tags, pre, pre_tags, comb, out, count_table, flags, err, done;
   size_t lists, local_delta, recv_rows, recv_offs, tune, prow, rowpos, rowslot, dot, parts, gprobs, glogits, ones,
       wscale, cwire, cscale, scratch, epoch, front_done, dbg, tile_hist, tile_base, counts_acc, arrive,
-      ready, xchg_counters, xchg_flags, xtrace, aa_table, rowdst, stage, sdesc, scount, nslot, total;
+      ready, xchg_counters, xchg_flags, xtrace, aa_table, rowdst, stage, sdesc, scount, nslot, bcnt, total;
 };
 
 struct Card {
@@ -88,6 +88,7 @@ struct Card {
   int32_t* aa_table = nullptr;        // [4 + max_chunks][E] token-side AA destinations
   char** rowdst = nullptr;            // [recv_cap] reverse-AllToAll row address (peer comb) or null
   int32_t* nslot = nullptr;           // node dedup: [T][e] staging slot of (token, remote node), -1 none
+  int32_t* bcnt = nullptr;            //             [e][ceil(T / 1024)] per-block counts
   unsigned* front_done = nullptr;  // CTA election counter of the front kernel
   // layer backward scratch (moe_ctx_backward)
   void* prow = nullptr;
@@ -243,6 +244,7 @@ SlabLayout make_layout(const moe_ctx* c) {
   s.sdesc = take(nd ? size_t(d.e) * T * (2 + 2 * k) * 4 : 0);
   s.scount = take(size_t(kMaxCards) * 4);
   s.nslot = take(nd ? size_t(T) * d.e * 4 : 0);
+  s.bcnt = take(nd ? size_t(d.e) * ((T + 1023) / 1024) * 4 : 0);
   s.total = off;
   return s;
 }
@@ -302,6 +304,7 @@ void bind_card(moe_ctx* c, Card& cd) {
   cd.aa_table = reinterpret_cast<int32_t*>(b + s.aa_table);
   cd.rowdst = reinterpret_cast<char**>(b + s.rowdst);
   cd.nslot = reinterpret_cast<int32_t*>(b + s.nslot);
+  cd.bcnt = reinterpret_cast<int32_t*>(b + s.bcnt);
 }
 
 void set_peer(moe_ctx* c, int card, char* slab) {
@@ -1262,6 +1265,7 @@ moe_status dispatch_node_dedup(moe_ctx* c, Card& cd, int level, int landing, cud
   ns.rho = cd.rho;
   ns.scount = c->peer[cd.id].scount;
   ns.nslot = cd.nslot;
+  ns.bcnt = cd.bcnt;
   for (int g = 0; g < d.e; ++g)
     if (g != cd.node) {
       const int q = card_of(c, g, cd.rho);
@@ -1293,17 +1297,44 @@ moe_status dispatch_node_dedup(moe_ctx* c, Card& cd, int level, int landing, cud
     fa.source_card[i] = card_of(c, g, 0);  // the tag names the source node's first card (as the token kernel does)
   }
   fa.row_bytes = c->row_bytes;
-  fa.col_lo = dedup ? int64_t(cd.rho) * (c->row_bytes / d.t) : 0;
-  fa.col_hi = dedup ? fa.col_lo + c->row_bytes / d.t : c->row_bytes;
+  fa.col_lo = 0;
+  fa.col_hi = c->row_bytes;
   fa.k = d.top_k;
   fa.recv = static_cast<char*>(cd.v.recv);
   fa.recv_tags = cd.v.recv_tags;
+  if (dedup) {
+    // the staged rows carry this rank's slice; the TP peers staged the same
+    // tokens at the same slots (deterministic slots): exchange the slices at
+    // the staging level, then every card fans out whole rows
+    StageAgArgs ga{};
+    ga.nsend = fa.nsend;
+    for (int i = 0; i < fa.nsend; ++i) {
+      ga.stage[i] = fa.stage[i];
+      ga.count[i] = fa.count[i];
+    }
+    for (int r = 0; r < d.t; ++r) {
+      const int q = card_of(c, cd.node, r);
+      if (q == cd.id) continue;
+      int i = 0;
+      for (int g = 0; g < d.e; ++g)
+        if (g != cd.node) ga.peer_stage[ga.npeer][i++] = c->peer[q].stage + size_t(g) * d.tokens * c->row_bytes;
+      ++ga.npeer;
+    }
+    if (ga.npeer > 8) return fail(MOE_ERR_UNSUPPORTED, "node dedup: at most 9 TP ranks");
+    ga.row_bytes = c->row_bytes;
+    ga.col_lo = int64_t(cd.rho) * (c->row_bytes / d.t);
+    ga.col_hi = ga.col_lo + c->row_bytes / d.t;
+    ga.sig = no_signal();
+    ga.sig.epoch_ptr = cd.epoch_dev;
+    ga.sig.done = cd.done + kPsAG * d.max_chunks + 0;
+    for (int r = 0; r < d.t; ++r)
+      if (r != cd.rho) ga.sig.flags[ga.sig.n++] = flag_at(c, card_of(c, cd.node, r), sig_chunk(c, kPsAG, 0), cd.id);
+    MONTA_CUDA(launch_stage_ag(ga, d.tokens, s));
+    ++c->launches;
+    if (moe_status st4 = dispatch_tail_wait(c, cd, level, 1, landing, s)) return st4;  // the peers' slices
+  }
   MONTA_CUDA(launch_node_fanout(fa, d.tokens, 16, s));
   ++c->launches;
-  if (dedup) {  // forward this rank's landed slices to the node's TP peers, then wait for theirs
-    if (moe_status st3 = launch_ag(c, cd, 0, landing, s, false)) return st3;
-    if (moe_status st4 = dispatch_tail_wait(c, cd, level, 1, landing, s)) return st4;
-  }
   return MOE_OK;
 }
 

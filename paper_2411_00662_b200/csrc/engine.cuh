@@ -146,8 +146,9 @@ struct NodeSlotArgs {
   const int32_t* table;      // aa_table: [0, E) card, [E, 2E) row base
   int64_t T;
   int32_t E, k, e, t, node, rho;
-  uint32_t* scount;          // this card's [kMaxCards] staged-row counters (zeroed per dispatch)
-  int32_t* nslot;            // [T][e]
+  uint32_t* scount;          // this card's [kMaxCards] staged-row counts
+  int32_t* nslot;            // [T][e] staging slot, or -1
+  int32_t* bcnt;             // [e][ceil(T / 1024)] per-block counts (deterministic slot scan)
   int32_t* sdesc[kMaxCards]; // each card's descriptor block for this node
 };
 cudaError_t launch_node_slots(const NodeSlotArgs& a, cudaStream_t s);
@@ -164,6 +165,16 @@ struct FanoutArgs {
   int32_t* recv_tags;
 };
 cudaError_t launch_node_fanout(const FanoutArgs& a, int64_t max_rows, int vec, cudaStream_t s);
+struct StageAgArgs {
+  int32_t nsend;                          // remote sender nodes
+  int32_t npeer;                          // TP peers of this card
+  const char* stage[kMaxCards];           // this card's staging block of sender i
+  char* peer_stage[8][kMaxCards];         // [peer][sender i]: the same block on TP peer p (t <= 9)
+  const uint32_t* count[kMaxCards];       // rows sender i staged (to this card and, equally, to the peers)
+  int64_t row_bytes, col_lo, col_hi;      // this rank's slice of a staged row
+  SignalList sig;
+};
+cudaError_t launch_stage_ag(const StageAgArgs& a, int64_t max_rows, cudaStream_t s);
 // Fused combine (experts.cu + ctx.cu): rowdst[r] = the address of final-layout
 // row r's reverse-AllToAll destination row (a peer's comb) from the CAA lists
 // of chunks [0, n), null for rows that stay on this node.
