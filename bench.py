@@ -848,6 +848,25 @@ def main():
                         "frac": nvlink["dispatch"]["gbs"] / NVLINK_PEAK_GBS, "traffic": None,
                         "algorithmic_bytes_per_launch": nvlink["dispatch"]["bytes"],
                         "peak_kind": "B200_PROFILING.md measured peer copy per direction"}
+        elif nvlink["combine"]["gbs"]:
+            # the node-dedup dispatch (per-launch kernels, no role traces) moves
+            # fewer bytes than the per-(token, expert) legs above; the combine
+            # runs the persistent kernel, whose reverse-AllToAll leg is timed
+            roofline = {"bound": "nvlink", "kernel": "k_combine_xchg (persistent combine: reverse AllToAll leg)",
+                        "achieved": nvlink["legs"]["caa"]["gbs"] or nvlink["combine"]["gbs"],
+                        "peak": NVLINK_PEAK_GBS, "unit": "GB/s",
+                        "frac": (nvlink["legs"]["caa"]["gbs"] or nvlink["combine"]["gbs"]) / NVLINK_PEAK_GBS,
+                        "traffic": None, "algorithmic_bytes_per_launch": nvlink["legs"]["caa"]["bytes"],
+                        "peak_kind": "B200_PROFILING.md measured peer copy per direction",
+                        "note": "dispatch: node dedup (one row per (token, remote node)); its legs are not traced"}
+        elif "caa" in stages and stages["caa"]["sum_us_per_step"] > 0:
+            # per-launch combine (unchunked EP-only): the reverse AllToAll launch's in-graph span
+            gbs = nvlink["legs"]["caa"]["bytes"] / stages["caa"]["sum_us_per_step"] / 1e3
+            roofline = {"bound": "nvlink", "kernel": "k_seg_copy (combine reverse AllToAll launch)",
+                        "achieved": gbs, "peak": NVLINK_PEAK_GBS, "unit": "GB/s", "frac": gbs / NVLINK_PEAK_GBS,
+                        "traffic": None, "algorithmic_bytes_per_launch": nvlink["legs"]["caa"]["bytes"],
+                        "peak_kind": "B200_PROFILING.md measured peer copy per direction",
+                        "note": "dispatch: node dedup (one row per (token, remote node)); its legs are not traced"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.quick:
