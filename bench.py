@@ -612,6 +612,10 @@ def main():
         cands = [(level, n, landing)]
         if (int(decision.level), rn) != (level, n):
             cands.append((int(decision.level), rn, landing))
+        if t > 1 and all(c[0] != BASELINE for c in cands):
+            # the naive exchange too: with few experts per node (Mixtral, 2x70B)
+            # the TP-redundant rows cost less than the AllGather round
+            cands.append((BASELINE, 1, LAND_FINAL))
         if len(cands) > 1:
             best, times = layer.autotune(cands, steps=5, stream=stream)
             autotune = {"candidates": [[_lib.LEVEL_NAMES[c[0]], c[1], us] for c, us in zip(cands, times)],
