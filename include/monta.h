@@ -358,9 +358,10 @@ moe_status moe_ctx_set_expert_overlap(moe_ctx* ctx, int32_t enable);
  * (this rank's 1/t slice under TP) crosses to a remote node once, however
  * many of its experts live there, into a staging block the receiving card
  * fans out to the experts' rows before the AllGather (the recv layout and
- * tags are the plain dispatch's, row for row).  Default on; 0 sends one row
- * per (token, expert) as the reference's dispatch does. */
-moe_status moe_ctx_set_node_dedup(moe_ctx* ctx, int32_t enable);
+ * tags are the plain dispatch's, row for row).  mode 0: one row per (token,
+ * expert) as the reference's dispatch does; 1: node dedup; 2 (default):
+ * node dedup when top_k >= 2 e (a token reaches ~k/e experts per node). */
+moe_status moe_ctx_set_node_dedup(moe_ctx* ctx, int32_t mode);
 
 /* Route every local card (moe_route_topk on its logits). */
 moe_status moe_ctx_route(moe_ctx* ctx, void* stream);

@@ -221,9 +221,9 @@ class MoeLayer:
     def experts(self, stream=None) -> None:
         check(self.lib.moe_ctx_experts(self._ctx, _stream_ptr(stream)))
 
-    def set_node_dedup(self, enable: bool) -> None:
-        """Send a token's row (TP slice) once per remote node, fanned out there; False: once per (token, expert)."""
-        check(self.lib.moe_ctx_set_node_dedup(self._ctx, int(bool(enable))))
+    def set_node_dedup(self, mode: int) -> None:
+        """Cross-node rows once per (token, remote node), fanned out there: 0 off, 1 on, 2 auto (k >= 2e)."""
+        check(self.lib.moe_ctx_set_node_dedup(self._ctx, int(mode)))
 
     def set_expert_overlap(self, enable: bool) -> None:
         """Fuse the reverse AllToAll into the experts' down-projection epilogue (multi-GPU forward)."""

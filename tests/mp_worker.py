@@ -47,7 +47,7 @@ def main():
     ap.add_argument("--persistent", type=int, default=1)
     ap.add_argument("--ffn", type=int, default=0)  # > 0: SwiGLU experts of this size bound on every card
     ap.add_argument("--host", type=int, default=0)  # 1: also forward_host (pipelined host copies) vs forward
-    ap.add_argument("--node-dedup", type=int, default=1)  # 0: one row per (token, expert) across nodes
+    ap.add_argument("--node-dedup", type=int, default=1)  # 0 off, 1 on (the tests' default), 2 auto
     a = ap.parse_args()
     rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
     local = int(os.environ.get("LOCAL_RANK", rank))
@@ -67,7 +67,7 @@ def main():
     layer.connect()
     layer.enable_graphs(bool(a.graphs))
     layer.set_persistent(bool(a.persistent))
-    layer.set_node_dedup(bool(a.node_dedup))
+    layer.set_node_dedup(a.node_dedup)
     cd = layer.cards[0]
     node = cd.node
     g = torch.Generator().manual_seed(a.seed * 1000 + node)
