@@ -1247,7 +1247,8 @@ bool node_dedup_ok(const moe_ctx* c, int level, int n, int landing) {
   const bool want = c->node_dedup == 1 || (c->node_dedup == 2 && d.top_k >= 2 * d.e);
   return env != 0 && want && !is_virtual(c) && d.e > 1 && n == 1 && landing == MOE_LAND_FINAL &&
          c->wire == MOE_WIRE_BF16 && !c->pace_bpus && c->aa_ctas == 0 && d.top_k <= 16 && c->row_bytes % 16 == 0 &&
-         c->local.size() == 1;  // (the staging regions exist exactly when t == 1, e > 1 and world > 1)
+         (c->row_bytes / d.t) % 16 == 0 && d.t <= 9 &&  // 16-byte slices; k_stage_ag's peer table
+         c->local.size() == 1;  // (the staging regions exist exactly when e > 1 and world > 1)
 }
 
 moe_status dispatch_node_dedup(moe_ctx* c, Card& cd, int level, int landing, cudaStream_t s) {
