@@ -363,9 +363,17 @@ __global__ void __launch_bounds__(front_threads(G, PER)) k_front(const __grid_co
       int* hc = W + E;  // [2][E] chunk parts (unaligned only)
       for (int i = tid; i < 3 * E; i += blockDim.x) W[i] = 0;
       if (a.route) {
-        for (int64_t r0 = i0; r0 < i1; r0 += front_threads(G, PER) / G)
-          route_tokens<T, G, PER>(static_cast<const T*>(a.logits), i1, E, k, a.experts, static_cast<T*>(a.probs),
-                                  r0 + tid / G, single ? s_exp : nullptr, i0);
+        constexpr int kPass = front_threads(G, PER) / G;  // tokens per pass of the CTA
+        if constexpr (sizeof(T) == 4 && G == 32 && PER <= 5) {  // two tokens per warp per pass (E <= 160: no spills)
+          for (int64_t r0 = i0; r0 < i1; r0 += 2 * kPass)
+            route_tokens_w32x2<PER>(reinterpret_cast<const float*>(a.logits), i1, E, k, a.experts,
+                                    reinterpret_cast<float*>(a.probs), r0 + tid / G, r0 + kPass + tid / G,
+                                    single ? s_exp : nullptr, i0);
+        } else {
+          for (int64_t r0 = i0; r0 < i1; r0 += kPass)
+            route_tokens<T, G, PER>(static_cast<const T*>(a.logits), i1, E, k, a.experts, static_cast<T*>(a.probs),
+                                    r0 + tid / G, single ? s_exp : nullptr, i0);
+        }
       } else if (single) {
         for (int q = tid; q < np; q += blockDim.x) s_exp[q] = a.experts[i0 * k + q];
       }

@@ -245,6 +245,114 @@ __device__ __forceinline__ void route_tokens(const T* __restrict__ logits, int64
   }
 }
 
+// Two tokens per warp (fp32 scores, whole-warp groups): the arithmetic of
+// route_tokens for token a and token b, interleaved so the dependent
+// reduction chains of the two overlap (the router is issue-latency bound:
+// ~65 % issue slots busy with one token per warp).  Bit-identical per token.
+template <int PER>
+__device__ __forceinline__ void route_tokens_w32x2(const float* __restrict__ logits, int64_t T_tokens, int E, int k,
+                                                   int32_t* __restrict__ experts, float* __restrict__ probs,
+                                                   int64_t tok_a, int64_t tok_b, int* s_exp, int64_t s_base) {
+  constexpr int G = 32;
+  const int lane = threadIdx.x & (kWarp - 1);
+  const int64_t tok[2] = {tok_a, tok_b};
+  bool active[2];
+  unsigned u[2][PER];
+  float ex[2][PER];
+  float sum[2];
+  float vv[2][PER];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    active[q] = tok[q] < T_tokens;
+    const float* row = logits + (active[q] ? tok[q] : 0) * int64_t(E);
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int x = lane + m * G;
+      vv[q][m] = (active[q] && x < E) ? row[x] : -INFINITY;
+    }
+  }
+  unsigned lmax[2] = {0u, 0u};
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      const int x = lane + m * G;
+      unsigned b = __float_as_uint(vv[q][m]);
+      b = (b == 0x80000000u) ? 0u : b;
+      u[q][m] = x < E ? ((b & 0x80000000u) ? ~b : (b | 0x80000000u)) : 0u;
+      lmax[q] = u[q][m] > lmax[q] ? u[q][m] : lmax[q];
+    }
+  float mx[2];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const unsigned mkey = __reduce_max_sync(0xffffffffu, lmax[q]);
+    mx[q] = __uint_as_float((mkey & 0x80000000u) ? (mkey & 0x7fffffffu) : ~mkey);
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    sum[q] = 0.f;
+#pragma unroll
+    for (int m = 0; m < PER; ++m) {
+      ex[q][m] = dev_exp<float>(vv[q][m] - mx[q]);
+      sum[q] += ex[q][m];
+    }
+  }
+#pragma unroll
+  for (int off = G / 2; off > 0; off >>= 1) {
+    sum[0] += __shfl_xor_sync(0xffffffffu, sum[0], off, G);
+    sum[1] += __shfl_xor_sync(0xffffffffu, sum[1], off, G);
+  }
+  int my_w[2] = {-1, -1};
+  float my_e[2] = {0.f, 0.f};
+  for (int s = 0; s < k; ++s) {
+    unsigned key[2], bm[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      key[q] = 0u;
+      bm[q] = 0u;
+#pragma unroll
+      for (int m = 0; m < PER; ++m)
+        if (u[q][m] > key[q]) {
+          key[q] = u[q][m];
+          bm[q] = unsigned(m);
+        }
+    }
+    unsigned wi[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const unsigned bi = key[q] ? unsigned(lane) + bm[q] * G : 0xffffffffu;
+      const unsigned mk = __reduce_max_sync(0xffffffffu, key[q]);
+      wi[q] = __reduce_min_sync(0xffffffffu, key[q] == mk ? bi : 0xffffffffu);
+    }
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      const unsigned mw = wi[q] / G, owner = wi[q] % G;
+      float e = 0.f;
+#pragma unroll
+      for (int m = 0; m < PER; ++m)
+        if (unsigned(m) == mw) {
+          e = ex[q][m];
+          if (owner == unsigned(lane)) u[q][m] = 0u;
+        }
+      e = __shfl_sync(0xffffffffu, e, int(owner));
+      if (lane == s) {
+        my_w[q] = int(wi[q]);
+        my_e[q] = e;
+      }
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    int slot = 0;
+    for (int s = 0; s < k; ++s) slot += __shfl_sync(0xffffffffu, my_w[q], s) < my_w[q] ? 1 : 0;
+    if (active[q] && lane < k) {
+      experts[tok[q] * k + slot] = my_w[q];
+      probs[tok[q] * k + slot] = my_e[q] / sum[q];
+      if (s_exp) s_exp[(tok[q] - s_base) * k + slot] = my_w[q];
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Index build by one CTA (any warp count).  smem layout (ints):
 //   hist [nw][E] | offs [E+1] | ccount [n][E] (when count_in_smem)
